@@ -1,0 +1,96 @@
+"""Literal definitions used to pin the oracle (tests only).
+
+Independent of oracle/ppipe_oracle.c: candidates are enumerated with
+itertools straight from the paper's definitions, and the frontier is the
+literal O(n^2) non-domination test (SURVEY.md §8(c) pin P8), not a sort+scan.
+"""
+from __future__ import annotations
+
+import itertools
+from fractions import Fraction
+
+import numpy as np
+
+
+def t_eff(slo_us: int, margin_permille: int) -> int:
+    # "deduct ... margin from the SLO", floor to integer us (reading A5)
+    return (int(slo_us) * (1000 - int(margin_permille))) // 1000
+
+
+def enumerate_candidates(w, m: int, slo_us=None):
+    """All candidates of model m: dict segment(K, cls) -> list of candidate dicts."""
+    mp = w.models[m]
+    lat = mp.lat_us.astype(object)
+    S = [int(x) for x in mp.act_bytes]
+    C, M, B = mp.lat_us.shape
+    T = t_eff(w.slo_us[m] if slo_us is None else slo_us, w.margin_permille)
+    out = {}
+    n_cand = 0
+    for K in range(1, min(w.kmax, M) + 1):
+        for cuts in itertools.combinations(range(1, M), K - 1):
+            bounds = (0,) + cuts + (M,)
+            for cls in itertools.product(range(C), repeat=K):
+                for bi in range(B):
+                    b = int(w.batches[bi])
+                    stages = [sum(int(lat[cls[d], l, bi]) for l in range(bounds[d], bounds[d + 1]))
+                              for d in range(K)]
+                    trans = [-(-8 * S[bounds[d + 1] - 1] * b // int(w.bw[cls[d], cls[d + 1]]))
+                             for d in range(K - 1)]
+                    E = sum(stages) + sum(trans)
+                    n_cand += 1
+                    if E > T:
+                        continue
+                    out.setdefault((K, cls), []).append(
+                        dict(E=E, b=b, cmax=max(stages), cuts=tuple(cuts) + (0,) * (2 - len(cuts)),
+                             stages=stages, trans=trans))
+    return out, n_cand
+
+
+def theta(c):
+    return Fraction(c["b"], c["cmax"]) if c["cmax"] > 0 else Fraction(10**30)
+
+
+def literal_frontier(cands):
+    """Keep p iff no q dominates it: q has E_q <= E_p and theta_q >= theta_p, and either
+    is strictly better in one objective, or equal in both and canonically smaller
+    (batch, then cuts) -- reading A1 / A17."""
+    keep = []
+    for p in cands:
+        tp = theta(p)
+        dominated = False
+        for q in cands:
+            if q is p:
+                continue
+            tq = theta(q)
+            if q["E"] <= p["E"] and tq >= tp:
+                if q["E"] < p["E"] or tq > tp:
+                    dominated = True
+                    break
+                if (q["b"], q["cuts"]) < (p["b"], p["cuts"]):
+                    dominated = True
+                    break
+        if not dominated:
+            keep.append(p)
+    keep.sort(key=lambda c: c["E"])
+    return keep
+
+
+def literal_frontier_np(cands):
+    """Same literal O(n^2) definition, vectorised with numpy for a few thousand points."""
+    if not cands:
+        return []
+    E = np.array([c["E"] for c in cands], dtype=np.int64)
+    b = np.array([c["b"] for c in cands], dtype=np.int64)
+    cm = np.array([c["cmax"] for c in cands], dtype=np.int64)
+    key = np.array([(c["b"] << 32) | (c["cuts"][0] << 16) | c["cuts"][1] for c in cands], dtype=np.int64)
+    keep = []
+    for i in range(len(cands)):
+        # theta_q >= theta_p  <=>  b_q * cm_p >= b_p * cm_q
+        ge = b * cm[i] >= b[i] * cm
+        gt = b * cm[i] > b[i] * cm
+        dom = (E <= E[i]) & ge & ((E < E[i]) | gt | (key < key[i]))
+        dom[i] = False
+        if not dom.any():
+            keep.append(cands[i])
+    keep.sort(key=lambda c: c["E"])
+    return keep
