@@ -1,0 +1,184 @@
+/*
+ * ppipe.h -- C ABI of the B200-native PPipe plan-enumeration library
+ * (libppipe_b200.so, built from paper_2507_18748_b200/csrc/).
+ *
+ * The library computes the data-parallel hot path of PPipe's control plane
+ * (arXiv 2507.18748, "PPipe: Efficient Video Analytics Serving on Heterogeneous
+ * GPU Clusters via Pool-Based Pipeline Parallelism"): for every model, every
+ * well-formed split into K <= 3 contiguous partitions, every assignment of a GPU
+ * class to each partition and every unified batch size, it scores the pooled
+ * pipeline candidate and reduces the feasible ones to a per-(model, K, class
+ * tuple) latency/throughput Pareto frontier -- the candidate set PPipe's MILP
+ * picks from (its p_{ldbij} = 1 configurations, App. A.1;
+ * PAPER.md:2365-2391, App. A.2).
+ *
+ * Definitions (all integer; DESIGN.md §2 lists every reading of the paper):
+ *   partitions      c_0 = 0 < c_1 < ... < c_{K-1} < c_K = M; partition d covers
+ *                   layers [c_{d-1}, c_d)           eqs. 1.1-1.5
+ *   stage latency   C_d = sum_{l in partition d} lat_us[k_d][l][b]
+ *                                                   C_{ldbij}, eq. 1.9
+ *   transfer        Y_d = ceil(8 * act_bytes[c_d - 1] * b / bw[k_d][k_{d+1}])  for d < K
+ *                                                   Y_{bj}, eq. 1.11
+ *   E2E latency     E = sum_d C_d + sum_d Y_d        eq. 1.12
+ *   feasible        E <= T_eff = floor(slo_us * (1000 - margin_permille) / 1000)
+ *                                                   PAPER.md:1386-1394 (§5.4), 1690-1693 (§7.1)
+ *   throughput      theta = b / max_d C_d (exact rational; max = 0 reads as +inf)
+ *                                                   X = b / C, x_l = min_d x_ld
+ *   frontier        per segment (model, K, k_1..k_K): feasible points not
+ *                   dominated in (E min, theta max); among identical (E, theta)
+ *                   the smallest batch, then the smallest (c_1, c_2) is kept.
+ *
+ * Conventions: every function returns PPIPE_OK (0) or a negative PPIPE_E*
+ * code; nothing aborts and no C++ exception crosses the ABI. On error,
+ * ppipe_last_error() returns a message naming the offending item. All input
+ * pointers are host pointers owned by the caller and only read during the call.
+ * Output arrays are owned by the context and stay valid until the next
+ * ppipe_enumerate / ppipe_pareto on it or ppipe_free. One context per rank
+ * (one process per GPU); calls on one context are not thread-safe. There is no
+ * CPU fallback: without a usable sm_100 device every compute call returns
+ * PPIPE_ECUDA.
+ */
+#ifndef PPIPE_H
+#define PPIPE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PPIPE_OK = 0,
+  PPIPE_EINVAL = -1, /* malformed input (sizes, ordering, zero bandwidth, bad K, margin >= 1000, NULL) */
+  PPIPE_ERANGE = -2, /* input outside the exact-int32 envelope (see ppipe_load_profiles) */
+  PPIPE_ENOMEM = -3, /* host or device allocation failed */
+  PPIPE_ECUDA = -4,  /* CUDA runtime error, or no sm_100 device */
+  PPIPE_ENCCL = -5,  /* NCCL unavailable or failed (world > 1 only) */
+  PPIPE_ESTATE = -6  /* call out of order, e.g. ppipe_pareto before ppipe_enumerate */
+};
+
+typedef struct ppipe_ctx ppipe_ctx; /* opaque; owns all host and device memory it returns */
+
+/* One model's profile (Table "Inputs to the MILP").
+ * lat_us    [n_classes][n_layers][n_batches], row-major, integer microseconds, >= 0
+ *           (L_{kbi}: latency of layer i at batch b on class k).
+ * act_bytes [n_layers]: bytes ON THE WIRE of layer l's output at batch 1 (S_l;
+ *           the caller halves fp32 sizes when quantising to fp16). */
+typedef struct {
+  uint32_t n_layers; /* M, 1..65535 (cuts are stored as u16) */
+  const uint32_t *lat_us;
+  const uint64_t *act_bytes;
+} ppipe_model;
+
+/* Multi-GPU placement: one process per GPU. The enumeration space is split by
+ * first-cut rows (contiguous (model, c_1) ranges of equal candidate weight);
+ * local frontiers are merged with an NCCL all-gather and one final frontier pass. */
+typedef struct {
+  int32_t rank;           /* 0..world-1 */
+  int32_t world;          /* >= 1 */
+  int32_t device;         /* CUDA device ordinal for this rank; -1 = current device */
+  const void *nccl_id;    /* 128-byte ncclUniqueId from ppipe_nccl_unique_id() on rank 0. NULL with
+                             world > 1 = shard mode: no NCCL, ppipe_pareto returns this rank's LOCAL
+                             frontier (exact over its rows; the union of all ranks' local frontiers
+                             reduces to the global one by one more frontier pass) */
+} ppipe_dist;
+
+/* Validate, copy and upload the profiles this rank needs (host -> device).
+ *   n_classes        1..8
+ *   batches          [n_batches] batch VALUES, strictly increasing, 1..65535 (n_batches 1..65535)
+ *   bw_bits_per_us   [n_classes][n_classes] effective bandwidth sender -> receiver in
+ *                    bits/us (= Mbit/s), every entry >= 1 (1/5 of NIC rate)
+ *   dist             NULL => single GPU, current device
+ * Errors: PPIPE_EINVAL (NULLs, M = 0 or > 65535, n_classes, batch list, bw = 0);
+ *         PPIPE_ERANGE (any whole-model latency sum at (class, batch) >= 2^28 us, or
+ *         8 * act_bytes * max batch >= 2^63); PPIPE_ECUDA / PPIPE_ENOMEM / PPIPE_ENCCL.
+ * On error *out is NULL and ppipe_last_error(NULL) holds the message. */
+int ppipe_load_profiles(ppipe_ctx **out, uint32_t n_models, const ppipe_model *models, uint32_t n_classes,
+                        uint32_t n_batches, const uint32_t *batches, const uint32_t *bw_bits_per_us,
+                        const ppipe_dist *dist);
+
+typedef struct {
+  uint32_t max_partitions;  /* Kmax, 1..3 */
+  const uint32_t *slo_us;   /* [n_models] raw latency SLO T per model, microseconds */
+  uint32_t margin_permille; /* 0..999 deducted from the SLO; paper default 400 */
+} ppipe_enum_params;
+
+/* Replace the profile values of an existing context (same model count and
+ * layer counts, same classes and batches): validate and copy host -> device.
+ * Profiles change as workloads drift and the planner re-runs;
+ * this keeps the device buffers and the NCCL communicator. Errors as for
+ * ppipe_load_profiles. Invalidates the last ppipe_enumerate. */
+int ppipe_update_profiles(ppipe_ctx *ctx, uint32_t n_models, const ppipe_model *models);
+
+/* Enqueue the whole enumeration on the context's stream: pack (prefix sums,
+ * transfer tables, T_eff), then score every candidate of this rank's range and
+ * fold feasible ones into per-(segment, batch) survivor sets. Asynchronous;
+ * results are read through ppipe_pareto. Errors: PPIPE_EINVAL (Kmax, margin),
+ * PPIPE_ERANGE (T_eff >= 2^28), PPIPE_ECUDA. */
+int ppipe_enumerate(ppipe_ctx *ctx, const ppipe_enum_params *params);
+
+/* One frontier point: 32 bytes, 4-byte aligned, little-endian. */
+typedef struct {
+  uint32_t model;       /* model index in the ppipe_load_profiles array */
+  uint16_t cut[2];      /* c_1, c_2; 0 when unused */
+  uint8_t K;            /* number of partitions, 1..3 */
+  uint8_t cls[3];       /* k_d for d < K; 0xFF when unused */
+  uint16_t batch;       /* batch VALUE b */
+  uint16_t reserved;    /* 0 */
+  uint32_t e2e_us;      /* E */
+  uint32_t stage_us[3]; /* C_1..C_K; 0 when unused. max = bottleneck latency; E - sum = transfers */
+} ppipe_point;
+
+typedef struct {
+  uint64_t n_candidates;  /* all ranks: sum_m sum_K C(M-1, K-1) * C^K * B */
+  uint64_t n_feasible;    /* all ranks: candidates with E <= T_eff */
+  uint64_t n_points;      /* frontier points */
+  uint64_t n_segments;    /* sum_m sum_{K <= min(Kmax, M)} C^K, canonical order (m, K, tuple lexicographic) */
+  const ppipe_point *points;     /* host copy, NULL unless copy_to_host */
+  const uint64_t *seg_offsets;   /* host [n_segments + 1] CSR, NULL unless copy_to_host */
+  const ppipe_point *d_points;   /* device (this rank's GPU), same content */
+  const uint64_t *d_seg_offsets; /* device [n_segments + 1] */
+  uint64_t n_survivors;   /* diagnostics: this rank's pre-frontier survivor count */
+  uint64_t n_candidates_local; /* this rank's share of n_candidates */
+  uint64_t n_feasible_local;   /* this rank's share of n_feasible */
+} ppipe_frontier;
+
+/* Reduce the survivors to the exact frontier on device (sort + staircase
+ * scan), merge across ranks (world > 1: NCCL all-gather + final pass; the
+ * result is replicated on every rank), optionally copy to host, and block until
+ * done. Errors: PPIPE_ESTATE (no prior ppipe_enumerate), PPIPE_ECUDA, PPIPE_ENCCL. */
+int ppipe_pareto(ppipe_ctx *ctx, int copy_to_host, ppipe_frontier *out);
+
+/* Free everything the context owns. NULL-safe. */
+void ppipe_free(ppipe_ctx *ctx);
+
+/* Last error message: for ctx == NULL, the calling thread's last failed load. */
+const char *ppipe_last_error(const ppipe_ctx *ctx);
+
+/* ---- helpers (not part of the four-call path) ---- */
+
+/* Write a fresh 128-byte ncclUniqueId into out (call on rank 0, broadcast it). */
+int ppipe_nccl_unique_id(void *out128);
+
+/* The CUDA stream (cudaStream_t) all of ctx's work is enqueued on. */
+void *ppipe_stream(ppipe_ctx *ctx);
+
+/* Device time (ms) of the last ppipe_enumerate's launches, measured with CUDA
+ * events on ctx's stream: [0] pack, [1] score (dominant kernel), [2] frontier
+ * (sort + scan), [3] merge (all-gather + final pass). Valid after ppipe_pareto. */
+int ppipe_phase_ms(ppipe_ctx *ctx, float out_ms[4]);
+
+/* Number of kernel launches the last enumerate + pareto issued (for bench accounting). */
+uint64_t ppipe_launch_count(ppipe_ctx *ctx);
+
+/* Host-only: this rank's first-cut row range per model under the row partition
+ * (see ppipe_dist). rows[2*m] = lo, rows[2*m+1] = hi (half-open; row 0 = the K=1
+ * candidates, row r >= 1 = candidates whose first cut c_1 = r). Returns
+ * PPIPE_OK. Usable without a GPU. */
+int ppipe_partition_rows(uint32_t n_models, const uint32_t *n_layers, uint32_t n_classes, uint32_t n_batches,
+                         uint32_t max_partitions, int32_t rank, int32_t world, uint32_t *rows);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PPIPE_H */

@@ -126,7 +126,7 @@ typedef struct {
   int Kmax;
   int only_K;               /* 0 = all */
   const uint8_t *only_cls;  /* NULL = all tuples */
-  int32_t row_lo, row_hi;   /* first-cut rows for K>=2 sampling; row_hi <= 0 = all */
+  int32_t row_lo, row_hi;   /* row sample [row_lo, row_hi): row 0 = K=1, row r>=1 = first cut r; row_hi <= 0 = all */
   uint32_t nseg[4];         /* C^K */
   /* hoisted direct quantities */
   int64_t *pre;  /* pre[c][k][b]  = sum_{l<c} lat[k][l][b]   for c=0..M, by direct summation */
@@ -253,12 +253,12 @@ static void *worker_main(void *arg) {
     pthread_mutex_unlock(&pb->mu);
     /* row 0: K=1 (no cuts). row r in 1..M-1: K=2 and K=3 with first cut c_1 = r. */
     if (r >= M) break;
+    int in_sample = pb->row_hi <= 0 || (r >= pb->row_lo && r < pb->row_hi);
+    if (!in_sample) continue;
     if (r == 0) {
       do_row(w, 1, -1);
       continue;
     }
-    int in_sample = pb->row_hi <= 0 || (r >= pb->row_lo && r < pb->row_hi);
-    if (!in_sample) continue;
     if (pb->Kmax >= 2) do_row(w, 2, r);                /* c_1 in [1, M-1] */
     if (pb->Kmax >= 3 && r <= M - 2) do_row(w, 3, r);  /* c_1 < c_2 <= M-1 */
   }
@@ -288,8 +288,9 @@ void oracle_result_free(oracle_result *r) {
 
 /*
  * Enumerate models [model_lo, model_hi), all K <= Kmax (or only_K), all tuples
- * (or only_cls). row_lo/row_hi restrict the first cut of K>=2 candidates
- * (sampling for timing; row_hi <= 0 disables). Returns 0 on success.
+ * (or only_cls). row_lo/row_hi restrict the enumeration to rows [row_lo, row_hi)
+ * where row 0 holds the K=1 candidates and row r >= 1 the candidates with first
+ * cut c_1 = r (sampling and rank shards; row_hi <= 0 disables). Returns 0 on success.
  */
 int oracle_run(uint32_t n_models, const oracle_model *models, uint32_t n_classes, uint32_t n_batches,
                const uint32_t *batches, const uint32_t *bw, uint32_t kmax, const uint32_t *slo_us,

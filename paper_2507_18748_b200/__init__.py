@@ -1,0 +1,23 @@
+"""B200-native PPipe plan enumeration (arXiv 2507.18748): the data-parallel hot
+path of PPipe's control plane -- exhaustive enumeration and scoring of
+pool-based pipeline plans and their reduction to a per-(model, K, class tuple)
+Pareto frontier -- as hand-written sm_100a CUDA kernels behind a C ABI
+(include/ppipe.h). See DESIGN.md.
+"""
+from ._binding import (  # noqa: F401
+    POINT_DTYPE,
+    Context,
+    Frontier,
+    PPipeError,
+    enumerate,
+    free,
+    load_profiles,
+    load_workload,
+    nccl_unique_id,
+    pareto,
+    partition_rows,
+    run,
+    update_profiles,
+    lib,
+    LIB_PATH,
+)

@@ -1,0 +1,238 @@
+"""Thin ctypes binding of libppipe_b200.so (include/ppipe.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+CUDA kernels. Same names as the C ABI: load_profiles, enumerate, pareto, free.
+There is no CPU fallback: if the library is missing or no sm_100 device is
+usable, calls raise PPipeError.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libppipe_b200.so")
+
+PPIPE_OK, PPIPE_EINVAL, PPIPE_ERANGE, PPIPE_ENOMEM, PPIPE_ECUDA, PPIPE_ENCCL, PPIPE_ESTATE = 0, -1, -2, -3, -4, -5, -6
+_CODES = {-1: "EINVAL", -2: "ERANGE", -3: "ENOMEM", -4: "ECUDA", -5: "ENCCL", -6: "ESTATE"}
+
+# ppipe_point, 32 bytes (include/ppipe.h)
+POINT_DTYPE = np.dtype([
+    ("model", "<u4"), ("cut", "<u2", (2,)), ("K", "u1"), ("cls", "u1", (3,)),
+    ("batch", "<u2"), ("reserved", "<u2"), ("e2e_us", "<u4"), ("stage_us", "<u4", (3,)),
+])
+assert POINT_DTYPE.itemsize == 32
+
+
+class PPipeError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_CODES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class _Model(ct.Structure):
+    _fields_ = [("n_layers", ct.c_uint32), ("lat_us", ct.POINTER(ct.c_uint32)),
+                ("act_bytes", ct.POINTER(ct.c_uint64))]
+
+
+class _Dist(ct.Structure):
+    _fields_ = [("rank", ct.c_int32), ("world", ct.c_int32), ("device", ct.c_int32), ("nccl_id", ct.c_void_p)]
+
+
+class _EnumParams(ct.Structure):
+    _fields_ = [("max_partitions", ct.c_uint32), ("slo_us", ct.POINTER(ct.c_uint32)),
+                ("margin_permille", ct.c_uint32)]
+
+
+class _Frontier(ct.Structure):
+    _fields_ = [("n_candidates", ct.c_uint64), ("n_feasible", ct.c_uint64), ("n_points", ct.c_uint64),
+                ("n_segments", ct.c_uint64), ("points", ct.c_void_p), ("seg_offsets", ct.POINTER(ct.c_uint64)),
+                ("d_points", ct.c_void_p), ("d_seg_offsets", ct.c_void_p), ("n_survivors", ct.c_uint64),
+                ("n_candidates_local", ct.c_uint64), ("n_feasible_local", ct.c_uint64)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise PPipeError(PPIPE_ECUDA, f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                                          "(there is no CPU fallback)")
+        L = ct.CDLL(LIB_PATH, mode=ct.RTLD_GLOBAL)
+        L.ppipe_load_profiles.restype = ct.c_int
+        L.ppipe_load_profiles.argtypes = [ct.POINTER(ct.c_void_p), ct.c_uint32, ct.POINTER(_Model), ct.c_uint32,
+                                          ct.c_uint32, ct.POINTER(ct.c_uint32), ct.POINTER(ct.c_uint32),
+                                          ct.POINTER(_Dist)]
+        L.ppipe_update_profiles.restype = ct.c_int
+        L.ppipe_update_profiles.argtypes = [ct.c_void_p, ct.c_uint32, ct.POINTER(_Model)]
+        L.ppipe_enumerate.restype = ct.c_int
+        L.ppipe_enumerate.argtypes = [ct.c_void_p, ct.POINTER(_EnumParams)]
+        L.ppipe_pareto.restype = ct.c_int
+        L.ppipe_pareto.argtypes = [ct.c_void_p, ct.c_int, ct.POINTER(_Frontier)]
+        L.ppipe_free.restype = None
+        L.ppipe_free.argtypes = [ct.c_void_p]
+        L.ppipe_last_error.restype = ct.c_char_p
+        L.ppipe_last_error.argtypes = [ct.c_void_p]
+        L.ppipe_nccl_unique_id.restype = ct.c_int
+        L.ppipe_nccl_unique_id.argtypes = [ct.c_void_p]
+        L.ppipe_stream.restype = ct.c_void_p
+        L.ppipe_stream.argtypes = [ct.c_void_p]
+        L.ppipe_phase_ms.restype = ct.c_int
+        L.ppipe_phase_ms.argtypes = [ct.c_void_p, ct.POINTER(ct.c_float)]
+        L.ppipe_launch_count.restype = ct.c_uint64
+        L.ppipe_launch_count.argtypes = [ct.c_void_p]
+        L.ppipe_partition_rows.restype = ct.c_int
+        L.ppipe_partition_rows.argtypes = [ct.c_uint32, ct.POINTER(ct.c_uint32), ct.c_uint32, ct.c_uint32,
+                                           ct.c_uint32, ct.c_int32, ct.c_int32, ct.POINTER(ct.c_uint32)]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, ctx=None):
+    if rc != PPIPE_OK:
+        msg = lib().ppipe_last_error(ctx)
+        raise PPipeError(rc, msg.decode() if msg else "")
+
+
+def _u32p(a):
+    return a.ctypes.data_as(ct.POINTER(ct.c_uint32))
+
+
+class Context:
+    """Owns a ppipe_ctx* plus the host arrays it was built from."""
+
+    def __init__(self, handle, n_models):
+        self.handle = handle
+        self.n_models = n_models
+
+    @property
+    def stream(self) -> int:
+        return int(lib().ppipe_stream(self.handle) or 0)
+
+    def phase_ms(self):
+        out = (ct.c_float * 4)()
+        _check(lib().ppipe_phase_ms(self.handle, out), self.handle)
+        return [float(x) for x in out]
+
+    def launch_count(self) -> int:
+        return int(lib().ppipe_launch_count(self.handle))
+
+
+def nccl_unique_id() -> bytes:
+    buf = ct.create_string_buffer(128)
+    _check(lib().ppipe_nccl_unique_id(buf))
+    return buf.raw
+
+
+def _models_array(lat_us, act_bytes):
+    n = len(lat_us)
+    models = (_Model * n)()
+    keep = []
+    for i in range(n):
+        lat = np.ascontiguousarray(lat_us[i], dtype=np.uint32)
+        S = np.ascontiguousarray(act_bytes[i], dtype=np.uint64)
+        keep += [lat, S]
+        models[i].n_layers = lat.shape[1]
+        models[i].lat_us = _u32p(lat)
+        models[i].act_bytes = S.ctypes.data_as(ct.POINTER(ct.c_uint64))
+    return models, keep
+
+
+def update_profiles(ctx: Context, lat_us: Sequence[np.ndarray], act_bytes: Sequence[np.ndarray]) -> None:
+    models, keep = _models_array(lat_us, act_bytes)
+    _check(lib().ppipe_update_profiles(ctx.handle, len(lat_us), models), ctx.handle)
+    del keep
+
+
+def load_profiles(lat_us: Sequence[np.ndarray], act_bytes: Sequence[np.ndarray], n_classes: int,
+                  batches: np.ndarray, bw_bits_per_us: np.ndarray, rank: int = 0, world: int = 1,
+                  device: int = -1, nccl_id: Optional[bytes] = None) -> Context:
+    n = len(lat_us)
+    models, keep = _models_array(lat_us, act_bytes)
+    b = np.ascontiguousarray(batches, dtype=np.uint32)
+    bw = np.ascontiguousarray(bw_bits_per_us, dtype=np.uint32).reshape(-1)
+    idbuf = ct.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+    dist = _Dist(rank, world, device, ct.cast(idbuf, ct.c_void_p) if idbuf is not None else None)
+    h = ct.c_void_p()
+    rc = lib().ppipe_load_profiles(ct.byref(h), n, models, n_classes, len(b), _u32p(b), _u32p(bw), ct.byref(dist))
+    _check(rc, None)
+    del keep
+    return Context(h, n)
+
+
+def load_workload(w, rank: int = 0, world: int = 1, device: int = -1, nccl_id: Optional[bytes] = None) -> Context:
+    """Convenience: load a workloads.Workload."""
+    return load_profiles([m.lat_us for m in w.models], [m.act_bytes for m in w.models], w.n_classes,
+                         w.batches, w.bw, rank, world, device, nccl_id)
+
+
+def enumerate(ctx: Context, max_partitions: int, slo_us: np.ndarray, margin_permille: int) -> None:  # noqa: A001
+    slo = np.ascontiguousarray(slo_us, dtype=np.uint32)
+    if slo.shape[0] != ctx.n_models:
+        raise PPipeError(PPIPE_EINVAL, f"slo_us has {slo.shape[0]} entries for {ctx.n_models} models")
+    p = _EnumParams(max_partitions, _u32p(slo), margin_permille)
+    _check(lib().ppipe_enumerate(ctx.handle, ct.byref(p)), ctx.handle)
+
+
+@dataclass
+class Frontier:
+    n_candidates: int
+    n_feasible: int
+    n_points: int
+    n_segments: int
+    n_survivors: int
+    points: Optional[np.ndarray]       # POINT_DTYPE (host), canonical order
+    seg_offsets: Optional[np.ndarray]  # uint64 [n_segments + 1]
+    d_points: int                      # device pointer
+    d_seg_offsets: int
+    n_candidates_local: int = 0
+    n_feasible_local: int = 0
+
+
+def pareto(ctx: Context, copy_to_host: bool = True) -> Frontier:
+    f = _Frontier()
+    _check(lib().ppipe_pareto(ctx.handle, 1 if copy_to_host else 0, ct.byref(f)), ctx.handle)
+    pts = seg = None
+    if copy_to_host:
+        n = int(f.n_points)
+        if n:
+            buf = (ct.c_char * (32 * n)).from_address(f.points)
+            pts = np.frombuffer(buf, dtype=POINT_DTYPE).copy()
+        else:
+            pts = np.zeros(0, dtype=POINT_DTYPE)
+        seg = np.ctypeslib.as_array(f.seg_offsets, shape=(int(f.n_segments) + 1,)).copy()
+    return Frontier(int(f.n_candidates), int(f.n_feasible), int(f.n_points), int(f.n_segments),
+                    int(f.n_survivors), pts, seg, int(f.d_points or 0), int(f.d_seg_offsets or 0),
+                    int(f.n_candidates_local), int(f.n_feasible_local))
+
+
+def free(ctx: Context) -> None:
+    if ctx is not None and ctx.handle:
+        lib().ppipe_free(ctx.handle)
+        ctx.handle = None
+
+
+def partition_rows(n_layers: Sequence[int], n_classes: int, n_batches: int, max_partitions: int, rank: int,
+                   world: int) -> np.ndarray:
+    Ms = np.ascontiguousarray(n_layers, dtype=np.uint32)
+    rows = np.zeros(2 * len(Ms), dtype=np.uint32)
+    _check(lib().ppipe_partition_rows(len(Ms), _u32p(Ms), n_classes, n_batches, max_partitions, rank, world,
+                                      _u32p(rows)))
+    return rows.reshape(-1, 2)
+
+
+def run(w, rank: int = 0, world: int = 1, device: int = -1, nccl_id: Optional[bytes] = None,
+        copy_to_host: bool = True) -> Frontier:
+    """One full pass: load, enumerate, pareto, free."""
+    ctx = load_workload(w, rank, world, device, nccl_id)
+    try:
+        enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
+        return pareto(ctx, copy_to_host)
+    finally:
+        free(ctx)

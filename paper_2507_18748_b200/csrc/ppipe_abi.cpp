@@ -1,0 +1,737 @@
+// ppipe_abi.cpp -- C-ABI shim of libppipe_b200.so (include/ppipe.h).
+//
+// Host side of the hot path: input validation with named errors (SURVEY.md
+// §8(b)), the first-cut-row partition across ranks (§8(e)), device memory and
+// stream ownership, kernel orchestration (pack -> score -> frontier), and the
+// NCCL frontier merge (all-gather of counts and local frontiers, then one final
+// frontier pass). No arithmetic of the method runs here except closed-form
+// bookkeeping (segment bases, row weights); every candidate is scored on the GPU.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <thread>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "ppipe_internal.h"
+
+#define PPIPE_API extern "C" __attribute__((visibility("default")))
+
+using namespace ppipe;
+
+namespace {
+
+thread_local std::string g_tls_error;
+
+// ---- NCCL, loaded at run time (the process's already-loaded libnccl.so.2 if any) ----
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+bool load_nccl(std::string* err) {
+  if (g_nccl.tried) {
+    if (!g_nccl.ok && err) *err = "NCCL library could not be loaded";
+    return g_nccl.ok;
+  }
+  g_nccl.tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    if (err) *err = std::string("dlopen(libnccl.so.2) failed: ") + dlerror();
+    return false;
+  }
+  g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.AllGather = (decltype(g_nccl.AllGather))dlsym(h, "ncclAllGather");
+  g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllGather && g_nccl.CommDestroy;
+  if (!g_nccl.ok && err) *err = "libnccl.so.2 lacks a required symbol";
+  return g_nccl.ok;
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;  // capacity in elements
+  cudaError_t reserve(size_t want) {
+    if (want <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(want, 1) * sizeof(T));
+    if (e == cudaSuccess) n = std::max<size_t>(want, 1);
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+// Row weights of the partition (candidates per first-cut row, §8(e)).
+// row 0: K = 1 (C * B); row r in [1, M-1]: K = 2 (C^2 B) + K = 3 with c_1 = r (C^3 B (M-1-r)).
+inline unsigned __int128 row_weight(uint32_t M, uint32_t r, uint64_t C, uint64_t B, uint32_t kmax) {
+  if (r == 0) return (unsigned __int128)C * B;
+  unsigned __int128 w = 0;
+  if (kmax >= 2 && M >= 2) w += (unsigned __int128)C * C * B;
+  if (kmax >= 3 && M >= 3 && r <= M - 2) w += (unsigned __int128)C * C * C * B * (M - 1 - r);
+  return w;
+}
+
+inline unsigned __int128 model_weight(uint32_t M, uint64_t C, uint64_t B, uint32_t kmax) {
+  unsigned __int128 w = (unsigned __int128)C * B;
+  if (kmax >= 2 && M >= 2) w += (unsigned __int128)C * C * B * (M - 1);
+  if (kmax >= 3 && M >= 3) w += (unsigned __int128)C * C * C * B * ((uint64_t)(M - 1) * (M - 2) / 2);
+  return w;
+}
+
+// Contiguous equal-weight split of the (model, row) sequence. A row whose
+// starting prefix weight s satisfies q*W <= s*world < (q+1)*W goes to rank q.
+void partition_rows(const std::vector<uint32_t>& Ms, uint64_t C, uint64_t B, uint32_t kmax, int rank, int world,
+                    std::vector<uint32_t>& rows) {
+  const size_t n = Ms.size();
+  rows.assign(2 * n, 0);
+  unsigned __int128 W = 0;
+  for (uint32_t M : Ms) W += model_weight(M, C, B, kmax);
+  if (world <= 1) {
+    for (size_t m = 0; m < n; ++m) {
+      rows[2 * m] = 0;
+      rows[2 * m + 1] = Ms[m];
+    }
+    return;
+  }
+  auto owner = [&](unsigned __int128 s) -> int {
+    unsigned __int128 q = s * (unsigned __int128)world / W;
+    return (int)std::min<unsigned __int128>(q, (unsigned __int128)(world - 1));
+  };
+  unsigned __int128 s = 0;
+  for (size_t m = 0; m < n; ++m) {
+    const uint32_t M = Ms[m];
+    const unsigned __int128 wm = model_weight(M, C, B, kmax);
+    int64_t lo = -1, hi = -1;
+    if (owner(s) == rank && owner(s + wm - 1) == rank) {
+      lo = 0;
+      hi = M;  // whole model
+    } else if (owner(s) <= rank && owner(s + wm - 1) >= rank) {
+      unsigned __int128 t = s;
+      for (uint32_t r = 0; r < M; ++r) {
+        const int o = owner(t);
+        if (o == rank) {
+          if (lo < 0) lo = r;
+          hi = r + 1;
+        }
+        t += row_weight(M, r, C, B, kmax);
+      }
+    }
+    if (lo >= 0) {
+      rows[2 * m] = (uint32_t)lo;
+      rows[2 * m + 1] = (uint32_t)hi;
+    }
+    s += wm;
+  }
+}
+
+}  // namespace
+
+struct ppipe_ctx {
+  std::string err;
+  int rank = 0, world = 1, device = 0;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  uint32_t C = 0, B = 0, n_models = 0, V = 0;
+  std::vector<uint32_t> Ms;        // all models
+  std::vector<uint32_t> h_batches;
+  std::vector<uint32_t> rows;      // [2*n_models] this rank's row ranges
+  std::vector<int> local;          // local model ids (work order)
+  std::vector<DevModel> h_models;  // per local model
+  uint32_t max_M = 0;
+  // device inputs
+  DevBuf<uint32_t> d_lat;
+  DevBuf<uint64_t> d_s;
+  DevBuf<int32_t> d_P, d_Y;
+  DevBuf<DevModel> d_models;
+  DevBuf<uint16_t> d_batches;
+  DevBuf<uint32_t> d_bwv;
+  DevBuf<uint8_t> d_pairv;
+  DevBuf<uint64_t> d_segbase;
+  // outputs
+  DevBuf<unsigned long long> d_counters;
+  DevBuf<ppipe_point> d_surv, d_local, d_gather, d_union, d_final;
+  DevBuf<uint64_t> d_segoff_local, d_segoff_final, d_cnt_send, d_cnt_recv;
+  FrontierScratch scratch;
+  std::vector<ppipe_point> h_points;
+  std::vector<uint64_t> h_segoff;
+  unsigned long long* h_counters = nullptr;  // pinned [3]
+  // enumerate state
+  bool enumerated = false;
+  ppipe_enum_params last_params{};
+  std::vector<uint32_t> last_slo;
+  uint64_t n_seg_total = 0;
+  uint64_t surv_cap = 1ull << 22;
+  cudaEvent_t ev[8] = {};
+  float phase_ms[4] = {0, 0, 0, 0};
+  uint64_t launches = 0;
+  int launches_i = 0;
+};
+
+namespace {
+
+int fail(ppipe_ctx* ctx, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  else g_tls_error = buf;
+  return code;
+}
+
+#define CU(ctx, call)                                                                        \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail((ctx), e_ == cudaErrorMemoryAllocation ? PPIPE_ENOMEM : PPIPE_ECUDA,       \
+                  "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);      \
+  } while (0)
+
+#define NC_(ctx, call)                                                                       \
+  do {                                                                                       \
+    ncclResult_t r_ = (call);                                                                \
+    if (r_ != ncclSuccess)                                                                   \
+      return fail((ctx), PPIPE_ENCCL, "%s: %s", #call,                                       \
+                  g_nccl.GetErrorString ? g_nccl.GetErrorString(r_) : "nccl error");         \
+  } while (0)
+
+void free_ctx(ppipe_ctx* c) {
+  if (!c) return;
+  if (c->device >= 0) cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  c->d_lat.release();
+  c->d_s.release();
+  c->d_P.release();
+  c->d_Y.release();
+  c->d_models.release();
+  c->d_batches.release();
+  c->d_bwv.release();
+  c->d_pairv.release();
+  c->d_segbase.release();
+  c->d_counters.release();
+  c->d_surv.release();
+  c->d_local.release();
+  c->d_gather.release();
+  c->d_union.release();
+  c->d_final.release();
+  c->d_segoff_local.release();
+  c->d_segoff_final.release();
+  c->d_cnt_send.release();
+  c->d_cnt_recv.release();
+  if (c->scratch.buf) cudaFree(c->scratch.buf);
+  if (c->h_counters) cudaFreeHost(c->h_counters);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+}  // namespace
+
+// Per-model checks of the exact-int32 envelope (threaded over models; the
+// first failing model in index order is reported, so the message is deterministic).
+static int validate_models(uint32_t n_models, const ppipe_model* models, uint32_t C, uint32_t B, const uint32_t* batches,
+                    std::string* err) {
+  const uint64_t bmax = batches[B - 1];
+  std::vector<int> code(n_models, PPIPE_OK);
+  std::vector<std::string> msg(n_models);
+  auto check = [&](uint32_t m) {
+    const ppipe_model& md = models[m];
+    char buf[256];
+    if (md.n_layers < 1 || md.n_layers > 65535) {
+      snprintf(buf, sizeof buf, "model %u: n_layers %u must be 1..65535", m, md.n_layers);
+      code[m] = PPIPE_EINVAL;
+      msg[m] = buf;
+      return;
+    }
+    if (!md.lat_us || !md.act_bytes) {
+      snprintf(buf, sizeof buf, "model %u: NULL profile pointer", m);
+      code[m] = PPIPE_EINVAL;
+      msg[m] = buf;
+      return;
+    }
+    const uint32_t M = md.n_layers;
+    std::vector<uint64_t> tot((size_t)C * B, 0);
+    for (uint32_t k = 0; k < C; ++k)
+      for (uint32_t l = 0; l < M; ++l) {
+        const uint32_t* row = md.lat_us + ((size_t)k * M + l) * B;
+        uint64_t* t = tot.data() + (size_t)k * B;
+        for (uint32_t bi = 0; bi < B; ++bi) t[bi] += row[bi];
+      }
+    for (uint32_t k = 0; k < C; ++k)
+      for (uint32_t bi = 0; bi < B; ++bi)
+        if (tot[(size_t)k * B + bi] >= (uint64_t)kRangeLimit) {
+          snprintf(buf, sizeof buf, "model %u class %u batch %u: whole-model latency %llu us >= 2^28 (int32 envelope)",
+                   m, k, batches[bi], (unsigned long long)tot[(size_t)k * B + bi]);
+          code[m] = PPIPE_ERANGE;
+          msg[m] = buf;
+          return;
+        }
+    const uint64_t smax = (uint64_t)INT64_MAX / (8 * bmax);
+    for (uint32_t l = 0; l < M; ++l)
+      if (md.act_bytes[l] > smax) {
+        snprintf(buf, sizeof buf, "model %u layer %u: act_bytes %llu too large (8*S*b >= 2^63)", m, l,
+                 (unsigned long long)md.act_bytes[l]);
+        code[m] = PPIPE_ERANGE;
+        msg[m] = buf;
+        return;
+      }
+  };
+  const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32u));
+  if (n_models < 4 || nt == 1) {
+    for (uint32_t m = 0; m < n_models; ++m) check(m);
+  } else {
+    std::atomic<uint32_t> next{0};
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t)
+      th.emplace_back([&] {
+        for (uint32_t m; (m = next.fetch_add(1)) < n_models;) check(m);
+      });
+    for (auto& t : th) t.join();
+  }
+  for (uint32_t m = 0; m < n_models; ++m)
+    if (code[m] != PPIPE_OK) {
+      *err = msg[m];
+      return code[m];
+    }
+  return PPIPE_OK;
+}
+
+// ===========================================================================
+// ABI
+// ===========================================================================
+
+PPIPE_API const char* ppipe_last_error(const ppipe_ctx* ctx) {
+  if (ctx) return ctx->err.c_str();
+  return g_tls_error.c_str();
+}
+
+PPIPE_API int ppipe_nccl_unique_id(void* out128) {
+  if (!out128) return fail(nullptr, PPIPE_EINVAL, "ppipe_nccl_unique_id: NULL output");
+  std::string err;
+  if (!load_nccl(&err)) return fail(nullptr, PPIPE_ENCCL, "%s", err.c_str());
+  ncclUniqueId id;
+  ncclResult_t r = g_nccl.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, PPIPE_ENCCL, "ncclGetUniqueId failed");
+  std::memcpy(out128, &id, sizeof id);
+  return PPIPE_OK;
+}
+
+PPIPE_API int ppipe_partition_rows(uint32_t n_models, const uint32_t* n_layers, uint32_t n_classes,
+                                   uint32_t n_batches, uint32_t max_partitions, int32_t rank, int32_t world,
+                                   uint32_t* rows) {
+  if (!n_layers || !rows || n_models == 0 || world < 1 || rank < 0 || rank >= world || n_classes == 0 ||
+      n_batches == 0 || max_partitions < 1 || max_partitions > 3)
+    return fail(nullptr, PPIPE_EINVAL, "ppipe_partition_rows: invalid arguments");
+  std::vector<uint32_t> Ms(n_layers, n_layers + n_models), r;
+  partition_rows(Ms, n_classes, n_batches, max_partitions, rank, world, r);
+  std::memcpy(rows, r.data(), r.size() * sizeof(uint32_t));
+  return PPIPE_OK;
+}
+
+PPIPE_API void* ppipe_stream(ppipe_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+PPIPE_API uint64_t ppipe_launch_count(ppipe_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+PPIPE_API int ppipe_phase_ms(ppipe_ctx* ctx, float out_ms[4]) {
+  if (!ctx || !out_ms) return PPIPE_EINVAL;
+  std::memcpy(out_ms, ctx->phase_ms, sizeof ctx->phase_ms);
+  return PPIPE_OK;
+}
+
+PPIPE_API void ppipe_free(ppipe_ctx* ctx) { free_ctx(ctx); }
+
+PPIPE_API int ppipe_load_profiles(ppipe_ctx** out, uint32_t n_models, const ppipe_model* models, uint32_t n_classes,
+                                  uint32_t n_batches, const uint32_t* batches, const uint32_t* bw_bits_per_us,
+                                  const ppipe_dist* dist) {
+  if (!out) return fail(nullptr, PPIPE_EINVAL, "ppipe_load_profiles: out is NULL");
+  *out = nullptr;
+  if (n_models == 0 || !models) return fail(nullptr, PPIPE_EINVAL, "ppipe_load_profiles: no models");
+  if (n_classes < 1 || n_classes > (uint32_t)kMaxClasses)
+    return fail(nullptr, PPIPE_EINVAL, "n_classes %u: must be 1..%d", n_classes, kMaxClasses);
+  if (n_batches < 1 || n_batches > 65535 || !batches)
+    return fail(nullptr, PPIPE_EINVAL, "n_batches %u: must be 1..65535 with a batch list", n_batches);
+  for (uint32_t i = 0; i < n_batches; ++i) {
+    if (batches[i] < 1 || batches[i] > 65535)
+      return fail(nullptr, PPIPE_EINVAL, "batch %u value %u: must be 1..65535", i, batches[i]);
+    if (i && batches[i] <= batches[i - 1])
+      return fail(nullptr, PPIPE_EINVAL, "batch %u value %u: batches must be strictly increasing", i, batches[i]);
+  }
+  if (!bw_bits_per_us) return fail(nullptr, PPIPE_EINVAL, "bandwidth matrix is NULL");
+  for (uint32_t i = 0; i < n_classes * n_classes; ++i)
+    if (bw_bits_per_us[i] == 0)
+      return fail(nullptr, PPIPE_EINVAL, "bandwidth class %u -> class %u: must be >= 1 bits/us", i / n_classes,
+                  i % n_classes);
+  {
+    std::string verr;
+    const int vrc = validate_models(n_models, models, n_classes, n_batches, batches, &verr);
+    if (vrc != PPIPE_OK) return fail(nullptr, vrc, "%s", verr.c_str());
+  }
+  int rank = 0, world = 1, device = -1;
+  const void* nccl_id = nullptr;
+  if (dist) {
+    rank = dist->rank;
+    world = dist->world;
+    device = dist->device;
+    nccl_id = dist->nccl_id;
+    if (world < 1 || rank < 0 || rank >= world)
+      return fail(nullptr, PPIPE_EINVAL, "dist: rank %d / world %d invalid", rank, world);
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(nullptr, PPIPE_ECUDA, "no CUDA device: this library has no CPU fallback");
+  if (device < 0) cudaGetDevice(&device);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess)
+    return fail(nullptr, PPIPE_ECUDA, "cudaGetDeviceProperties(%d) failed", device);
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(nullptr, PPIPE_ECUDA, "device %d is sm_%d%d; this build targets sm_100a (B200) only", device,
+                prop.major, prop.minor);
+
+  ppipe_ctx* c = new ppipe_ctx();
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  c->C = n_classes;
+  c->B = n_batches;
+  c->n_models = n_models;
+  c->h_batches.assign(batches, batches + n_batches);
+  auto bail = [&](int code) {
+    g_tls_error = c->err;
+    free_ctx(c);
+    return code;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) {
+    fail(c, PPIPE_ECUDA, "cudaSetDevice(%d) failed", device);
+    return bail(PPIPE_ECUDA);
+  }
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    fail(c, PPIPE_ECUDA, "cudaStreamCreate failed");
+    return bail(PPIPE_ECUDA);
+  }
+  for (auto& e : c->ev)
+    if (cudaEventCreate(&e) != cudaSuccess) {
+      fail(c, PPIPE_ECUDA, "cudaEventCreate failed");
+      return bail(PPIPE_ECUDA);
+    }
+  if (cudaMallocHost(&c->h_counters, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+    fail(c, PPIPE_ENOMEM, "cudaMallocHost failed");
+    return bail(PPIPE_ENOMEM);
+  }
+  if (world > 1 && nccl_id) {
+    std::string err;
+    if (!load_nccl(&err)) {
+      fail(c, PPIPE_ENCCL, "%s", err.c_str());
+      return bail(PPIPE_ENCCL);
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof id);
+    ncclResult_t r = g_nccl.CommInitRank(&c->comm, world, id, rank);
+    if (r != ncclSuccess) {
+      fail(c, PPIPE_ENCCL, "ncclCommInitRank(world=%d, rank=%d): %s", world, rank,
+           g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "error");
+      return bail(PPIPE_ENCCL);
+    }
+  }
+  // partition (weights with Kmax = 3; valid for any Kmax)
+  c->Ms.resize(n_models);
+  for (uint32_t m = 0; m < n_models; ++m) c->Ms[m] = models[m].n_layers;
+  partition_rows(c->Ms, n_classes, n_batches, 3, rank, world, c->rows);
+  for (uint32_t m = 0; m < n_models; ++m)
+    if (c->rows[2 * m + 1] > c->rows[2 * m]) c->local.push_back((int)m);
+  // heavy models first (K = 3 work ~ M^2) for a short tail
+  std::stable_sort(c->local.begin(), c->local.end(), [&](int a, int b) { return c->Ms[a] > c->Ms[b]; });
+  // distinct bandwidth values and the class-pair map
+  std::vector<uint32_t> bwv(bw_bits_per_us, bw_bits_per_us + n_classes * n_classes);
+  std::sort(bwv.begin(), bwv.end());
+  bwv.erase(std::unique(bwv.begin(), bwv.end()), bwv.end());
+  std::vector<uint8_t> pairv(n_classes * n_classes);
+  for (uint32_t i = 0; i < n_classes * n_classes; ++i)
+    pairv[i] = (uint8_t)(std::lower_bound(bwv.begin(), bwv.end(), bw_bits_per_us[i]) - bwv.begin());
+  c->V = (uint32_t)bwv.size();
+  // device layout
+  uint64_t lat_n = 0, s_n = 0, p_n = 0, y_n = 0;
+  for (int m : c->local) {
+    DevModel d{};
+    d.M = c->Ms[m];
+    d.Mp = (d.M + 1 + 3) / 4 * 4;
+    d.lat_off = lat_n;
+    d.s_off = s_n;
+    d.p_off = p_n;
+    d.y_off = y_n;
+    d.model = (uint32_t)m;
+    d.row_lo = c->rows[2 * m];
+    d.row_hi = c->rows[2 * m + 1];
+    lat_n += (uint64_t)n_classes * d.M * n_batches;
+    s_n += d.M;
+    p_n += (uint64_t)n_classes * n_batches * d.Mp;
+    y_n += (uint64_t)c->V * n_batches * d.Mp;
+    c->max_M = std::max(c->max_M, d.M);
+    c->h_models.push_back(d);
+  }
+  int rc;
+#define CUL(call)                                                                                          \
+  do {                                                                                                     \
+    cudaError_t e_ = (call);                                                                               \
+    if (e_ != cudaSuccess) {                                                                               \
+      rc = fail(c, e_ == cudaErrorMemoryAllocation ? PPIPE_ENOMEM : PPIPE_ECUDA, "%s: %s", #call,          \
+                cudaGetErrorString(e_));                                                                   \
+      return bail(rc);                                                                                     \
+    }                                                                                                      \
+  } while (0)
+  CUL(c->d_lat.reserve(lat_n));
+  CUL(c->d_s.reserve(s_n));
+  CUL(c->d_P.reserve(p_n));
+  CUL(c->d_Y.reserve(y_n));
+  CUL(c->d_models.reserve(c->h_models.size()));
+  CUL(c->d_batches.reserve(n_batches));
+  CUL(c->d_bwv.reserve(c->V));
+  CUL(c->d_pairv.reserve(pairv.size()));
+  CUL(c->d_segbase.reserve(n_models));
+  CUL(c->d_counters.reserve(4));
+  // host -> device: the profiles this rank needs
+  for (size_t i = 0; i < c->local.size(); ++i) {
+    const int m = c->local[i];
+    const DevModel& d = c->h_models[i];
+    CUL(cudaMemcpyAsync(c->d_lat.p + d.lat_off, models[m].lat_us, sizeof(uint32_t) * n_classes * d.M * n_batches,
+                        cudaMemcpyHostToDevice, c->stream));
+    CUL(cudaMemcpyAsync(c->d_s.p + d.s_off, models[m].act_bytes, sizeof(uint64_t) * d.M, cudaMemcpyHostToDevice,
+                        c->stream));
+  }
+  std::vector<uint16_t> b16(batches, batches + n_batches);
+  CUL(cudaMemcpyAsync(c->d_batches.p, b16.data(), 2 * n_batches, cudaMemcpyHostToDevice, c->stream));
+  CUL(cudaMemcpyAsync(c->d_bwv.p, bwv.data(), 4 * bwv.size(), cudaMemcpyHostToDevice, c->stream));
+  CUL(cudaMemcpyAsync(c->d_pairv.p, pairv.data(), pairv.size(), cudaMemcpyHostToDevice, c->stream));
+  CUL(cudaStreamSynchronize(c->stream));
+#undef CUL
+  *out = c;
+  return PPIPE_OK;
+}
+
+PPIPE_API int ppipe_update_profiles(ppipe_ctx* c, uint32_t n_models, const ppipe_model* models) {
+  if (!c) return fail(nullptr, PPIPE_EINVAL, "ppipe_update_profiles: NULL ctx");
+  if (n_models != c->n_models || !models)
+    return fail(c, PPIPE_EINVAL, "ppipe_update_profiles: %u models, context has %u", n_models, c->n_models);
+  for (uint32_t m = 0; m < n_models; ++m)
+    if (models[m].n_layers != c->Ms[m])
+      return fail(c, PPIPE_EINVAL, "model %u: n_layers %u differs from the loaded %u", m, models[m].n_layers,
+                  c->Ms[m]);
+  {
+    std::string verr;
+    const int vrc = validate_models(n_models, models, c->C, c->B, c->h_batches.data(), &verr);
+    if (vrc != PPIPE_OK) return fail(c, vrc, "%s", verr.c_str());
+  }
+  CU(c, cudaSetDevice(c->device));
+  for (size_t i = 0; i < c->local.size(); ++i) {
+    const int m = c->local[i];
+    const DevModel& d = c->h_models[i];
+    CU(c, cudaMemcpyAsync(c->d_lat.p + d.lat_off, models[m].lat_us, sizeof(uint32_t) * c->C * d.M * c->B,
+                          cudaMemcpyHostToDevice, c->stream));
+    CU(c, cudaMemcpyAsync(c->d_s.p + d.s_off, models[m].act_bytes, sizeof(uint64_t) * d.M, cudaMemcpyHostToDevice,
+                          c->stream));
+  }
+  CU(c, cudaStreamSynchronize(c->stream));
+  c->enumerated = false;
+  return PPIPE_OK;
+}
+
+static int run_enumerate(ppipe_ctx* c) {
+  const ppipe_enum_params* p = &c->last_params;
+  CU(c, cudaSetDevice(c->device));
+  // global segment bases (all models; same on every rank)
+  std::vector<uint64_t> segbase(c->n_models);
+  uint64_t acc = 0;
+  for (uint32_t m = 0; m < c->n_models; ++m) {
+    segbase[m] = acc;
+    uint64_t pw = 1;
+    for (uint32_t K = 1; K <= p->max_partitions && K <= c->Ms[m]; ++K) {
+      pw *= c->C;
+      acc += pw;
+    }
+  }
+  c->n_seg_total = acc;
+  for (size_t i = 0; i < c->local.size(); ++i) c->h_models[i].slo_us = c->last_slo[c->local[i]];
+  CU(c, cudaMemcpyAsync(c->d_segbase.p, segbase.data(), 8 * segbase.size(), cudaMemcpyHostToDevice, c->stream));
+  CU(c, cudaMemcpyAsync(c->d_models.p, c->h_models.data(), sizeof(DevModel) * c->h_models.size(),
+                        cudaMemcpyHostToDevice, c->stream));
+  CU(c, c->d_surv.reserve(c->surv_cap));
+  Problem pb{};
+  pb.C = (int)c->C;
+  pb.B = (int)c->B;
+  pb.V = (int)c->V;
+  pb.Kmax = (int)p->max_partitions;
+  pb.margin = (int)p->margin_permille;
+  pb.batches = c->d_batches.p;
+  pb.bw_v = c->d_bwv.p;
+  pb.pair_v = c->d_pairv.p;
+  pb.models = c->d_models.p;
+  pb.n_local = (int)c->local.size();
+  pb.raw_lat = c->d_lat.p;
+  pb.raw_s = c->d_s.p;
+  pb.P = c->d_P.p;
+  pb.Y = c->d_Y.p;
+  pb.seg_base = c->d_segbase.p;
+  pb.max_M = c->max_M;
+  ScoreOut so{c->d_surv.p, c->d_counters.p, (unsigned long long)c->d_surv.n};
+  c->launches_i = 0;
+  CU(c, cudaEventRecord(c->ev[0], c->stream));
+  CU(c, launch_pack(pb, c->stream));
+  c->launches_i += pb.n_local ? 2 : 0;
+  CU(c, cudaEventRecord(c->ev[1], c->stream));
+  CU(c, cudaMemsetAsync(c->d_counters.p, 0, 4 * sizeof(unsigned long long), c->stream));
+  CU(c, launch_score(pb, so, c->stream, &c->launches_i));
+  CU(c, cudaEventRecord(c->ev[2], c->stream));
+  return PPIPE_OK;
+}
+
+PPIPE_API int ppipe_enumerate(ppipe_ctx* ctx, const ppipe_enum_params* p) {
+  if (!ctx) return fail(nullptr, PPIPE_EINVAL, "ppipe_enumerate: NULL ctx");
+  if (!p || !p->slo_us) return fail(ctx, PPIPE_EINVAL, "ppipe_enumerate: NULL params or slo_us");
+  if (p->max_partitions < 1 || p->max_partitions > 3)
+    return fail(ctx, PPIPE_EINVAL, "max_partitions %u: must be 1..3", p->max_partitions);
+  if (p->margin_permille >= 1000)
+    return fail(ctx, PPIPE_EINVAL, "margin_permille %u: must be < 1000", p->margin_permille);
+  for (uint32_t m = 0; m < ctx->n_models; ++m) {
+    const uint64_t T = (uint64_t)p->slo_us[m] * (1000 - p->margin_permille) / 1000;
+    if (T >= (uint64_t)kRangeLimit)
+      return fail(ctx, PPIPE_ERANGE, "model %u: T_eff %llu us >= 2^28 (int32 envelope)", m,
+                  (unsigned long long)T);
+  }
+  ctx->last_params = *p;
+  ctx->last_slo.assign(p->slo_us, p->slo_us + ctx->n_models);
+  ctx->last_params.slo_us = ctx->last_slo.data();
+  ctx->enumerated = false;
+  int rc = run_enumerate(ctx);
+  if (rc == PPIPE_OK) ctx->enumerated = true;
+  return rc;
+}
+
+PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) {
+  if (!c) return fail(nullptr, PPIPE_EINVAL, "ppipe_pareto: NULL ctx");
+  if (!out) return fail(c, PPIPE_EINVAL, "ppipe_pareto: NULL output");
+  if (!c->enumerated) return fail(c, PPIPE_ESTATE, "ppipe_pareto called before ppipe_enumerate");
+  CU(c, cudaSetDevice(c->device));
+  // survivors; grow and re-run on overflow (deterministic, so the result is unchanged)
+  for (;;) {
+    CU(c, cudaMemcpyAsync(c->h_counters, c->d_counters.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
+    if (c->h_counters[0] <= c->d_surv.n) break;
+    c->surv_cap = c->h_counters[0] + c->h_counters[0] / 4 + 1024;
+    int rc = run_enumerate(c);
+    if (rc != PPIPE_OK) return rc;
+  }
+  const uint64_t n_surv = c->h_counters[0];
+  uint64_t n_feas = c->h_counters[1], n_cand = c->h_counters[2];
+  int nl = c->launches_i;
+  // local frontier
+  CU(c, c->d_local.reserve(std::max<uint64_t>(n_surv, 1)));
+  CU(c, c->d_segoff_local.reserve(c->n_seg_total + 1));
+  uint64_t n_local_pts = 0;
+  CU(c, frontier_pass(c->d_surv.p, n_surv, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_local.p,
+                      c->d_segoff_local.p, &n_local_pts, &c->scratch, c->stream, &nl));
+  CU(c, cudaEventRecord(c->ev[3], c->stream));
+  const ppipe_point* d_pts = c->d_local.p;
+  const uint64_t* d_off = c->d_segoff_local.p;
+  uint64_t n_pts = n_local_pts;
+  if (c->world > 1 && c->comm) {
+    // all-gather [n_points, n_cand, n_feas, n_surv] per rank
+    CU(c, c->d_cnt_send.reserve(4));
+    CU(c, c->d_cnt_recv.reserve(4 * (size_t)c->world));
+    uint64_t hs[4] = {n_local_pts, n_cand, n_feas, n_surv};
+    CU(c, cudaMemcpyAsync(c->d_cnt_send.p, hs, sizeof hs, cudaMemcpyHostToDevice, c->stream));
+    NC_(c, g_nccl.AllGather(c->d_cnt_send.p, c->d_cnt_recv.p, 4, ncclUint64, c->comm, c->stream));
+    std::vector<uint64_t> cnts(4 * (size_t)c->world);
+    CU(c, cudaMemcpyAsync(cnts.data(), c->d_cnt_recv.p, 8 * cnts.size(), cudaMemcpyDeviceToHost, c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
+    uint64_t maxc = 1, tot = 0;
+    n_cand = n_feas = 0;
+    for (int r = 0; r < c->world; ++r) {
+      maxc = std::max(maxc, cnts[4 * r]);
+      tot += cnts[4 * r];
+      n_cand += cnts[4 * r + 1];
+      n_feas += cnts[4 * r + 2];
+    }
+    // padded all-gather of local frontiers (32-byte records as bytes)
+    if (c->d_local.n < maxc) {
+      DevBuf<ppipe_point> tmp;
+      CU(c, tmp.reserve(maxc));
+      CU(c, cudaMemcpyAsync(tmp.p, c->d_local.p, sizeof(ppipe_point) * n_local_pts, cudaMemcpyDeviceToDevice,
+                            c->stream));
+      CU(c, cudaStreamSynchronize(c->stream));
+      c->d_local.release();
+      c->d_local = tmp;
+    }
+    CU(c, c->d_gather.reserve(maxc * c->world));
+    NC_(c, g_nccl.AllGather(c->d_local.p, c->d_gather.p, maxc * sizeof(ppipe_point), ncclUint8, c->comm,
+                            c->stream));
+    CU(c, c->d_union.reserve(std::max<uint64_t>(tot, 1)));
+    uint64_t off = 0;
+    for (int r = 0; r < c->world; ++r) {
+      if (cnts[4 * r])
+        CU(c, cudaMemcpyAsync(c->d_union.p + off, c->d_gather.p + (size_t)r * maxc,
+                              sizeof(ppipe_point) * cnts[4 * r], cudaMemcpyDeviceToDevice, c->stream));
+      off += cnts[4 * r];
+    }
+    CU(c, c->d_final.reserve(std::max<uint64_t>(tot, 1)));
+    CU(c, c->d_segoff_final.reserve(c->n_seg_total + 1));
+    CU(c, frontier_pass(c->d_union.p, tot, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_final.p,
+                        c->d_segoff_final.p, &n_pts, &c->scratch, c->stream, &nl));
+    nl += 2;
+    d_pts = c->d_final.p;
+    d_off = c->d_segoff_final.p;
+  }
+  CU(c, cudaEventRecord(c->ev[4], c->stream));
+  CU(c, cudaEventSynchronize(c->ev[4]));
+  cudaEventElapsedTime(&c->phase_ms[0], c->ev[0], c->ev[1]);
+  cudaEventElapsedTime(&c->phase_ms[1], c->ev[1], c->ev[2]);
+  cudaEventElapsedTime(&c->phase_ms[2], c->ev[2], c->ev[3]);
+  cudaEventElapsedTime(&c->phase_ms[3], c->ev[3], c->ev[4]);
+  c->launches = (uint64_t)nl;
+  std::memset(out, 0, sizeof *out);
+  out->n_candidates = n_cand;
+  out->n_feasible = n_feas;
+  out->n_points = n_pts;
+  out->n_segments = c->n_seg_total;
+  out->d_points = d_pts;
+  out->d_seg_offsets = d_off;
+  out->n_survivors = n_surv;
+  out->n_candidates_local = c->h_counters[2];
+  out->n_feasible_local = c->h_counters[1];
+  if (copy_to_host) {
+    c->h_points.resize(n_pts);
+    c->h_segoff.resize(c->n_seg_total + 1);
+    if (n_pts)
+      CU(c, cudaMemcpyAsync(c->h_points.data(), d_pts, sizeof(ppipe_point) * n_pts, cudaMemcpyDeviceToHost,
+                            c->stream));
+    CU(c, cudaMemcpyAsync(c->h_segoff.data(), d_off, 8 * (c->n_seg_total + 1), cudaMemcpyDeviceToHost, c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
+    out->points = c->h_points.data();
+    out->seg_offsets = c->h_segoff.data();
+  }
+  return PPIPE_OK;
+}

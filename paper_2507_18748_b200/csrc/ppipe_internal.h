@@ -1,0 +1,73 @@
+// Internal declarations shared by the C-ABI shim (ppipe_abi.cpp) and the
+// kernels (ppipe_kernels.cu). Not part of the public ABI (include/ppipe.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ppipe.h"
+
+namespace ppipe {
+
+constexpr int kMaxClasses = 8;
+constexpr int kMaxPartitions = 3;
+constexpr int32_t kRangeLimit = 1 << 28;  // exact-int32 envelope
+constexpr int kNumBuckets = 2048;         // E-buckets per (segment, batch) in the fold tables
+constexpr int kScoreThreads = 128;        // 4 warps per CTA
+constexpr int kJ1 = 4;                    // first-cut slots per lane (tile = 32 * kJ1 first cuts)
+constexpr int kMaxMSmem = 8192;           // B(c2) row staged in smem up to this many layers
+
+// Per-model device metadata. Row layouts (int32):
+//   P[k][bi][l], l = 0..M   prefix sums sum_{l' < l} lat[k][l'][bi]           (row length Mp)
+//   Y[v][bi][c], c = 1..M-1 ceil(8 * S[c-1] * b / bw_v) clamped to kRangeLimit (row length Mp)
+struct DevModel {
+  uint32_t M;          // layers
+  uint32_t Mp;         // padded row length (>= M + 1, multiple of 4)
+  uint64_t lat_off;    // u32 offset of raw lat [C][M][B] in the raw upload buffer
+  uint64_t s_off;      // u64 offset of act bytes [M]
+  uint64_t p_off;      // int32 offset of P[m]
+  uint64_t y_off;      // int32 offset of Y[m]
+  uint32_t model;      // index in the caller's model array
+  uint32_t row_lo;     // this rank's first-cut rows [row_lo, row_hi)
+  uint32_t row_hi;
+  uint32_t slo_us;     // raw SLO (set per enumerate)
+  int32_t T;           // T_eff, written by the pack kernel
+  uint32_t pad;
+};
+
+struct Problem {
+  int C, B, V, Kmax, margin;
+  const uint16_t* batches;   // [B] values (device)
+  const uint32_t* bw_v;      // [V] distinct bandwidth values (device)
+  const uint8_t* pair_v;     // [C][C] -> index into bw_v (device)
+  DevModel* models;          // [n_local] (device)
+  int n_local;
+  const uint32_t* raw_lat;   // device
+  const uint64_t* raw_s;     // device
+  int32_t* P;                // device
+  int32_t* Y;                // device
+  const uint64_t* seg_base;  // [n_models_total] global segment id base per model (device)
+  uint32_t max_M;
+};
+
+struct ScoreOut {
+  ppipe_point* surv;
+  unsigned long long* counters;  // [0] survivors, [1] feasible, [2] candidates
+  unsigned long long cap;
+};
+
+// Launchers (stream-ordered). Return cudaError_t of the launch.
+cudaError_t launch_pack(const Problem& pb, cudaStream_t s);
+cudaError_t launch_score(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches);
+
+// Frontier pass over n records: sort by (segment, E), per-(segment, E) best,
+// strict staircase over theta, compaction. seg_base_by_model gives each model's
+// first global segment id; n_seg is the total number of segments.
+struct FrontierScratch {
+  void* buf = nullptr;
+  size_t bytes = 0;
+};
+cudaError_t frontier_pass(const ppipe_point* in, uint64_t n, const uint64_t* seg_base_by_model, int C,
+                          uint64_t n_seg, ppipe_point* out, uint64_t* seg_offsets /* [n_seg+1] device */,
+                          uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches);
+
+}  // namespace ppipe
