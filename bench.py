@@ -167,6 +167,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--models", type=int, default=None, help="config 5 only: first N models (profiling)")
+    ap.add_argument("--margin", type=int, default=None, help="override margin_permille (experiments)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -194,7 +196,9 @@ def main():
     if world > 1:
         dist.barrier()
 
-    w = make_config(args.config)
+    w = make_config(args.config, **({"n_models": args.models} if args.models and args.config == 5 else {}))
+    if args.margin is not None:
+        w.margin_permille = args.margin
     nccl_id = None
     if world > 1:
         t = torch.zeros(128, dtype=torch.uint8, device=dev)
@@ -338,7 +342,7 @@ def main():
         "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded; recipe in DESIGN.md §3)",
         "config": {"workload": f"config {args.config}: {CONFIG_NAMES[args.config]}",
                    "candidates_per_step": n_cand, "feasible_per_step": f.n_feasible,
-                   "frontier_points": f.n_points, "segments": f.n_segments,
+                   "frontier_points": f.n_points, "segments": f.n_segments, "survivors_rank0": f.n_survivors,
                    "l2": "inputs > L2 (P, Y tables ~1.1 GB at N=1) and a 256 MiB L2 flush between timed steps",
                    "parallelism": f"dp{world}: first-cut-row shards + NCCL all-gather frontier merge"
                    if world > 1 else "dp1"},

@@ -65,7 +65,7 @@ typedef struct ppipe_ctx ppipe_ctx; /* opaque; owns all host and device memory i
  * act_bytes [n_layers]: bytes ON THE WIRE of layer l's output at batch 1 (S_l;
  *           the caller halves fp32 sizes when quantising to fp16). */
 typedef struct {
-  uint32_t n_layers; /* M, 1..65535 (cuts are stored as u16) */
+  uint32_t n_layers; /* M, 1..16384 (a model's c2 rows are staged in shared memory) */
   const uint32_t *lat_us;
   const uint64_t *act_bytes;
 } ppipe_model;
@@ -89,7 +89,7 @@ typedef struct {
  *   bw_bits_per_us   [n_classes][n_classes] effective bandwidth sender -> receiver in
  *                    bits/us (= Mbit/s), every entry >= 1 (1/5 of NIC rate)
  *   dist             NULL => single GPU, current device
- * Errors: PPIPE_EINVAL (NULLs, M = 0 or > 65535, n_classes, batch list, bw = 0);
+ * Errors: PPIPE_EINVAL (NULLs, M = 0 or > 16384, n_classes, batch list, bw = 0);
  *         PPIPE_ERANGE (any whole-model latency sum at (class, batch) >= 2^28 us, or
  *         8 * act_bytes * max batch >= 2^63); PPIPE_ECUDA / PPIPE_ENOMEM / PPIPE_ENCCL.
  * On error *out is NULL and ppipe_last_error(NULL) holds the message. */

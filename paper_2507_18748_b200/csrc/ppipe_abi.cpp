@@ -15,6 +15,7 @@
 #include <thread>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -262,8 +263,8 @@ static int validate_models(uint32_t n_models, const ppipe_model* models, uint32_
   auto check = [&](uint32_t m) {
     const ppipe_model& md = models[m];
     char buf[256];
-    if (md.n_layers < 1 || md.n_layers > 65535) {
-      snprintf(buf, sizeof buf, "model %u: n_layers %u must be 1..65535", m, md.n_layers);
+    if (md.n_layers < 1 || md.n_layers > (uint32_t)kMaxLayers) {
+      snprintf(buf, sizeof buf, "model %u: n_layers %u must be 1..%d", m, md.n_layers, kMaxLayers);
       code[m] = PPIPE_EINVAL;
       msg[m] = buf;
       return;
@@ -420,6 +421,10 @@ PPIPE_API int ppipe_load_profiles(ppipe_ctx** out, uint32_t n_models, const ppip
   c->B = n_batches;
   c->n_models = n_models;
   c->h_batches.assign(batches, batches + n_batches);
+  if (const char* cap = getenv("PPIPE_SURVIVOR_CAP")) {  // initial survivor capacity (tests of the regrow path)
+    const long long v = atoll(cap);
+    if (v > 0) c->surv_cap = (uint64_t)v;
+  }
   auto bail = [&](int code) {
     g_tls_error = c->err;
     free_ctx(c);
@@ -596,6 +601,11 @@ static int run_enumerate(ppipe_ctx* c) {
   pb.Y = c->d_Y.p;
   pb.seg_base = c->d_segbase.p;
   pb.max_M = c->max_M;
+  pb.neg_one = -1;
+  {
+    const char* dbg = getenv("PPIPE_DEBUG_FLAGS");
+    pb.debug_flags = dbg ? atoi(dbg) : 0;
+  }
   ScoreOut so{c->d_surv.p, c->d_counters.p, (unsigned long long)c->d_surv.n};
   c->launches_i = 0;
   CU(c, cudaEventRecord(c->ev[0], c->stream));

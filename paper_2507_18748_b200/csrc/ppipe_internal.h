@@ -11,10 +11,8 @@ namespace ppipe {
 constexpr int kMaxClasses = 8;
 constexpr int kMaxPartitions = 3;
 constexpr int32_t kRangeLimit = 1 << 28;  // exact-int32 envelope
-constexpr int kNumBuckets = 2048;         // E-buckets per (segment, batch) in the fold tables
-constexpr int kScoreThreads = 128;        // 4 warps per CTA
 constexpr int kJ1 = 4;                    // first-cut slots per lane (tile = 32 * kJ1 first cuts)
-constexpr int kMaxMSmem = 8192;           // B(c2) row staged in smem up to this many layers
+constexpr int kMaxLayers = 16384;         // c2 rows (B, Q, R) of a model are staged in shared memory
 
 // Per-model device metadata. Row layouts (int32):
 //   P[k][bi][l], l = 0..M   prefix sums sum_{l' < l} lat[k][l'][bi]           (row length Mp)
@@ -47,6 +45,8 @@ struct Problem {
   int32_t* Y;                // device
   const uint64_t* seg_base;  // [n_models_total] global segment id base per model (device)
   uint32_t max_M;
+  int neg_one;                // -1, passed at run time (keeps IMAD on the FMA pipe)
+  int debug_flags;            // timing experiments only (PPIPE_DEBUG_FLAGS); 0 in production
 };
 
 struct ScoreOut {

@@ -143,58 +143,99 @@ __device__ __forceinline__ Rec make_rec(uint32_t model, int K, int c1, int c2, i
   return r;
 }
 
-__device__ __forceinline__ void store_rec(ppipe_point* dst, const Rec& r) {
-  int4* d = reinterpret_cast<int4*>(dst);
-  d[0] = make_int4((int)r.w[0], (int)r.w[1], (int)r.w[2], (int)r.w[3]);
-  d[1] = make_int4((int)r.w[4], (int)r.w[5], (int)r.w[6], (int)r.w[7]);
-}
+constexpr int kWarps = 2;      // warps per CTA (share the fold tables and the staged rows)
+constexpr int kEmitBuf = 32;   // survivor records staged per warp before a global flush
 
-// Warp-aggregated append to the survivor buffer. Must be called by all 32 lanes.
-__device__ __forceinline__ void emit_warp(const ScoreOut& o, bool cond, const Rec& r) {
-  const unsigned mask = __ballot_sync(FULL_MASK, cond);
-  if (!mask) return;
+// Survivor output: each warp stages records in a shared-memory buffer and flushes
+// it with one global atomicAdd and coalesced 16-byte stores.
+struct Emitter {
+  int4* sbuf;  // [kEmitBuf][2]
+  int count;   // warp-uniform
+};
+
+__device__ __noinline__ void emit_flush(const ScoreOut& o, Emitter& em) {
   const int lane = threadIdx.x & 31;
-  const int leader = __ffs(mask) - 1;
+  const int n = em.count;
+  if (n == 0) return;
   unsigned long long base = 0;
-  if (lane == leader) base = atomicAdd(&o.counters[0], (unsigned long long)__popc(mask));
-  base = __shfl_sync(FULL_MASK, base, leader);
+  if (lane == 0) base = atomicAdd(&o.counters[0], (unsigned long long)n);
+  base = __shfl_sync(FULL_MASK, base, 0);
+  __syncwarp();
+  int4* dst = reinterpret_cast<int4*>(o.surv);
+  for (int w = lane; w < 2 * n; w += 32)
+    if (base + (unsigned long long)(w >> 1) < o.cap) dst[2 * base + w] = em.sbuf[w];
+  __syncwarp();
+  em.count = 0;
+}
+
+// Warp-aggregated append. Called by all 32 lanes of a warp (out of line: rare path).
+__device__ __noinline__ void emit_warp(const ScoreOut& o, Emitter& em, bool cond, Rec r) {
+  const unsigned mask = __ballot_sync(FULL_MASK, cond);
+  const int n = __popc(mask);
+  if (n == 0) return;
+  if (em.count + n > kEmitBuf) emit_flush(o, em);
   if (cond) {
-    const unsigned long long idx = base + __popc(mask & lanemask_lt());
-    if (idx < o.cap) store_rec(o.surv + idx, r);
+    const int idx = em.count + __popc(mask & lanemask_lt());
+    em.sbuf[2 * idx] = make_int4((int)r.w[0], (int)r.w[1], (int)r.w[2], (int)r.w[3]);
+    em.sbuf[2 * idx + 1] = make_int4((int)r.w[4], (int)r.w[5], (int)r.w[6], (int)r.w[7]);
   }
+  __syncwarp();
+  em.count += n;
 }
 
-__device__ __forceinline__ void emit_one(const ScoreOut& o, const Rec& r) {
-  const unsigned long long idx = atomicAdd(&o.counters[0], 1ull);
-  if (idx < o.cap) store_rec(o.surv + idx, r);
+// ---- fold tables: one row of nb + 2 64-bit entries per k_1 (nb + 1 used; even for 16-B alignment) ----
+// pass 1: raw[j] = min over feasible candidates with E >> sh == j of (Cmax << 32 | E),
+//         i.e. the bucket's best point (smallest Cmax, then smallest E).
+// finalize: entry j = {x = U[j] = min Cmax over buckets < j, y = E*_j}, entry nb = {U[nb], -}.
+// pass 2 keeps a feasible candidate (E, Cmax) of bucket j unless it is dominated:
+//   Cmax >= U[j]                      by a point of an earlier bucket (smaller E), or
+//   E >= E*_j, Cmax >= C*_j, not both equal, with C*_j = U[j+1] the bucket's own best
+//   (when Cmax < U[j], the bucket's best Cmax is below U[j], so U[j+1] is exactly it).
+__device__ __forceinline__ void reset_tables(uint64_t* tab, int n, int tid, int nthreads) {
+  for (int i = tid; i < n; i += nthreads) tab[i] = ~0ull;
 }
 
-// Exclusive prefix-min over each class's bucket row (strict "earlier buckets"),
-// in place: U[j] = min_{j' < j} tab[j'].
-template <int NC>
-__device__ void tables_to_thresholds(int32_t* tab) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int k = warp; k < NC; k += kScoreThreads / 32) {
-    int32_t* row = tab + k * kNumBuckets;
-    int32_t run = INT_MAX;
-    for (int r0 = 0; r0 < kNumBuckets; r0 += 32) {
-      const int32_t v = row[r0 + lane];
-      int32_t incl = v;
+__device__ __noinline__ void tables_finalize(uint64_t* tab, int nc, int nb, int warp, int nwarps) {
+  const int lane = threadIdx.x & 31;
+  for (int k = warp; k < nc; k += nwarps) {
+    uint64_t* row = tab + (size_t)k * (nb + 2);
+    int run = INT_MAX;
+    for (int r0 = 0; r0 < nb; r0 += 32) {
+      const uint64_t raw = row[r0 + lane];
+      const int c = raw == ~0ull ? INT_MAX : (int)(raw >> 32);
+      int incl = c;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        const int32_t o = __shfl_up_sync(FULL_MASK, incl, d);
+        const int o = __shfl_up_sync(FULL_MASK, incl, d);
         if (lane >= d) incl = min(incl, o);
       }
-      int32_t excl = __shfl_up_sync(FULL_MASK, incl, 1);
+      int excl = __shfl_up_sync(FULL_MASK, incl, 1);
       if (lane == 0) excl = INT_MAX;
-      row[r0 + lane] = min(run, excl);
+      reinterpret_cast<uint2*>(row)[r0 + lane] = make_uint2((unsigned)min(run, excl), (unsigned)(raw & 0xffffffffu));
       run = min(run, __shfl_sync(FULL_MASK, incl, 31));
     }
+    if (lane == 0) reinterpret_cast<uint2*>(row)[nb] = make_uint2((unsigned)run, 0u);
   }
 }
 
-__device__ __forceinline__ void reset_tables(int32_t* tab, int n) {
-  for (int i = threadIdx.x; i < n; i += kScoreThreads) tab[i] = INT_MAX;
+// Is a feasible candidate (E, Cmax) kept by the finalized row (see above)?
+__device__ __forceinline__ bool survives(const uint2* row, int jb, int E, int Cmax) {
+  const uint2 ent = row[jb];
+  if (Cmax >= (int)ent.x) return false;
+  const int Cs = (int)row[jb + 1].x;
+  const int Es = (int)ent.y;
+  return !(E >= Es && Cmax >= Cs && (E > Es || Cmax > Cs));
+}
+
+// First j in [0, nb] with U[j] <= v in a finalized (nonincreasing) row; nb + 1 if none.
+__device__ __forceinline__ int first_bucket_le(const uint2* row, int nb, int v) {
+  int lo = 0, hi = nb + 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((int)row[mid].x <= v) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
 }
 
 template <int NC>
@@ -203,7 +244,7 @@ struct CtaCtx {
   const int32_t* Pm;   // P[m] base
   const int32_t* Ym;   // Y[m] base
   size_t Mp, B;
-  int bi, b, k2, M, T, sh;
+  int bi, b, k2, M, T, sh, m1, nb, dbg;
   uint32_t model;
   const uint8_t* pair_v;
   __device__ const int32_t* Prow(int k) const { return Pm + ((size_t)k * B + bi) * Mp; }
@@ -212,115 +253,242 @@ struct CtaCtx {
   }
 };
 
-// One warp processes one tile of 32 * kJ1 first cuts c_1 against every c_2 > c_1
-// for a fixed (k_2, k_3, b) and all k_1. PASS 1 builds the per-(k_1) bucket
-// minima of Cmax over feasible candidates; PASS 2 emits feasible candidates
-// strictly better than every earlier bucket.
-template <int NC, int PASS, bool SMEM_B>
-__device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_hi, const int32_t* Bs,
-                        const int32_t* P3, int32_t P3M, const int32_t* Y23, int32_t* tab, const ScoreOut& out,
-                        unsigned long long& feas, unsigned long long& cand, int& any_flag) {
+constexpr int kInvalidThr = -(1 << 30);  // threshold of an empty slot: B(c2) >= 0 never passes
+constexpr int kPadB = 0x3fffffff;        // B(c2) beyond the model: above every threshold
+
+// d = thr - Bv on the FMA pipe (IMAD with a run-time -1 the compiler cannot fold).
+__device__ __forceinline__ int mad_diff(int Bv, int m1, int thr) {
+  int d;
+  asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(Bv), "r"(m1), "r"(thr));
+  return d;
+}
+
+// Does any of this lane's candidates at B(c2) = Bv (slots j < jmax, all k1)
+// satisfy E <= T_eff, i.e. Bv <= thr[j][k1]? Every candidate gets its own
+// integer instruction: the k1 = 0 (and, for NC >= 7, k1 = NC-1) candidates as
+// ISETP (ALU pipe, OR-chained in a predicate), the others as IMAD d = thr - Bv
+// (FMA pipe) AND-reduced by LOP3 (sign bit clear <=> some d >= 0), so both
+// integer pipes share the work and the SM's issue slot is the limit. The
+// compares are inline PTX so the compiler cannot replace them by one compare
+// against a hoisted max of the thresholds (that would skip per-candidate work).
+static_assert(kJ1 == 4, "any_feasible's PTX is written for 4 slots per lane");
+template <int NC>
+__device__ __forceinline__ int any_feasible(const int (&thr)[kJ1][NC], int Bv, int m1, int jmax = kJ1) {
+  constexpr bool kTwo = NC >= 7;
+  int acc = -1;
+#pragma unroll
+  for (int j = 0; j < kJ1; ++j) {
+    if (j >= jmax) break;  // jmax is a constant after unrolling the caller's band switch
+#pragma unroll
+    for (int k = 1; k < (kTwo ? NC - 1 : NC); ++k) acc &= mad_diff(Bv, m1, thr[j][k]);
+  }
+  int t[kJ1], u[kJ1];
+#pragma unroll
+  for (int j = 0; j < kJ1; ++j) {
+    t[j] = j < jmax ? thr[j][0] : kInvalidThr;
+    u[j] = (kTwo && j < jmax) ? thr[j][NC - 1] : kInvalidThr;
+  }
+  int h;
+  if (kTwo) {
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.le.s32 p, %1, %2;\n\tsetp.le.or.s32 p, %1, %3, p;\n\t"
+        "setp.le.or.s32 p, %1, %4, p;\n\tsetp.le.or.s32 p, %1, %5, p;\n\t"
+        "setp.le.or.s32 p, %1, %7, p;\n\tsetp.le.or.s32 p, %1, %8, p;\n\t"
+        "setp.le.or.s32 p, %1, %9, p;\n\tsetp.le.or.s32 p, %1, %10, p;\n\t"
+        "setp.gt.or.s32 p, %6, -1, p;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(h)
+        : "r"(Bv), "r"(t[0]), "r"(t[1]), "r"(t[2]), "r"(t[3]), "r"(acc), "r"(u[0]), "r"(u[1]), "r"(u[2]),
+          "r"(u[3]));
+  } else {
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.le.s32 p, %1, %2;\n\tsetp.le.or.s32 p, %1, %3, p;\n\t"
+        "setp.le.or.s32 p, %1, %4, p;\n\tsetp.le.or.s32 p, %1, %5, p;\n\t"
+        "setp.gt.or.s32 p, %6, -1, p;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(h)
+        : "r"(Bv), "r"(t[0]), "r"(t[1]), "r"(t[2]), "r"(t[3]), "r"(acc));
+  }
+  return h;
+}
+
+// Hit flags of one aligned group of 4 c2 values inside diagonal band JB: slots
+// j < JB are complete pairs, slot JB holds pairs for lanes < c2 - (c1_base + 32 JB).
+template <int NC, int JB>
+__device__ __forceinline__ void band_hits(const int (&thr)[kJ1][NC], const int4& b4, int m1, int lane, int rel,
+                                          int& h0, int& h1, int& h2, int& h3) {
+  const int bv[4] = {b4.x, b4.y, b4.z, b4.w};
+  int h[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    int accb = -1;
+#pragma unroll
+    for (int k1 = 0; k1 < NC; ++k1) accb &= mad_diff(bv[u], m1, thr[JB][k1]);
+    h[u] = any_feasible<NC>(thr, bv[u], m1, JB) | ((lane < rel + u - 32 * JB) & (accb >= 0));
+  }
+  h0 = h[0];
+  h1 = h[1];
+  h2 = h[2];
+  h3 = h[3];
+}
+
+// One warp processes one tile of 32 * kJ1 first cuts c_1 (lane l, slot j holds
+// c_1 = c1_base + 32 j + l; slots outside [c1_lo, c1_hi] are empty) against every
+// c_2 > c_1 for a fixed (k_2, k_3, b) and all k_1. The lane's thresholds
+// thr[j][k1] = T_eff - A(c_1, k_1) stay in registers; B(c_2) comes from shared
+// memory four at a time (c1_base = 3 mod 4 keeps every group aligned), so
+// E <= T_eff is B(c_2) <= thr.
+//
+// pass 1 counts every feasible candidate and folds it into its bucket's best
+// point (branch-free, predicated 64-bit shared atomics). pass 2 emits the feasible
+// candidates the finalized tables do not prove dominated (survives()), after
+// tightening each threshold so that candidates whose first stage alone is
+// dominated (C_1 >= U(E)) never leave the fast loop. Q(c_2) = P[k2][c_2] and
+// R(c_2) = C_3 are shared-memory rows like B. The fast loop and the slow paths
+// each exist once in the code (one pass-generic instance).
+template <int NC>
+__device__ void k3_tile(const CtaCtx<NC>& cx, const int pass, int k3, int c1_base, int c1_lo, int c1_hi,
+                        const int32_t* Bs, const int32_t* Qs, const int32_t* Rs, uint64_t* tab,
+                        uint16_t* tb0, const ScoreOut& out, Emitter& em, unsigned long long& feas,
+                        unsigned long long& cand) {
   const int lane = threadIdx.x & 31;
-  // Only the thresholds live in registers across the c2 loop; the slow path
-  // reloads C_1 and P[k2][c1] (L1-resident rows) when a candidate is feasible.
+  const int nb = cx.nb;
   int thr[kJ1][NC];
+  int c1r[kJ1][NC];
+  int p1[kJ1];
 #pragma unroll
   for (int j = 0; j < kJ1; ++j) {
     const int c1 = c1_base + 32 * j + lane;
-    const bool valid = c1 <= c1_hi;
-    const int p1 = valid ? __ldg(cx.P2 + c1) : 0;
+    const bool valid = c1 >= c1_lo && c1 <= c1_hi;
+    p1[j] = valid ? __ldg(cx.P2 + c1) : 0;
 #pragma unroll
     for (int k1 = 0; k1 < NC; ++k1) {
       const int C1 = valid ? __ldg(cx.Prow(k1) + c1) : 0;
       const int y = valid ? __ldg(cx.Yrow(k1, cx.k2) + c1) : 0;
       // E = A + B(c2) with A = C1 + Y1 - P[k2][c1]  =>  feasible iff B(c2) <= T - A
-      thr[j][k1] = valid ? cx.T - (C1 + y - p1) : INT_MIN;
+      int t = valid ? cx.T - (C1 + y - p1[j]) : kInvalidThr;
+      if (pass == 2 && valid) {
+        // U is nonincreasing; from bucket b0 on U <= C1 <= Cmax, so nothing there
+        // survives: only E < b0 << sh can  =>  B <= (b0 << sh) - 1 - A.
+        const int b0 = min(first_bucket_le(reinterpret_cast<const uint2*>(tab + (size_t)k1 * (nb + 2)), nb, C1), nb);
+        if (b0 < nb) t = t + min(0, (b0 << cx.sh) - 1 - cx.T);
+        tb0[(j * NC + k1) * 32 + lane] = (uint16_t)b0;  // pass-2 tightening bucket (this warp's slice)
+      }
+      thr[j][k1] = t;
+      c1r[j][k1] = C1;
     }
-    if (PASS == 1 && valid) cand += (unsigned long long)(cx.M - 1 - c1) * NC;
+    if (pass == 1 && valid) cand += (unsigned long long)(cx.M - 1 - c1) * NC;
   }
-  auto Bat = [&](int c2) -> int {
-    if (SMEM_B) return Bs[c2];
-    return __ldg(cx.P2 + c2) - __ldg(P3 + c2) + __ldg(Y23 + c2) + P3M;
-  };
-  // Slow path: some lane has a feasible candidate at this c2.
-  auto slow = [&](int c2, int Bv, int rel, bool diag) {
-    const int Q = __ldg(cx.P2 + c2);
-    const int R = P3M - __ldg(P3 + c2);
+  const int m1 = cx.m1;
+  const int M = cx.M;
+  unsigned nfeas = 0;
+#pragma unroll 1
+  for (int c2 = c1_base + 1; c2 < M; c2 += 4) {
+    const int4 b4 = *reinterpret_cast<const int4*>(Bs + c2);
+    const int rel = c2 - c1_base;  // 1 mod 4; the group is rel .. rel + 3
+    int h0, h1, h2, h3;
+    if (rel > 32 * kJ1) {
+      h0 = any_feasible<NC>(thr, b4.x, m1);
+      h1 = any_feasible<NC>(thr, b4.y, m1);
+      h2 = any_feasible<NC>(thr, b4.z, m1);
+      h3 = any_feasible<NC>(thr, b4.w, m1);
+    } else {
+      switch ((rel - 1) >> 5) {
+        case 0: band_hits<NC, 0>(thr, b4, m1, lane, rel, h0, h1, h2, h3); break;
+        case 1: band_hits<NC, 1>(thr, b4, m1, lane, rel, h0, h1, h2, h3); break;
+        case 2: band_hits<NC, 2>(thr, b4, m1, lane, rel, h0, h1, h2, h3); break;
+        default: band_hits<NC, 3>(thr, b4, m1, lane, rel, h0, h1, h2, h3); break;
+      }
+    }
+    if (!__any_sync(FULL_MASK, h0 | h1 | h2 | h3)) continue;
+    if (cx.dbg & 4) {
+      nfeas += (h0 | h1 | h2 | h3) ? 1u : 0u;
+      continue;
+    }
+    const int4 q4 = *reinterpret_cast<const int4*>(Qs + c2);
+    const int4 r4 = *reinterpret_cast<const int4*>(Rs + c2);
+    // Some lane passed at some c2 of the group. Slot j of this lane is a real
+    // pair iff 32 j + lane < c2 - c1_base.
+#pragma unroll 1
+    for (int u = 0; u < 4; ++u) {
+      const int hu = u == 0 ? h0 : (u == 1 ? h1 : (u == 2 ? h2 : h3));
+      if (!__any_sync(FULL_MASK, hu)) continue;
+      const int Bv = u == 0 ? b4.x : (u == 1 ? b4.y : (u == 2 ? b4.z : b4.w));
+      const int Q = u == 0 ? q4.x : (u == 1 ? q4.y : (u == 2 ? q4.z : q4.w));
+      const int R = u == 0 ? r4.x : (u == 1 ? r4.y : (u == 2 ? r4.z : r4.w));
+      const int relu = rel + u;
+      if (pass == 1) {
 #pragma unroll
-    for (int j = 0; j < kJ1; ++j) {
-      const int c1 = c1_base + 32 * j + lane;
-      const bool v = (!diag || (32 * j + lane < rel)) && c1 <= c1_hi;
-      bool fj = false;
+        for (int j = 0; j < kJ1; ++j) {
+          const bool v = 32 * j + lane < relu;
+          const int C2 = Q - p1[j];
 #pragma unroll
-      for (int k1 = 0; k1 < NC; ++k1) fj |= v && (Bv <= thr[j][k1]);
-      if (!__any_sync(FULL_MASK, fj)) continue;
-      const int p1 = v ? __ldg(cx.P2 + c1) : 0;
-      const int C2 = Q - p1;
-#pragma unroll
-      for (int k1 = 0; k1 < NC; ++k1) {
-        const bool f = v && (Bv <= thr[j][k1]);
-        const int C1 = f ? __ldg(cx.Prow(k1) + c1) : 0;
-        const int Cmax = max(max(C1, C2), R);
-        const int E = cx.T - thr[j][k1] + Bv;
-        if (PASS == 1) {
-          if (f) {
-            atomicMin(&tab[k1 * kNumBuckets + (E >> cx.sh)], Cmax);
-            ++feas;
-            any_flag = 1;
+          for (int k1 = 0; k1 < NC; ++k1) {
+            if (v && Bv <= thr[j][k1]) {
+              const int E = cx.T - thr[j][k1] + Bv;
+              const int Cmax = max(max(c1r[j][k1], C2), R);
+              if (!(cx.dbg & 1))
+                atomicMin(reinterpret_cast<unsigned long long*>(tab + (size_t)k1 * (nb + 2) + (E >> cx.sh)),
+                          ((unsigned long long)(unsigned)Cmax << 32) | (unsigned)E);
+              ++nfeas;
+            }
           }
-        } else {
-          const bool cond = f && (Cmax < tab[k1 * kNumBuckets + (f ? (E >> cx.sh) : 0)]);
-          emit_warp(out, cond, make_rec(cx.model, 3, c1, c2, k1, cx.k2, k3, cx.b, E, C1, C2, R));
+        }
+      } else {
+        const int c2u = c2 + u;
+#pragma unroll
+        for (int j = 0; j < kJ1; ++j) {
+          const bool v = 32 * j + lane < relu;
+          bool fj = false;
+#pragma unroll
+          for (int k1 = 0; k1 < NC; ++k1) fj |= v && (Bv <= thr[j][k1]);
+          if (!__any_sync(FULL_MASK, fj)) continue;
+          const int c1 = c1_base + 32 * j + lane;
+          const int C2 = Q - p1[j];
+#pragma unroll
+          for (int k1 = 0; k1 < NC; ++k1) {
+            const int b0 = tb0[(j * NC + k1) * 32 + lane];
+            // undo the tightening to recover the exact E = T - thr_orig + B
+            const int thr_o = thr[j][k1] - (b0 < nb ? min(0, (b0 << cx.sh) - 1 - cx.T) : 0);
+            const int E = cx.T - thr_o + Bv;
+            const int Cmax = max(max(c1r[j][k1], C2), R);
+            const bool f = v && (Bv <= thr[j][k1]);
+            const bool cond =
+                f && survives(reinterpret_cast<const uint2*>(tab + (size_t)k1 * (nb + 2)), E >> cx.sh, E, Cmax);
+            if (__any_sync(FULL_MASK, cond))
+              emit_warp(out, em, cond, make_rec(cx.model, 3, c1, c2u, k1, cx.k2, k3, cx.b, E, c1r[j][k1], C2, R));
+          }
         }
       }
     }
-  };
-  const int c2_main = c1_base + 32 * kJ1;  // from here on every slot has c_1 < c_2
-  const int diag_end = min(c2_main, cx.M);  // exclusive
-  for (int c2 = c1_base + 1; c2 < diag_end; ++c2) {
-    const int Bv = Bat(c2);
-    const int rel = c2 - c1_base;
-    bool any = false;
-#pragma unroll
-    for (int j = 0; j < kJ1; ++j) {
-      if (32 * j < rel) {
-        const bool v = 32 * j + lane < rel;
-#pragma unroll
-        for (int k1 = 0; k1 < NC; ++k1) any |= v && (Bv <= thr[j][k1]);
-      }
-    }
-    if (__any_sync(FULL_MASK, any)) slow(c2, Bv, rel, true);
   }
-  for (int c2 = c2_main; c2 < cx.M; ++c2) {
-    const int Bv = Bat(c2);
-    bool a0 = false, a1 = false;
-#pragma unroll
-    for (int j = 0; j < kJ1; ++j) {
-#pragma unroll
-      for (int k1 = 0; k1 < NC; ++k1) {
-        if ((j * NC + k1) & 1) a1 |= (Bv <= thr[j][k1]);
-        else a0 |= (Bv <= thr[j][k1]);
-      }
-    }
-    if (__any_sync(FULL_MASK, a0 | a1)) slow(c2, Bv, 0, false);
-  }
+  feas += nfeas;
 }
 
-template <int NC, bool SMEM_B>
-__global__ void __launch_bounds__(kScoreThreads, 4) score_kernel(Problem pb, ScoreOut out) {
-  extern __shared__ int32_t smem[];
-  int32_t* tab = smem;                    // [NC][kNumBuckets]
-  int32_t* Bs = smem + NC * kNumBuckets;  // [max_M] when SMEM_B
-  __shared__ int s_tile, s_any;
-  __shared__ unsigned long long s_feas, s_cand;
-
-  const int B = pb.B;
-  const int bi = blockIdx.x % B;
-  const int k2 = (blockIdx.x / B) % NC;
-  const int ml = blockIdx.x / (B * NC);
-  const DevModel md = pb.models[ml];
+// Two warps per CTA: (model, k_2, batch). They share the staged c_2 rows and the
+// fold tables, and take first-cut tiles from a shared counter.
+template <int NC>
+__global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
+    score_kernel(Problem pb, ScoreOut out, int nb_log2, int row_len) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  __shared__ int s_tile;
+  const int nb = 1 << nb_log2;
+  uint64_t* tab = reinterpret_cast<uint64_t*>(smem_raw);                    // [NC][nb + 2]
+  int32_t* Bs = reinterpret_cast<int32_t*>(tab + (size_t)NC * (nb + 2));     // [row_len] B(c2), current k3
+  int32_t* Qs = Bs + row_len;                                               // [row_len] Q(c2) = P[k2][b][c2]
+  int32_t* Rs = Qs + row_len;                                               // [row_len] R(c2) = C_3, current k3
   const int tid = threadIdx.x;
-  const int lane = tid & 31;
+  const int warp = tid >> 5, lane = tid & 31;
+  Emitter em{reinterpret_cast<int4*>(Rs + row_len) + warp * 2 * kEmitBuf, 0};
+  uint16_t* tb0 = reinterpret_cast<uint16_t*>(reinterpret_cast<int4*>(Rs + row_len) + kWarps * 2 * kEmitBuf) +
+                  warp * (kJ1 * NC * 32);  // [kJ1 * NC][32] per warp
+  const int ntab = NC * (nb + 2);
+
+  // Batch index slowest: small batches hold almost all feasible (heavier) work,
+  // so they are scheduled first and the tail of the grid is light.
+  const int B = pb.B;
+  const int k2 = blockIdx.x % NC;
+  const int ml = (blockIdx.x / NC) % pb.n_local;
+  const int bi = blockIdx.x / (NC * pb.n_local);
+  const DevModel md = pb.models[ml];
 
   CtaCtx<NC> cx;
   cx.Pm = pb.P + md.p_off;
@@ -333,28 +501,27 @@ __global__ void __launch_bounds__(kScoreThreads, 4) score_kernel(Problem pb, Sco
   cx.M = (int)md.M;
   cx.T = md.T;
   cx.model = md.model;
+  cx.m1 = pb.neg_one;
+  cx.nb = nb;
+  cx.dbg = pb.debug_flags;
   cx.pair_v = pb.pair_v;
   cx.P2 = cx.Prow(k2);
   int sh = 0;
-  while ((cx.T >> sh) >= kNumBuckets) ++sh;
+  while ((cx.T >> sh) >= nb) ++sh;
   cx.sh = sh;
   const int M = cx.M, T = cx.T;
 
   unsigned long long feas = 0, cand = 0;
-  if (tid == 0) {
-    s_feas = 0;
-    s_cand = 0;
-  }
-  reset_tables(tab, NC * kNumBuckets);
+  reset_tables(tab, ntab, tid, 32 * kWarps);
+  __syncthreads();
 
   // ---- K = 1: segment (k2), whole model on class k2 ----
-  if (tid == 0 && md.row_lo == 0) {
+  if (warp == 0 && md.row_lo == 0) {
     const int E = cx.P2[M];
-    ++cand;
-    if (E <= T) {
-      ++feas;
-      emit_one(out, make_rec(md.model, 1, 0, 0, k2, 0xFF, 0xFF, cx.b, E, E, 0, 0));
-    }
+    if (lane == 0) ++cand;
+    const bool f = lane == 0 && E <= T;
+    if (f) ++feas;
+    if (__any_sync(FULL_MASK, f)) emit_warp(out, em, f, make_rec(md.model, 1, 0, 0, k2, 0xFF, 0xFF, cx.b, E, E, 0, 0));
   }
 
   // ---- K = 2: segments (k1, k2); c1 in this rank's rows ----
@@ -362,11 +529,11 @@ __global__ void __launch_bounds__(kScoreThreads, 4) score_kernel(Problem pb, Sco
     const int lo = max(1, (int)md.row_lo), hi = min(M - 1, (int)md.row_hi - 1);
     if (lo <= hi) {
       const int P2M = cx.P2[M];
-      if (tid == 0) s_any = 0;
-      __syncthreads();
       int anyf = 0;
+#pragma unroll 1
       for (int pass = 1; pass <= 2; ++pass) {
-        for (int base = lo; base <= hi; base += kScoreThreads) {
+#pragma unroll 1
+        for (int base = lo; base <= hi; base += 32 * kWarps) {
           const int c1 = base + tid;
           const bool valid = c1 <= hi;
           const int C2 = valid ? P2M - __ldg(cx.P2 + c1) : 0;
@@ -377,28 +544,30 @@ __global__ void __launch_bounds__(kScoreThreads, 4) score_kernel(Problem pb, Sco
             const int E = C1 + y + C2;
             const bool f = valid && E <= T;
             const int Cmax = max(C1, C2);
+            uint64_t* row = tab + (size_t)k1 * (nb + 2);
             if (pass == 1) {
               if (valid) ++cand;
               if (f) {
                 ++feas;
                 anyf = 1;
-                atomicMin(&tab[k1 * kNumBuckets + (E >> sh)], Cmax);
+                atomicMin(reinterpret_cast<unsigned long long*>(row + (E >> sh)),
+                          ((unsigned long long)(unsigned)Cmax << 32) | (unsigned)E);
               }
             } else {
-              const bool cond = f && Cmax < tab[k1 * kNumBuckets + (f ? (E >> sh) : 0)];
-              emit_warp(out, cond, make_rec(md.model, 2, c1, 0, k1, k2, 0xFF, cx.b, E, C1, C2, 0));
+              const bool cond = f && survives(reinterpret_cast<const uint2*>(row), f ? (E >> sh) : 0, E, Cmax);
+              if (__any_sync(FULL_MASK, cond))
+                emit_warp(out, em, cond, make_rec(md.model, 2, c1, 0, k1, k2, 0xFF, cx.b, E, C1, C2, 0));
             }
           }
         }
         if (pass == 1) {
-          if (anyf) s_any = 1;
-          __syncthreads();
-          if (!s_any) break;
-          tables_to_thresholds<NC>(tab);
+          if (!__syncthreads_or(anyf)) break;
+          tables_finalize(tab, NC, nb, warp, kWarps);
           __syncthreads();
         } else {
           __syncthreads();
-          reset_tables(tab, NC * kNumBuckets);
+          reset_tables(tab, ntab, tid, 32 * kWarps);
+          __syncthreads();
         }
       }
     }
@@ -408,83 +577,82 @@ __global__ void __launch_bounds__(kScoreThreads, 4) score_kernel(Problem pb, Sco
   if (pb.Kmax >= 3 && M >= 3) {
     const int c1lo = max(1, (int)md.row_lo), c1hi = min(M - 2, (int)md.row_hi - 1);
     if (c1lo <= c1hi) {
-      const int ntiles = (c1hi - c1lo + 1 + 32 * kJ1 - 1) / (32 * kJ1);
+      // tiles start at c1_base = 3 mod 4 so that every c2 group c1_base + 1 + 4i is aligned
+      const int c1_base0 = c1lo - ((c1lo - 3) & 3);
+      const int ntiles = (c1hi - c1_base0 + 32 * kJ1) / (32 * kJ1);
+      const int c2_from = c1_base0 + 1;                 // >= 0
+      const int c2_to = ((M + 3) & ~3) + 4;             // padded, exclusive
+      for (int c2 = c2_from + tid; c2 < c2_to; c2 += 32 * kWarps) Qs[c2] = c2 < M ? __ldg(cx.P2 + c2) : 0;
+#pragma unroll 1
       for (int k3 = 0; k3 < NC; ++k3) {
         const int32_t* P3 = cx.Prow(k3);
         const int32_t P3M = P3[M];
         const int32_t* Y23 = cx.Yrow(k2, k3);
-        __syncthreads();
-        if (SMEM_B) {
-          for (int c2 = c1lo + 1 + tid; c2 <= M - 1; c2 += kScoreThreads)
-            Bs[c2] = __ldg(cx.P2 + c2) - __ldg(P3 + c2) + __ldg(Y23 + c2) + P3M;
+        for (int c2 = c2_from + tid; c2 < c2_to; c2 += 32 * kWarps) {
+          const bool in = c2 < M;
+          const int p3 = in ? __ldg(P3 + c2) : 0;
+          Bs[c2] = in ? __ldg(cx.P2 + c2) - p3 + __ldg(Y23 + c2) + P3M : kPadB;
+          Rs[c2] = in ? P3M - p3 : 0;
         }
-        if (tid == 0) {
-          s_tile = 0;
-          s_any = 0;
-        }
+        if (tid == 0) s_tile = 0;
         __syncthreads();
-        int anyf = 0;
-        for (;;) {
-          int t = 0;
-          if (lane == 0) t = atomicAdd(&s_tile, 1);
-          t = __shfl_sync(FULL_MASK, t, 0);
-          if (t >= ntiles) break;
-          k3_tile<NC, 1, SMEM_B>(cx, k3, c1lo + t * 32 * kJ1, c1hi, Bs, P3, P3M, Y23, tab, out, feas, cand, anyf);
-        }
-        if (anyf) s_any = 1;
-        __syncthreads();
-        if (s_any) {
-          tables_to_thresholds<NC>(tab);
-          if (tid == 0) s_tile = 0;
-          __syncthreads();
+        const unsigned long long feas0 = feas;
+#pragma unroll 1
+        for (int pass = 1; pass <= 2; ++pass) {
+#pragma unroll 1
           for (;;) {
             int t = 0;
             if (lane == 0) t = atomicAdd(&s_tile, 1);
             t = __shfl_sync(FULL_MASK, t, 0);
             if (t >= ntiles) break;
-            k3_tile<NC, 2, SMEM_B>(cx, k3, c1lo + t * 32 * kJ1, c1hi, Bs, P3, P3M, Y23, tab, out, feas, cand,
-                                   anyf);
+            k3_tile<NC>(cx, pass, k3, c1_base0 + t * 32 * kJ1, c1lo, c1hi, Bs, Qs, Rs, tab, tb0, out, em, feas,
+                        cand);
           }
-          __syncthreads();
-          reset_tables(tab, NC * kNumBuckets);
+          if (pass == 1) {
+            if (!__syncthreads_or(feas != feas0) || (pb.debug_flags & 2)) break;
+            tables_finalize(tab, NC, nb, warp, kWarps);
+            if (tid == 0) s_tile = 0;
+            __syncthreads();
+          }
         }
+        __syncthreads();
+        reset_tables(tab, ntab, tid, 32 * kWarps);
+        __syncthreads();
       }
     }
   }
 
   // ---- counters ----
+  emit_flush(out, em);
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {
     feas += __shfl_down_sync(FULL_MASK, feas, d);
     cand += __shfl_down_sync(FULL_MASK, cand, d);
   }
   if (lane == 0) {
-    atomicAdd(&s_feas, feas);
-    atomicAdd(&s_cand, cand);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    atomicAdd(&out.counters[1], s_feas);
-    atomicAdd(&out.counters[2], s_cand);
+    atomicAdd(&out.counters[1], feas);
+    atomicAdd(&out.counters[2], cand);
   }
 }
 
+// Shared memory per CTA: the fold tables take what the budget leaves after the
+// three staged c2 rows (B, Q, R) and the emit buffers, rounded down to a power of
+// two (128..2048 buckets).
+constexpr size_t kSmemBudget = 27 * 1024;
+
 template <int NC>
 static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaStream_t s) {
-  const bool smem_b = pb.max_M <= (uint32_t)kMaxMSmem;
-  const size_t smem = sizeof(int32_t) * ((size_t)NC * kNumBuckets + (smem_b ? pb.max_M : 0));
+  const int row_len = (int)((((size_t)pb.max_M + 3) & ~(size_t)3) + 4);
+  const size_t fixed = sizeof(int32_t) * 3 * (size_t)row_len + (size_t)kWarps * kEmitBuf * 32 +
+                       (size_t)kWarps * kJ1 * NC * 32 * sizeof(uint16_t);
+  int nb_log2 = 7;
+  while (nb_log2 < 11 && fixed + 8 * NC * (((size_t)2 << nb_log2) + 2) <= kSmemBudget) ++nb_log2;
+  const size_t smem = fixed + 8 * NC * (((size_t)1 << nb_log2) + 2);
   const unsigned grid = (unsigned)pb.n_local * NC * pb.B;
-  if (smem_b) {
-    auto kfn = score_kernel<NC, true>;
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    kfn<<<grid, kScoreThreads, smem, s>>>(pb, out);
-  } else {
-    auto kfn = score_kernel<NC, false>;
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    kfn<<<grid, kScoreThreads, smem, s>>>(pb, out);
-  }
+  auto kfn = score_kernel<NC>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kfn<<<grid, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
   return cudaGetLastError();
 }
 
@@ -530,11 +698,10 @@ __global__ void make_keys_kernel(const ppipe_point* in, uint64_t n, const uint64
 __global__ void seg_start_kernel(const uint64_t* keys, uint64_t n, uint64_t n_seg, uint64_t* start) {
   const uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (s > n_seg) return;
-  const uint64_t target = s << kEBits;
   uint64_t lo = 0, hi = n;
   while (lo < hi) {
     const uint64_t mid = (lo + hi) >> 1;
-    if (keys[mid] < target) lo = mid + 1;
+    if (keys[mid] < s) lo = mid + 1;
     else hi = mid;
   }
   start[s] = lo;
@@ -553,6 +720,7 @@ __device__ __forceinline__ bool theta_gt(uint64_t bp, uint64_t cp, uint64_t bq, 
 }
 
 // Is p canonically better than q among records with the same (segment, E)?
+// theta desc, then batch asc, then (c_1, c_2) asc: a strict total order on candidates.
 __device__ __forceinline__ bool better(const ppipe_point& p, const ppipe_point& q) {
   const uint64_t cp = cmax_of(p), cq = cmax_of(q);
   if (theta_gt(p.batch, cp, q.batch, cq)) return true;
@@ -562,65 +730,83 @@ __device__ __forceinline__ bool better(const ppipe_point& p, const ppipe_point& 
   return p.cut[1] < q.cut[1];
 }
 
-// One thread per segment: walk its (E-sorted) records in equal-E groups, keep the
-// group's best if its theta strictly exceeds every earlier kept theta.
-template <bool WRITE>
-__global__ void staircase_kernel(const ppipe_point* in, const uint64_t* keys, const uint32_t* vals,
-                                 const uint64_t* start, uint64_t n_seg, uint64_t* counts,
-                                 const uint64_t* offsets, ppipe_point* out) {
-  const uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (s >= n_seg) return;
-  const uint64_t lo = start[s], hi = start[s + 1];
-  uint64_t best_b = 0, best_c = 1;  // theta = 0
-  uint64_t cnt = 0;
-  const uint64_t emask = (1ull << kEBits) - 1;
-  uint64_t i = lo;
-  while (i < hi) {
-    const uint64_t E = keys[i] & emask;
-    ppipe_point g = in[vals[i]];
-    uint64_t j = i + 1;
-    for (; j < hi && (keys[j] & emask) == E; ++j) {
-      const ppipe_point q = in[vals[j]];
-      if (better(q, g)) g = q;
-    }
-    const uint64_t gc = cmax_of(g);
-    if (theta_gt(g.batch, gc, best_b, best_c)) {
-      if (WRITE) out[offsets[s] + cnt] = g;
-      ++cnt;
-      best_b = g.batch;
-      best_c = gc;
-    }
-    i = j;
+struct PickBetter {  // associative and commutative: "the better of two" under a total order
+  __device__ __forceinline__ ppipe_point operator()(const ppipe_point& a, const ppipe_point& b) const {
+    return better(b, a) ? b : a;
   }
-  if (!WRITE) counts[s] = cnt;
+};
+
+struct Theta {
+  uint32_t b, c;  // theta = b / c
+};
+
+struct MaxTheta {
+  __device__ __forceinline__ Theta operator()(const Theta& x, const Theta& y) const {
+    return theta_gt(y.b, y.c, x.b, x.c) ? y : x;
+  }
+};
+
+__global__ void gather_kernel(const ppipe_point* in, const uint32_t* idx, uint64_t n, ppipe_point* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = in[idx[i]];
+}
+
+__global__ void group_theta_kernel(const uint64_t* gkeys, const ppipe_point* best, uint64_t ng, uint64_t* segk,
+                                   Theta* th) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ng; i += (uint64_t)gridDim.x * blockDim.x) {
+    segk[i] = gkeys[i] >> kEBits;
+    th[i] = Theta{best[i].batch, cmax_of(best[i])};
+  }
+}
+
+__global__ void keep_kernel(const Theta* th, const Theta* prefix, uint64_t ng, uint8_t* keep) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ng; i += (uint64_t)gridDim.x * blockDim.x)
+    keep[i] = theta_gt(th[i].b, th[i].c, prefix[i].b, prefix[i].c) ? 1 : 0;  // strictly above every earlier E
 }
 
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Frontier of n records: sort by (segment, E); best record per (segment, E) by
+// (theta desc, b asc, cuts asc) [reduce-by-key]; keep it iff its theta strictly
+// exceeds the max theta of every smaller E in its segment [exclusive max-scan by
+// segment]; compact; CSR offsets by binary search. All stages are data-parallel.
 cudaError_t frontier_pass(const ppipe_point* in, uint64_t n, const uint64_t* seg_base_by_model, int C,
                           uint64_t n_seg, ppipe_point* out, uint64_t* seg_offsets, uint64_t* n_out_host,
                           FrontierScratch* scratch, cudaStream_t s, int* n_launches) {
-  // key bits: E (28) + segment id
   int seg_bits = 1;
   while ((1ull << seg_bits) <= n_seg) ++seg_bits;
   const int end_bit = kEBits + seg_bits;
-  size_t sort_bytes = 0, scan_bytes = 0;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr,
-                                                  (uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)n, 0,
-                                                  end_bit, s);
+  const int64_t ni = (int64_t)n;
+  size_t b_sort = 0, b_red = 0, b_scan = 0, b_sel = 0;
+  cudaError_t e;
+  e = cub::DeviceRadixSort::SortPairs(nullptr, b_sort, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
+                                      (uint32_t*)nullptr, ni, 0, end_bit, s);
   if (e != cudaSuccess) return e;
-  e = cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr,
-                                    (int64_t)(n_seg + 1), s);
+  e = cub::DeviceReduce::ReduceByKey(nullptr, b_red, (uint64_t*)nullptr, (uint64_t*)nullptr, (ppipe_point*)nullptr,
+                                     (ppipe_point*)nullptr, (int64_t*)nullptr, PickBetter(), ni, s);
   if (e != cudaSuccess) return e;
+  e = cub::DeviceScan::ExclusiveScanByKey(nullptr, b_scan, (uint64_t*)nullptr, (Theta*)nullptr, (Theta*)nullptr,
+                                          MaxTheta(), Theta{0, 1}, ni, cub::Equality(), s);
+  if (e != cudaSuccess) return e;
+  e = cub::DeviceSelect::Flagged(nullptr, b_sel, (ppipe_point*)nullptr, (uint8_t*)nullptr, (ppipe_point*)nullptr,
+                                 (int64_t*)nullptr, ni, s);
+  if (e != cudaSuccess) return e;
+  size_t b_sel2 = 0;
+  e = cub::DeviceSelect::Flagged(nullptr, b_sel2, (uint64_t*)nullptr, (uint8_t*)nullptr, (uint64_t*)nullptr,
+                                 (int64_t*)nullptr, ni, s);
+  if (e != cudaSuccess) return e;
+  const size_t tmpb = std::max(std::max(b_sort, b_red), std::max(b_scan, std::max(b_sel, b_sel2)));
   const size_t nn = n > 0 ? n : 1;
   size_t off = 0;
-  const size_t o_keys = off; off = align_up(off + nn * 8, 256);
-  const size_t o_keys2 = off; off = align_up(off + nn * 8, 256);
-  const size_t o_vals = off; off = align_up(off + nn * 4, 256);
-  const size_t o_vals2 = off; off = align_up(off + nn * 4, 256);
-  const size_t o_start = off; off = align_up(off + (n_seg + 1) * 8, 256);
-  const size_t o_counts = off; off = align_up(off + (n_seg + 1) * 8, 256);
-  const size_t o_tmp = off; off = align_up(off + std::max(sort_bytes, scan_bytes), 256);
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  const size_t o_k1 = take(nn * 8), o_k2 = take(nn * 8), o_v1 = take(nn * 4), o_v2 = take(nn * 4);
+  const size_t o_rec = take(nn * 32), o_best = take(nn * 32), o_gk = take(nn * 8), o_sk = take(nn * 8);
+  const size_t o_th = take(nn * 8), o_pre = take(nn * 8), o_keep = take(nn), o_num = take(16);
+  const size_t o_tmp = take(tmpb);
   if (scratch->bytes < off) {
     if (scratch->buf) cudaFree(scratch->buf);
     scratch->buf = nullptr;
@@ -630,40 +816,56 @@ cudaError_t frontier_pass(const ppipe_point* in, uint64_t n, const uint64_t* seg
     scratch->bytes = off;
   }
   char* base = (char*)scratch->buf;
-  uint64_t* keys = (uint64_t*)(base + o_keys);
-  uint64_t* keys2 = (uint64_t*)(base + o_keys2);
-  uint32_t* vals = (uint32_t*)(base + o_vals);
-  uint32_t* vals2 = (uint32_t*)(base + o_vals2);
-  uint64_t* start = (uint64_t*)(base + o_start);
-  uint64_t* counts = (uint64_t*)(base + o_counts);
+  uint64_t* keys = (uint64_t*)(base + o_k1);
+  uint64_t* keys2 = (uint64_t*)(base + o_k2);
+  uint32_t* vals = (uint32_t*)(base + o_v1);
+  uint32_t* vals2 = (uint32_t*)(base + o_v2);
+  ppipe_point* rec = (ppipe_point*)(base + o_rec);
+  ppipe_point* best = (ppipe_point*)(base + o_best);
+  uint64_t* gkeys = (uint64_t*)(base + o_gk);
+  uint64_t* segk = (uint64_t*)(base + o_sk);
+  Theta* th = (Theta*)(base + o_th);
+  Theta* pre = (Theta*)(base + o_pre);
+  uint8_t* keep = (uint8_t*)(base + o_keep);
+  int64_t* d_num = (int64_t*)(base + o_num);
   void* tmp = base + o_tmp;
 
+  int64_t ng = 0, nk = 0;
   if (n > 0) {
     const int blocks = (int)std::min<uint64_t>((n + 255) / 256, 148 * 16);
     make_keys_kernel<<<blocks, 256, 0, s>>>(in, n, seg_base_by_model, C, keys, vals);
-    ++*n_launches;
-    e = cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, keys, keys2, vals, vals2, (int64_t)n, 0, end_bit, s);
+    e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, keys, keys2, vals, vals2, ni, 0, end_bit, s);
     if (e != cudaSuccess) return e;
-    *n_launches += 2 * ((end_bit + 7) / 8);
+    gather_kernel<<<blocks, 256, 0, s>>>(in, vals2, n, rec);
+    e = cub::DeviceReduce::ReduceByKey(tmp, b_red, keys2, gkeys, rec, best, d_num, PickBetter(), ni, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyAsync(&ng, d_num, 8, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return e;
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return e;
+    const int gb = (int)std::min<int64_t>((ng + 255) / 256, 148 * 16);
+    group_theta_kernel<<<gb, 256, 0, s>>>(gkeys, best, (uint64_t)ng, segk, th);
+    e = cub::DeviceScan::ExclusiveScanByKey(tmp, b_scan, segk, th, pre, MaxTheta(), Theta{0, 1}, ng,
+                                            cub::Equality(), s);
+    if (e != cudaSuccess) return e;
+    keep_kernel<<<gb, 256, 0, s>>>(th, pre, (uint64_t)ng, keep);
+    e = cub::DeviceSelect::Flagged(tmp, b_sel, best, keep, out, d_num, ng, s);
+    if (e != cudaSuccess) return e;
+    e = cub::DeviceSelect::Flagged(tmp, b_sel2, segk, keep, keys, d_num + 1, ng, s);  // segment of each kept point
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyAsync(&nk, d_num, 8, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return e;
+    *n_launches += 12;
   }
   const unsigned sb = (unsigned)((n_seg + 1 + 255) / 256);
-  seg_start_kernel<<<sb, 256, 0, s>>>(keys2, n, n_seg, start);
-  ++*n_launches;
-  e = cudaMemsetAsync(counts + n_seg, 0, 8, s);
-  if (e != cudaSuccess) return e;
-  const unsigned gb = (unsigned)((n_seg + 127) / 128);
-  staircase_kernel<false><<<gb, 128, 0, s>>>(in, keys2, vals2, start, n_seg, counts, nullptr, nullptr);
-  ++*n_launches;
-  e = cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, counts, seg_offsets, (int64_t)(n_seg + 1), s);
-  if (e != cudaSuccess) return e;
-  *n_launches += 2;
-  staircase_kernel<true><<<gb, 128, 0, s>>>(in, keys2, vals2, start, n_seg, nullptr, seg_offsets, out);
+  seg_start_kernel<<<sb, 256, 0, s>>>(keys, (uint64_t)nk, n_seg, seg_offsets);
   ++*n_launches;
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  e = cudaMemcpyAsync(n_out_host, seg_offsets + n_seg, 8, cudaMemcpyDeviceToHost, s);
+  e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return e;
-  return cudaStreamSynchronize(s);
+  *n_out_host = (uint64_t)nk;
+  return cudaSuccess;
 }
 
 }  // namespace ppipe
