@@ -27,7 +27,7 @@ sys.path.insert(0, ROOT)
 METRIC = "pipeline-plan candidates scored/sec at 1/2/4/8 B200; % of INT32 issue roofline"
 UNIT = "candidates/s"
 SM_COUNT = 148
-ALU_LANES_PER_CLK_PER_SM = 64  # alu pipe: 1 warp-instruction per 2 clk per SMSP
+ISSUE_LANES_PER_CLK_PER_SM = 128  # 4 SMSPs x 1 warp-instruction/clk x 32 lanes: integer issue ceiling
 
 
 def _peaks():
@@ -286,7 +286,7 @@ def main():
     achieved_local = ops_local / (kern_avg / 1000.0)
     peaks = _peaks()
     f_clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    peak_ops = SM_COUNT * ALU_LANES_PER_CLK_PER_SM * f_clk
+    peak_ops = SM_COUNT * ISSUE_LANES_PER_CLK_PER_SM * f_clk
     achieved = allsum(achieved_local) / world  # per-GPU average of per-launch rates
     traffic = None
     prof = os.path.join(ROOT, "profiles", "score_kernel_dram.json")
@@ -350,7 +350,8 @@ def main():
                      "frac": achieved / peak_ops, "traffic": traffic,
                      "kernel": "score_kernel", "kernel_ms": kern_max,
                      "ops_per_launch": "candidates + 3 x feasible (int32 lane-ops, DESIGN.md §5)",
-                     "peak_basis": f"{SM_COUNT} SMs x {ALU_LANES_PER_CLK_PER_SM} alu lanes/clk x "
+                     "frac_survey_w4": n_cand * 4 / (ms_per_step / 1000.0) / peak_ops,
+                     "peak_basis": f"{SM_COUNT} SMs x {ISSUE_LANES_PER_CLK_PER_SM} int lane-ops/clk (issue) x "
                                    f"{f_clk / 1e6:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"},
         "cpu_baseline": cpu,
         "e2e": e2e,
