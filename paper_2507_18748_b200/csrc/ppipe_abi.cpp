@@ -172,12 +172,15 @@ struct ppipe_ctx {
   DevBuf<uint64_t> d_segbase;
   // outputs
   DevBuf<unsigned long long> d_counters;
+  DevBuf<uint4> d_hot;
+  DevBuf<uint64_t> d_hot_tab;
+  uint64_t hot_cap = 0;
   DevBuf<ppipe_point> d_surv, d_local, d_gather, d_union, d_final;
   DevBuf<uint64_t> d_segoff_local, d_segoff_final, d_cnt_send, d_cnt_recv;
   FrontierScratch scratch;
   std::vector<ppipe_point> h_points;
   std::vector<uint64_t> h_segoff;
-  unsigned long long* h_counters = nullptr;  // pinned [3]
+  unsigned long long* h_counters = nullptr;  // pinned [5]
   // enumerate state
   bool enumerated = false;
   ppipe_enum_params last_params{};
@@ -233,6 +236,8 @@ void free_ctx(ppipe_ctx* c) {
   c->d_pairv.release();
   c->d_segbase.release();
   c->d_counters.release();
+  c->d_hot.release();
+  c->d_hot_tab.release();
   c->d_surv.release();
   c->d_local.release();
   c->d_gather.release();
@@ -443,7 +448,7 @@ PPIPE_API int ppipe_load_profiles(ppipe_ctx** out, uint32_t n_models, const ppip
       fail(c, PPIPE_ECUDA, "cudaEventCreate failed");
       return bail(PPIPE_ECUDA);
     }
-  if (cudaMallocHost(&c->h_counters, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+  if (cudaMallocHost(&c->h_counters, 5 * sizeof(unsigned long long)) != cudaSuccess) {
     fail(c, PPIPE_ENOMEM, "cudaMallocHost failed");
     return bail(PPIPE_ENOMEM);
   }
@@ -517,7 +522,7 @@ PPIPE_API int ppipe_load_profiles(ppipe_ctx** out, uint32_t n_models, const ppip
   CUL(c->d_bwv.reserve(c->V));
   CUL(c->d_pairv.reserve(pairv.size()));
   CUL(c->d_segbase.reserve(n_models));
-  CUL(c->d_counters.reserve(4));
+  CUL(c->d_counters.reserve(5));
   // host -> device: the profiles this rank needs
   for (size_t i = 0; i < c->local.size(); ++i) {
     const int m = c->local[i];
@@ -606,13 +611,21 @@ static int run_enumerate(ppipe_ctx* c) {
     const char* dbg = getenv("PPIPE_DEBUG_FLAGS");
     pb.debug_flags = dbg ? atoi(dbg) : 0;
   }
-  ScoreOut so{c->d_surv.p, c->d_counters.p, (unsigned long long)c->d_surv.n};
+  if (c->hot_cap == 0) {
+    const uint64_t units = (uint64_t)c->local.size() * c->C * c->C * c->B;
+    c->hot_cap = std::max<uint64_t>(1, std::min<uint64_t>(units, std::max<uint64_t>(4096, units / 8)));
+  }
+  const size_t tab_words = hot_unit_table_bytes(pb) / 8;
+  CU(c, c->d_hot.reserve(c->hot_cap));
+  CU(c, c->d_hot_tab.reserve(c->hot_cap * tab_words));
+  ScoreOut so{c->d_surv.p, c->d_counters.p, (unsigned long long)c->d_surv.n, c->d_hot.p, c->d_hot_tab.p,
+              (unsigned long long)c->hot_cap};
   c->launches_i = 0;
   CU(c, cudaEventRecord(c->ev[0], c->stream));
   CU(c, launch_pack(pb, c->stream));
   c->launches_i += pb.n_local ? 2 : 0;
   CU(c, cudaEventRecord(c->ev[1], c->stream));
-  CU(c, cudaMemsetAsync(c->d_counters.p, 0, 4 * sizeof(unsigned long long), c->stream));
+  CU(c, cudaMemsetAsync(c->d_counters.p, 0, 5 * sizeof(unsigned long long), c->stream));
   CU(c, launch_score(pb, so, c->stream, &c->launches_i));
   CU(c, cudaEventRecord(c->ev[2], c->stream));
   return PPIPE_OK;
@@ -647,11 +660,14 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
   CU(c, cudaSetDevice(c->device));
   // survivors; grow and re-run on overflow (deterministic, so the result is unchanged)
   for (;;) {
-    CU(c, cudaMemcpyAsync(c->h_counters, c->d_counters.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+    CU(c, cudaMemcpyAsync(c->h_counters, c->d_counters.p, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                           c->stream));
     CU(c, cudaStreamSynchronize(c->stream));
-    if (c->h_counters[0] <= c->d_surv.n) break;
-    c->surv_cap = c->h_counters[0] + c->h_counters[0] / 4 + 1024;
+    const bool surv_ok = c->h_counters[0] <= c->d_surv.n;
+    const bool hot_ok = c->h_counters[3] <= c->hot_cap;
+    if (surv_ok && hot_ok) break;
+    if (!surv_ok) c->surv_cap = c->h_counters[0] + c->h_counters[0] / 4 + 1024;
+    if (!hot_ok) c->hot_cap = c->h_counters[3] + c->h_counters[3] / 4 + 64;
     int rc = run_enumerate(c);
     if (rc != PPIPE_OK) return rc;
   }

@@ -51,9 +51,14 @@ struct Problem {
 
 struct ScoreOut {
   ppipe_point* surv;
-  unsigned long long* counters;  // [0] survivors, [1] feasible, [2] candidates
+  unsigned long long* counters;  // [0] survivors, [1] feasible, [2] candidates, [3] hot units, [4] pass-2 progress
   unsigned long long cap;
+  uint4* hot;                    // [hot_cap] (local model, k2, k3, batch index) of units with feasible candidates
+  uint64_t* hot_tab;             // [hot_cap][table words] their finalized fold tables
+  unsigned long long hot_cap;
 };
+
+size_t hot_unit_table_bytes(const Problem& pb);
 
 // Launchers (stream-ordered). Return cudaError_t of the launch.
 cudaError_t launch_pack(const Problem& pb, cudaStream_t s);

@@ -344,8 +344,8 @@ __device__ __forceinline__ void band_hits(const int (&thr)[kJ1][NC], const int4&
 // dominated (C_1 >= U(E)) never leave the fast loop. Q(c_2) = P[k2][c_2] and
 // R(c_2) = C_3 are shared-memory rows like B. The fast loop and the slow paths
 // each exist once in the code (one pass-generic instance).
-template <int NC>
-__device__ void k3_tile(const CtaCtx<NC>& cx, const int pass, int k3, int c1_base, int c1_lo, int c1_hi,
+template <int NC, int pass>
+__device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, int c1_hi,
                         const int32_t* Bs, const int32_t* Qs, const int32_t* Rs, uint64_t* tab,
                         uint16_t* tb0, const ScoreOut& out, Emitter& em, unsigned long long& feas,
                         unsigned long long& cand) {
@@ -463,38 +463,13 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, const int pass, int k3, int c1_bas
   feas += nfeas;
 }
 
-// Two warps per CTA: (model, k_2, batch). They share the staged c_2 rows and the
-// fold tables, and take first-cut tiles from a shared counter.
 template <int NC>
-__global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
-    score_kernel(Problem pb, ScoreOut out, int nb_log2, int row_len) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  __shared__ int s_tile;
-  const int nb = 1 << nb_log2;
-  uint64_t* tab = reinterpret_cast<uint64_t*>(smem_raw);                    // [NC][nb + 2]
-  int32_t* Bs = reinterpret_cast<int32_t*>(tab + (size_t)NC * (nb + 2));     // [row_len] B(c2), current k3
-  int32_t* Qs = Bs + row_len;                                               // [row_len] Q(c2) = P[k2][b][c2]
-  int32_t* Rs = Qs + row_len;                                               // [row_len] R(c2) = C_3, current k3
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  Emitter em{reinterpret_cast<int4*>(Rs + row_len) + warp * 2 * kEmitBuf, 0};
-  uint16_t* tb0 = reinterpret_cast<uint16_t*>(reinterpret_cast<int4*>(Rs + row_len) + kWarps * 2 * kEmitBuf) +
-                  warp * (kJ1 * NC * 32);  // [kJ1 * NC][32] per warp
-  const int ntab = NC * (nb + 2);
-
-  // Batch index slowest: small batches hold almost all feasible (heavier) work,
-  // so they are scheduled first and the tail of the grid is light.
-  const int B = pb.B;
-  const int k2 = blockIdx.x % NC;
-  const int ml = (blockIdx.x / NC) % pb.n_local;
-  const int bi = blockIdx.x / (NC * pb.n_local);
-  const DevModel md = pb.models[ml];
-
-  CtaCtx<NC> cx;
+__device__ __forceinline__ void make_ctx(CtaCtx<NC>& cx, const Problem& pb, const DevModel& md, int k2, int bi,
+                                         int nb) {
   cx.Pm = pb.P + md.p_off;
   cx.Ym = pb.Y + md.y_off;
   cx.Mp = md.Mp;
-  cx.B = B;
+  cx.B = pb.B;
   cx.bi = bi;
   cx.b = pb.batches[bi];
   cx.k2 = k2;
@@ -509,13 +484,106 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
   int sh = 0;
   while ((cx.T >> sh) >= nb) ++sh;
   cx.sh = sh;
-  const int M = cx.M, T = cx.T;
+}
 
+// Shared-memory layout common to the score kernels (2 warps per CTA).
+struct ScoreSmem {
+  uint64_t* tab;  // [NC][nb + 2] fold tables
+  int32_t* Bs;    // [row_len] B(c2) for the current k3
+  int32_t* Qs;    // [row_len] Q(c2) = P[k2][b][c2]
+  int32_t* Rs;    // [row_len] R(c2) = C_3 for the current k3
+  int4* ebuf;     // [kWarps][kEmitBuf][2] survivor records
+  uint16_t* tb0;  // [kWarps][kJ1 * NC][32] pass-2 tightening buckets
+};
+
+template <int NC>
+__device__ __forceinline__ ScoreSmem carve_smem(uint8_t* raw, int nb, int row_len) {
+  ScoreSmem m;
+  m.tab = reinterpret_cast<uint64_t*>(raw);
+  m.Bs = reinterpret_cast<int32_t*>(m.tab + (size_t)NC * (nb + 2));
+  m.Qs = m.Bs + row_len;
+  m.Rs = m.Qs + row_len;
+  m.ebuf = reinterpret_cast<int4*>(m.Rs + row_len);
+  m.tb0 = reinterpret_cast<uint16_t*>(m.ebuf + kWarps * 2 * kEmitBuf);
+  return m;
+}
+
+template <int NC>
+static size_t score_smem_bytes(int nb, int row_len) {
+  return 8 * (size_t)NC * (nb + 2) + sizeof(int32_t) * 3 * (size_t)row_len + (size_t)kWarps * kEmitBuf * 32 +
+         (size_t)kWarps * kJ1 * NC * 32 * sizeof(uint16_t);
+}
+
+// Stage the c2 rows of (k2, k3, b): B(c2) and R(c2) (Q(c2) is k3-independent).
+template <int NC>
+__device__ __forceinline__ void stage_rows(const CtaCtx<NC>& cx, const ScoreSmem& sm, int k3, int c2_from, int c2_to,
+                                           bool with_q) {
+  const int M = cx.M;
+  const int32_t* P3 = cx.Prow(k3);
+  const int32_t P3M = P3[M];
+  const int32_t* Y23 = cx.Yrow(cx.k2, k3);
+  for (int c2 = c2_from + (int)threadIdx.x; c2 < c2_to; c2 += 32 * kWarps) {
+    const bool in = c2 < M;
+    const int p2 = in ? __ldg(cx.P2 + c2) : 0;
+    const int p3 = in ? __ldg(P3 + c2) : 0;
+    sm.Bs[c2] = in ? p2 - p3 + __ldg(Y23 + c2) + P3M : kPadB;
+    sm.Rs[c2] = in ? P3M - p3 : 0;
+    if (with_q) sm.Qs[c2] = p2;
+  }
+}
+
+struct K3Range {
+  int c1lo, c1hi, c1_base0, ntiles, c2_from, c2_to;
+  bool empty;
+};
+
+__device__ __forceinline__ K3Range k3_range(const DevModel& md) {
+  K3Range r;
+  const int M = (int)md.M;
+  r.c1lo = max(1, (int)md.row_lo);
+  r.c1hi = min(M - 2, (int)md.row_hi - 1);
+  r.empty = M < 3 || r.c1lo > r.c1hi;
+  // tiles start at c1_base = 3 mod 4 so that every c2 group c1_base + 1 + 4i is aligned
+  r.c1_base0 = r.c1lo - ((r.c1lo - 3) & 3);
+  r.ntiles = (r.c1hi - r.c1_base0 + 32 * kJ1) / (32 * kJ1);
+  r.c2_from = r.c1_base0 + 1;          // >= 0
+  r.c2_to = ((M + 3) & ~3) + 4;        // padded, exclusive
+  return r;
+}
+
+__device__ __forceinline__ void flush_counters(const ScoreOut& out, unsigned long long feas, unsigned long long cand) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    feas += __shfl_down_sync(FULL_MASK, feas, d);
+    cand += __shfl_down_sync(FULL_MASK, cand, d);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (feas) atomicAdd(&out.counters[1], feas);
+    if (cand) atomicAdd(&out.counters[2], cand);
+  }
+}
+
+// ---- kernel 1: K = 1 and K = 2 candidates. CTA = (model, k_2, batch), 2 warps. ----
+template <int NC>
+__global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
+    score12_kernel(Problem pb, ScoreOut out, int nb_log2, int row_len) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int nb = 1 << nb_log2;
+  const ScoreSmem sm = carve_smem<NC>(smem_raw, nb, row_len);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  Emitter em{sm.ebuf + warp * 2 * kEmitBuf, 0};
+  const int ntab = NC * (nb + 2);
+  const int k2 = blockIdx.x % NC;
+  const int ml = (blockIdx.x / NC) % pb.n_local;
+  const int bi = blockIdx.x / (NC * pb.n_local);
+  const DevModel md = pb.models[ml];
+  CtaCtx<NC> cx;
+  make_ctx(cx, pb, md, k2, bi, nb);
+  const int M = cx.M, T = cx.T, sh = cx.sh;
+  uint64_t* tab = sm.tab;
   unsigned long long feas = 0, cand = 0;
-  reset_tables(tab, ntab, tid, 32 * kWarps);
-  __syncthreads();
 
-  // ---- K = 1: segment (k2), whole model on class k2 ----
+  // K = 1: segment (k2), whole model on class k2
   if (warp == 0 && md.row_lo == 0) {
     const int E = cx.P2[M];
     if (lane == 0) ++cand;
@@ -523,11 +591,12 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
     if (f) ++feas;
     if (__any_sync(FULL_MASK, f)) emit_warp(out, em, f, make_rec(md.model, 1, 0, 0, k2, 0xFF, 0xFF, cx.b, E, E, 0, 0));
   }
-
-  // ---- K = 2: segments (k1, k2); c1 in this rank's rows ----
+  // K = 2: segments (k1, k2); c1 in this rank's rows
   if (pb.Kmax >= 2 && M >= 2) {
     const int lo = max(1, (int)md.row_lo), hi = min(M - 1, (int)md.row_hi - 1);
     if (lo <= hi) {
+      reset_tables(tab, ntab, tid, 32 * kWarps);
+      __syncthreads();
       const int P2M = cx.P2[M];
       int anyf = 0;
 #pragma unroll 1
@@ -564,110 +633,181 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
           if (!__syncthreads_or(anyf)) break;
           tables_finalize(tab, NC, nb, warp, kWarps);
           __syncthreads();
-        } else {
-          __syncthreads();
-          reset_tables(tab, ntab, tid, 32 * kWarps);
-          __syncthreads();
         }
       }
     }
   }
-
-  // ---- K = 3: for each k3, segments (k1, k2, k3) ----
-  if (pb.Kmax >= 3 && M >= 3) {
-    const int c1lo = max(1, (int)md.row_lo), c1hi = min(M - 2, (int)md.row_hi - 1);
-    if (c1lo <= c1hi) {
-      // tiles start at c1_base = 3 mod 4 so that every c2 group c1_base + 1 + 4i is aligned
-      const int c1_base0 = c1lo - ((c1lo - 3) & 3);
-      const int ntiles = (c1hi - c1_base0 + 32 * kJ1) / (32 * kJ1);
-      const int c2_from = c1_base0 + 1;                 // >= 0
-      const int c2_to = ((M + 3) & ~3) + 4;             // padded, exclusive
-      for (int c2 = c2_from + tid; c2 < c2_to; c2 += 32 * kWarps) Qs[c2] = c2 < M ? __ldg(cx.P2 + c2) : 0;
-#pragma unroll 1
-      for (int k3 = 0; k3 < NC; ++k3) {
-        const int32_t* P3 = cx.Prow(k3);
-        const int32_t P3M = P3[M];
-        const int32_t* Y23 = cx.Yrow(k2, k3);
-        for (int c2 = c2_from + tid; c2 < c2_to; c2 += 32 * kWarps) {
-          const bool in = c2 < M;
-          const int p3 = in ? __ldg(P3 + c2) : 0;
-          Bs[c2] = in ? __ldg(cx.P2 + c2) - p3 + __ldg(Y23 + c2) + P3M : kPadB;
-          Rs[c2] = in ? P3M - p3 : 0;
-        }
-        if (tid == 0) s_tile = 0;
-        __syncthreads();
-        const unsigned long long feas0 = feas;
-#pragma unroll 1
-        for (int pass = 1; pass <= 2; ++pass) {
-#pragma unroll 1
-          for (;;) {
-            int t = 0;
-            if (lane == 0) t = atomicAdd(&s_tile, 1);
-            t = __shfl_sync(FULL_MASK, t, 0);
-            if (t >= ntiles) break;
-            k3_tile<NC>(cx, pass, k3, c1_base0 + t * 32 * kJ1, c1lo, c1hi, Bs, Qs, Rs, tab, tb0, out, em, feas,
-                        cand);
-          }
-          if (pass == 1) {
-            if (!__syncthreads_or(feas != feas0) || (pb.debug_flags & 2)) break;
-            tables_finalize(tab, NC, nb, warp, kWarps);
-            if (tid == 0) s_tile = 0;
-            __syncthreads();
-          }
-        }
-        __syncthreads();
-        reset_tables(tab, ntab, tid, 32 * kWarps);
-        __syncthreads();
-      }
-    }
-  }
-
-  // ---- counters ----
   emit_flush(out, em);
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) {
-    feas += __shfl_down_sync(FULL_MASK, feas, d);
-    cand += __shfl_down_sync(FULL_MASK, cand, d);
+  flush_counters(out, feas, cand);
+}
+
+// ---- kernel 2: K = 3 pass 1 over every (model, k_2, batch) CTA (2 warps, tiles from
+// a shared counter). Counts every candidate and feasible candidate and builds the
+// bucket-best tables of each (k_2, k_3, b) unit; units with a feasible candidate
+// are "hot": their finalized tables go to global memory for kernel 3. ----
+template <int NC>
+__global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
+    score3a_kernel(Problem pb, ScoreOut out, int nb_log2, int row_len) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  __shared__ int s_tile;
+  __shared__ unsigned long long s_slot;
+  const int nb = 1 << nb_log2;
+  const ScoreSmem sm = carve_smem<NC>(smem_raw, nb, row_len);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ntab = NC * (nb + 2);
+  const int k2 = blockIdx.x % NC;
+  const int ml = (blockIdx.x / NC) % pb.n_local;
+  const int bi = blockIdx.x / (NC * pb.n_local);
+  const DevModel md = pb.models[ml];
+  CtaCtx<NC> cx;
+  make_ctx(cx, pb, md, k2, bi, nb);
+  Emitter em{sm.ebuf + warp * 2 * kEmitBuf, 0};  // unused in pass 1
+  unsigned long long feas = 0, cand = 0;
+  const K3Range r = k3_range(md);
+  if (pb.Kmax >= 3 && !r.empty) {
+    reset_tables(sm.tab, ntab, tid, 32 * kWarps);
+#pragma unroll 1
+    for (int k3 = 0; k3 < NC; ++k3) {
+      stage_rows(cx, sm, k3, r.c2_from, r.c2_to, k3 == 0);
+      if (tid == 0) s_tile = 0;
+      __syncthreads();
+      const unsigned long long feas0 = feas;
+#pragma unroll 1
+      for (;;) {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(&s_tile, 1);
+        t = __shfl_sync(FULL_MASK, t, 0);
+        if (t >= r.ntiles) break;
+        k3_tile<NC, 1>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.tab,
+                       sm.tb0 + warp * (kJ1 * NC * 32), out, em, feas, cand);
+      }
+      if (__syncthreads_or(feas != feas0) && !(pb.debug_flags & 2)) {
+        tables_finalize(sm.tab, NC, nb, warp, kWarps);
+        if (tid == 0) {
+          s_slot = atomicAdd(&out.counters[3], 1ull);
+          if (s_slot < out.hot_cap) out.hot[s_slot] = make_uint4(ml, k2, k3, bi);
+        }
+        __syncthreads();
+        if (s_slot < out.hot_cap) {
+          uint64_t* dst = out.hot_tab + s_slot * (unsigned long long)ntab;
+          for (int i = tid; i < ntab; i += 32 * kWarps) dst[i] = sm.tab[i];
+        }
+      }
+      __syncthreads();
+      reset_tables(sm.tab, ntab, tid, 32 * kWarps);
+      __syncthreads();
+    }
   }
-  if (lane == 0) {
-    atomicAdd(&out.counters[1], feas);
-    atomicAdd(&out.counters[2], cand);
+  flush_counters(out, feas, cand);
+}
+
+// ---- kernel 3: K = 3 pass 2 over the hot units only (persistent CTAs pull units
+// from a counter): reload the unit's tables, re-scan with tightened thresholds and
+// emit the survivors. ----
+template <int NC>
+__global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
+    score3b_kernel(Problem pb, ScoreOut out, int nb_log2, int row_len) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  __shared__ int s_tile;
+  __shared__ unsigned long long s_unit;
+  const int nb = 1 << nb_log2;
+  const ScoreSmem sm = carve_smem<NC>(smem_raw, nb, row_len);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ntab = NC * (nb + 2);
+  Emitter em{sm.ebuf + warp * 2 * kEmitBuf, 0};
+  unsigned long long feas = 0, cand = 0;
+  const unsigned long long n_hot = min(out.counters[3], out.hot_cap);
+#pragma unroll 1
+  for (;;) {
+    if (tid == 0) s_unit = atomicAdd(&out.counters[4], 1ull);
+    __syncthreads();
+    const unsigned long long u = s_unit;
+    if (u >= n_hot) break;
+    const uint4 hu = out.hot[u];
+    const int ml = (int)hu.x, k2 = (int)hu.y, k3 = (int)hu.z, bi = (int)hu.w;
+    const DevModel md = pb.models[ml];
+    CtaCtx<NC> cx;
+    make_ctx(cx, pb, md, k2, bi, nb);
+    const K3Range r = k3_range(md);
+    const uint64_t* src = out.hot_tab + u * (unsigned long long)ntab;
+    for (int i = tid; i < ntab; i += 32 * kWarps) sm.tab[i] = src[i];
+    stage_rows(cx, sm, k3, r.c2_from, r.c2_to, true);
+    if (tid == 0) s_tile = 0;
+    __syncthreads();
+#pragma unroll 1
+    for (;;) {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(&s_tile, 1);
+      t = __shfl_sync(FULL_MASK, t, 0);
+      if (t >= r.ntiles) break;
+      k3_tile<NC, 2>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.tab,
+                     sm.tb0 + warp * (kJ1 * NC * 32), out, em, feas, cand);
+    }
+    __syncthreads();
   }
+  emit_flush(out, em);
 }
 
 // Shared memory per CTA: the fold tables take what the budget leaves after the
-// three staged c2 rows (B, Q, R) and the emit buffers, rounded down to a power of
-// two (128..2048 buckets).
+// three staged c2 rows (B, Q, R), the emit buffers and the pass-2 slot data,
+// rounded down to a power of two (128..2048 buckets).
 constexpr size_t kSmemBudget = 27 * 1024;
 
 template <int NC>
-static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaStream_t s) {
+static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches) {
   const int row_len = (int)((((size_t)pb.max_M + 3) & ~(size_t)3) + 4);
-  const size_t fixed = sizeof(int32_t) * 3 * (size_t)row_len + (size_t)kWarps * kEmitBuf * 32 +
-                       (size_t)kWarps * kJ1 * NC * 32 * sizeof(uint16_t);
   int nb_log2 = 7;
-  while (nb_log2 < 11 && fixed + 8 * NC * (((size_t)2 << nb_log2) + 2) <= kSmemBudget) ++nb_log2;
-  const size_t smem = fixed + 8 * NC * (((size_t)1 << nb_log2) + 2);
+  while (nb_log2 < 11 && score_smem_bytes<NC>(2 << nb_log2, row_len) <= kSmemBudget) ++nb_log2;
+  const size_t smem = score_smem_bytes<NC>(1 << nb_log2, row_len);
   const unsigned grid = (unsigned)pb.n_local * NC * pb.B;
-  auto kfn = score_kernel<NC>;
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e;
+  e = cudaFuncSetAttribute(score12_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kfn<<<grid, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
+  e = cudaFuncSetAttribute(score3a_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(score3b_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (pb.Kmax >= 3) {
+    score3a_kernel<NC><<<grid, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
+    score3b_kernel<NC><<<148 * (16 / kWarps), 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
+    *n_launches += 2;
+  }
+  score12_kernel<NC><<<grid, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
+  ++*n_launches;
   return cudaGetLastError();
+}
+
+// Bytes of one hot unit's tables for this problem (the ABI sizes its buffer with it).
+size_t hot_unit_table_bytes(const Problem& pb) {
+  const int row_len = (int)((((size_t)pb.max_M + 3) & ~(size_t)3) + 4);
+  int nb_log2 = 7;
+  auto smem_for = [&](int nb) -> size_t {
+    switch (pb.C) {
+      case 1: return score_smem_bytes<1>(nb, row_len);
+      case 2: return score_smem_bytes<2>(nb, row_len);
+      case 3: return score_smem_bytes<3>(nb, row_len);
+      case 4: return score_smem_bytes<4>(nb, row_len);
+      case 5: return score_smem_bytes<5>(nb, row_len);
+      case 6: return score_smem_bytes<6>(nb, row_len);
+      case 7: return score_smem_bytes<7>(nb, row_len);
+      default: return score_smem_bytes<8>(nb, row_len);
+    }
+  };
+  while (nb_log2 < 11 && smem_for(2 << nb_log2) <= kSmemBudget) ++nb_log2;
+  return 8 * (size_t)pb.C * ((1 << nb_log2) + 2);
 }
 
 cudaError_t launch_score(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches) {
   if (pb.n_local == 0) return cudaSuccess;
-  ++*n_launches;
   switch (pb.C) {
-    case 1: return launch_score_nc<1>(pb, out, s);
-    case 2: return launch_score_nc<2>(pb, out, s);
-    case 3: return launch_score_nc<3>(pb, out, s);
-    case 4: return launch_score_nc<4>(pb, out, s);
-    case 5: return launch_score_nc<5>(pb, out, s);
-    case 6: return launch_score_nc<6>(pb, out, s);
-    case 7: return launch_score_nc<7>(pb, out, s);
-    case 8: return launch_score_nc<8>(pb, out, s);
+    case 1: return launch_score_nc<1>(pb, out, s, n_launches);
+    case 2: return launch_score_nc<2>(pb, out, s, n_launches);
+    case 3: return launch_score_nc<3>(pb, out, s, n_launches);
+    case 4: return launch_score_nc<4>(pb, out, s, n_launches);
+    case 5: return launch_score_nc<5>(pb, out, s, n_launches);
+    case 6: return launch_score_nc<6>(pb, out, s, n_launches);
+    case 7: return launch_score_nc<7>(pb, out, s, n_launches);
+    case 8: return launch_score_nc<8>(pb, out, s, n_launches);
     default: return cudaErrorInvalidValue;
   }
 }
