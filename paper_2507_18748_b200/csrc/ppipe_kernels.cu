@@ -183,56 +183,74 @@ __device__ __noinline__ void emit_warp(const ScoreOut& o, Emitter& em, bool cond
   em.count += n;
 }
 
-// ---- fold tables: one row of nb + 2 64-bit entries per k_1 (nb + 1 used; even for 16-B alignment) ----
-// pass 1: raw[j] = min over feasible candidates with E >> sh == j of (Cmax << 32 | E),
-//         i.e. the bucket's best point (smallest Cmax, then smallest E).
-// finalize: entry j = {x = U[j] = min Cmax over buckets < j, y = E*_j}, entry nb = {U[nb], -}.
+// ---- fold tables ----
+// Pass 1 keeps, per k_1 and E-bucket j = E >> sh, the bucket's best point (smallest
+// Cmax, then smallest E) packed in 32 bits: key = (ceil(Cmax / 2^q) << sh) | (E mod 2^sh),
+// so a plain 32-bit shared atomicMin folds it (a 64-bit min would be a CAS loop).
+// q = 0 (exact) whenever bits(T_eff) + 1 + sh <= 32, i.e. for SLOs below ~1 s at
+// 256 buckets; otherwise Cmax is rounded UP, which only makes the tests below
+// more conservative. Row length nb + 2 (nb + 1 used).
+// finalize: fin[j] = {U[j] = min rounded Cmax over buckets < j, key[j]}, fin[nb].x = U[nb].
 // pass 2 keeps a feasible candidate (E, Cmax) of bucket j unless it is dominated:
-//   Cmax >= U[j]                      by a point of an earlier bucket (smaller E), or
-//   E >= E*_j, Cmax >= C*_j, not both equal, with C*_j = U[j+1] the bucket's own best
-//   (when Cmax < U[j], the bucket's best Cmax is below U[j], so U[j+1] is exactly it).
-__device__ __forceinline__ void reset_tables(uint64_t* tab, int n, int tid, int nthreads) {
-  for (int i = tid; i < n; i += nthreads) tab[i] = ~0ull;
+//   Cmax >= U[j] << q                  by a point of an earlier bucket (smaller E), or
+//   E >= E*_j, Cmax >= C*_j << q, not both equal, with (C*_j, E*_j) decoded from key[j]:
+//                                      by the bucket's own best point.
+// (proof sketch: every pruned candidate has a real candidate with E' <= E and
+// Cmax' <= Cmax, strictly better in one, or is an exact duplicate kept elsewhere.)
+constexpr uint32_t kEmpty = 0xffffffffu;
+
+__device__ __forceinline__ void reset_raw(uint32_t* raw, int n, int tid, int nthreads) {
+  for (int i = tid; i < n; i += nthreads) raw[i] = kEmpty;
 }
 
-__device__ __noinline__ void tables_finalize(uint64_t* tab, int nc, int nb, int warp, int nwarps) {
+__device__ __forceinline__ uint32_t pack_key(int E, int Cmax, int sh, int q) {
+  const uint32_t cr = ((uint32_t)Cmax + ((1u << q) - 1u)) >> q;
+  return (cr << sh) | ((uint32_t)E & ((1u << sh) - 1u));
+}
+
+// raw [nc][nb + 2] -> fin [nc][nb + 2] (fin may be global memory). One warp per k_1.
+__device__ __noinline__ void tables_finalize(const uint32_t* raw, uint2* fin, int nc, int nb, int sh, int warp,
+                                             int nwarps) {
   const int lane = threadIdx.x & 31;
   for (int k = warp; k < nc; k += nwarps) {
-    uint64_t* row = tab + (size_t)k * (nb + 2);
-    int run = INT_MAX;
+    const uint32_t* r = raw + (size_t)k * (nb + 2);
+    uint2* f = fin + (size_t)k * (nb + 2);
+    uint32_t run = kEmpty;
     for (int r0 = 0; r0 < nb; r0 += 32) {
-      const uint64_t raw = row[r0 + lane];
-      const int c = raw == ~0ull ? INT_MAX : (int)(raw >> 32);
-      int incl = c;
+      const uint32_t key = r[r0 + lane];
+      const uint32_t c = key == kEmpty ? kEmpty : key >> sh;
+      uint32_t incl = c;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        const int o = __shfl_up_sync(FULL_MASK, incl, d);
+        const uint32_t o = __shfl_up_sync(FULL_MASK, incl, d);
         if (lane >= d) incl = min(incl, o);
       }
-      int excl = __shfl_up_sync(FULL_MASK, incl, 1);
-      if (lane == 0) excl = INT_MAX;
-      reinterpret_cast<uint2*>(row)[r0 + lane] = make_uint2((unsigned)min(run, excl), (unsigned)(raw & 0xffffffffu));
+      uint32_t excl = __shfl_up_sync(FULL_MASK, incl, 1);
+      if (lane == 0) excl = kEmpty;
+      f[r0 + lane] = make_uint2(min(run, excl), key);
       run = min(run, __shfl_sync(FULL_MASK, incl, 31));
     }
-    if (lane == 0) reinterpret_cast<uint2*>(row)[nb] = make_uint2((unsigned)run, 0u);
+    if (lane == 0) f[nb] = make_uint2(run, kEmpty);
   }
 }
 
 // Is a feasible candidate (E, Cmax) kept by the finalized row (see above)?
-__device__ __forceinline__ bool survives(const uint2* row, int jb, int E, int Cmax) {
+__device__ __forceinline__ bool survives(const uint2* row, int jb, int E, int Cmax, int sh, int q) {
   const uint2 ent = row[jb];
-  if (Cmax >= (int)ent.x) return false;
-  const int Cs = (int)row[jb + 1].x;
-  const int Es = (int)ent.y;
+  if (ent.x != kEmpty && (unsigned)Cmax >= (ent.x << q)) return false;
+  if (ent.y == kEmpty) return true;
+  const int Cs = (int)((ent.y >> sh) << q);
+  const int Es = (jb << sh) | (int)(ent.y & ((1u << sh) - 1u));
   return !(E >= Es && Cmax >= Cs && (E > Es || Cmax > Cs));
 }
 
-// First j in [0, nb] with U[j] <= v in a finalized (nonincreasing) row; nb + 1 if none.
-__device__ __forceinline__ int first_bucket_le(const uint2* row, int nb, int v) {
+// First j in [0, nb] with U[j] << q <= v in a finalized (nonincreasing) row; nb + 1 if none.
+__device__ __forceinline__ int first_bucket_le(const uint2* row, int nb, int v, int q) {
   int lo = 0, hi = nb + 1;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if ((int)row[mid].x <= v) hi = mid;
+    const uint32_t u = row[mid].x;
+    if (u != kEmpty && (u << q) <= (unsigned)v) hi = mid;
     else lo = mid + 1;
   }
   return lo;
@@ -244,7 +262,7 @@ struct CtaCtx {
   const int32_t* Pm;   // P[m] base
   const int32_t* Ym;   // Y[m] base
   size_t Mp, B;
-  int bi, b, k2, M, T, sh, m1, nb, dbg;
+  int bi, b, k2, M, T, sh, q, m1, nb, dbg;
   uint32_t model;
   const uint8_t* pair_v;
   __device__ const int32_t* Prow(int k) const { return Pm + ((size_t)k * B + bi) * Mp; }
@@ -346,7 +364,7 @@ __device__ __forceinline__ void band_hits(const int (&thr)[kJ1][NC], const int4&
 // each exist once in the code (one pass-generic instance).
 template <int NC, int pass>
 __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, int c1_hi,
-                        const int32_t* Bs, const int32_t* Qs, const int32_t* Rs, uint64_t* tab,
+                        const int32_t* Bs, const int32_t* Qs, const int32_t* Rs, uint32_t* raw, const uint2* fin,
                         uint16_t* tb0, const ScoreOut& out, Emitter& em, unsigned long long& feas,
                         unsigned long long& cand) {
   const int lane = threadIdx.x & 31;
@@ -368,7 +386,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
       if (pass == 2 && valid) {
         // U is nonincreasing; from bucket b0 on U <= C1 <= Cmax, so nothing there
         // survives: only E < b0 << sh can  =>  B <= (b0 << sh) - 1 - A.
-        const int b0 = min(first_bucket_le(reinterpret_cast<const uint2*>(tab + (size_t)k1 * (nb + 2)), nb, C1), nb);
+        const int b0 = min(first_bucket_le(fin + (size_t)k1 * (nb + 2), nb, C1, cx.q), nb);
         if (b0 < nb) t = t + min(0, (b0 << cx.sh) - 1 - cx.T);
         tb0[(j * NC + k1) * 32 + lane] = (uint16_t)b0;  // pass-2 tightening bucket (this warp's slice)
       }
@@ -425,9 +443,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
             if (v && Bv <= thr[j][k1]) {
               const int E = cx.T - thr[j][k1] + Bv;
               const int Cmax = max(max(c1r[j][k1], C2), R);
-              if (!(cx.dbg & 1))
-                atomicMin(reinterpret_cast<unsigned long long*>(tab + (size_t)k1 * (nb + 2) + (E >> cx.sh)),
-                          ((unsigned long long)(unsigned)Cmax << 32) | (unsigned)E);
+              if (!(cx.dbg & 1)) atomicMin(raw + (size_t)k1 * (nb + 2) + (E >> cx.sh), pack_key(E, Cmax, cx.sh, cx.q));
               ++nfeas;
             }
           }
@@ -452,7 +468,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
             const int Cmax = max(max(c1r[j][k1], C2), R);
             const bool f = v && (Bv <= thr[j][k1]);
             const bool cond =
-                f && survives(reinterpret_cast<const uint2*>(tab + (size_t)k1 * (nb + 2)), E >> cx.sh, E, Cmax);
+                f && survives(fin + (size_t)k1 * (nb + 2), E >> cx.sh, E, Cmax, cx.sh, cx.q);
             if (__any_sync(FULL_MASK, cond))
               emit_warp(out, em, cond, make_rec(cx.model, 3, c1, c2u, k1, cx.k2, k3, cx.b, E, c1r[j][k1], C2, R));
           }
@@ -484,11 +500,14 @@ __device__ __forceinline__ void make_ctx(CtaCtx<NC>& cx, const Problem& pb, cons
   int sh = 0;
   while ((cx.T >> sh) >= nb) ++sh;
   cx.sh = sh;
+  const int bits_t = 32 - __clz(cx.T | 1);
+  cx.q = max(0, bits_t + 1 - (32 - sh));
 }
 
 // Shared-memory layout common to the score kernels (2 warps per CTA).
 struct ScoreSmem {
-  uint64_t* tab;  // [NC][nb + 2] fold tables
+  uint2* fin;     // [NC][nb + 2] finalized fold tables (pass 2); pass 1 uses the first half as
+  uint32_t* raw;  // [NC][nb + 2] raw bucket-best keys
   int32_t* Bs;    // [row_len] B(c2) for the current k3
   int32_t* Qs;    // [row_len] Q(c2) = P[k2][b][c2]
   int32_t* Rs;    // [row_len] R(c2) = C_3 for the current k3
@@ -499,8 +518,9 @@ struct ScoreSmem {
 template <int NC>
 __device__ __forceinline__ ScoreSmem carve_smem(uint8_t* raw, int nb, int row_len) {
   ScoreSmem m;
-  m.tab = reinterpret_cast<uint64_t*>(raw);
-  m.Bs = reinterpret_cast<int32_t*>(m.tab + (size_t)NC * (nb + 2));
+  m.fin = reinterpret_cast<uint2*>(raw);
+  m.raw = reinterpret_cast<uint32_t*>(raw);
+  m.Bs = reinterpret_cast<int32_t*>(m.fin + (size_t)NC * (nb + 2));
   m.Qs = m.Bs + row_len;
   m.Rs = m.Qs + row_len;
   m.ebuf = reinterpret_cast<int4*>(m.Rs + row_len);
@@ -564,14 +584,23 @@ __device__ __forceinline__ void flush_counters(const ScoreOut& out, unsigned lon
 }
 
 // ---- kernel 1: K = 1 and K = 2 candidates. CTA = (model, k_2, batch), 2 warps. ----
+// Shared memory: fin [NC][nb + 2] (8 B) | raw [NC][nb + 2] (4 B) | emit buffers.
+template <int NC>
+static size_t score12_smem_bytes(int nb) {
+  return 8 * (size_t)NC * (nb + 2) + ((4 * (size_t)NC * (nb + 2) + 15) & ~(size_t)15) + (size_t)kWarps * kEmitBuf * 32;
+}
+
 template <int NC>
 __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
-    score12_kernel(Problem pb, ScoreOut out, int nb_log2, int row_len) {
+    score12_kernel(Problem pb, ScoreOut out, int nb_log2) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int nb = 1 << nb_log2;
-  const ScoreSmem sm = carve_smem<NC>(smem_raw, nb, row_len);
+  uint2* fin = reinterpret_cast<uint2*>(smem_raw);
+  uint32_t* raw = reinterpret_cast<uint32_t*>(fin + (size_t)NC * (nb + 2));
+  int4* ebuf = reinterpret_cast<int4*>(smem_raw + 8 * (size_t)NC * (nb + 2) +
+                                       ((4 * (size_t)NC * (nb + 2) + 15) & ~(size_t)15));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  Emitter em{sm.ebuf + warp * 2 * kEmitBuf, 0};
+  Emitter em{ebuf + warp * 2 * kEmitBuf, 0};
   const int ntab = NC * (nb + 2);
   const int k2 = blockIdx.x % NC;
   const int ml = (blockIdx.x / NC) % pb.n_local;
@@ -579,8 +608,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
   const DevModel md = pb.models[ml];
   CtaCtx<NC> cx;
   make_ctx(cx, pb, md, k2, bi, nb);
-  const int M = cx.M, T = cx.T, sh = cx.sh;
-  uint64_t* tab = sm.tab;
+  const int M = cx.M, T = cx.T, sh = cx.sh, q = cx.q;
   unsigned long long feas = 0, cand = 0;
 
   // K = 1: segment (k2), whole model on class k2
@@ -595,7 +623,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
   if (pb.Kmax >= 2 && M >= 2) {
     const int lo = max(1, (int)md.row_lo), hi = min(M - 1, (int)md.row_hi - 1);
     if (lo <= hi) {
-      reset_tables(tab, ntab, tid, 32 * kWarps);
+      reset_raw(raw, ntab, tid, 32 * kWarps);
       __syncthreads();
       const int P2M = cx.P2[M];
       int anyf = 0;
@@ -613,17 +641,15 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
             const int E = C1 + y + C2;
             const bool f = valid && E <= T;
             const int Cmax = max(C1, C2);
-            uint64_t* row = tab + (size_t)k1 * (nb + 2);
             if (pass == 1) {
               if (valid) ++cand;
               if (f) {
                 ++feas;
                 anyf = 1;
-                atomicMin(reinterpret_cast<unsigned long long*>(row + (E >> sh)),
-                          ((unsigned long long)(unsigned)Cmax << 32) | (unsigned)E);
+                atomicMin(raw + (size_t)k1 * (nb + 2) + (E >> sh), pack_key(E, Cmax, sh, q));
               }
             } else {
-              const bool cond = f && survives(reinterpret_cast<const uint2*>(row), f ? (E >> sh) : 0, E, Cmax);
+              const bool cond = f && survives(fin + (size_t)k1 * (nb + 2), f ? (E >> sh) : 0, E, Cmax, sh, q);
               if (__any_sync(FULL_MASK, cond))
                 emit_warp(out, em, cond, make_rec(md.model, 2, c1, 0, k1, k2, 0xFF, cx.b, E, C1, C2, 0));
             }
@@ -631,7 +657,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
         }
         if (pass == 1) {
           if (!__syncthreads_or(anyf)) break;
-          tables_finalize(tab, NC, nb, warp, kWarps);
+          tables_finalize(raw, fin, NC, nb, sh, warp, kWarps);
           __syncthreads();
         }
       }
@@ -665,7 +691,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
   unsigned long long feas = 0, cand = 0;
   const K3Range r = k3_range(md);
   if (pb.Kmax >= 3 && !r.empty) {
-    reset_tables(sm.tab, ntab, tid, 32 * kWarps);
+    reset_raw(sm.raw, ntab, tid, 32 * kWarps);
 #pragma unroll 1
     for (int k3 = 0; k3 < NC; ++k3) {
       stage_rows(cx, sm, k3, r.c2_from, r.c2_to, k3 == 0);
@@ -678,23 +704,21 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
         if (lane == 0) t = atomicAdd(&s_tile, 1);
         t = __shfl_sync(FULL_MASK, t, 0);
         if (t >= r.ntiles) break;
-        k3_tile<NC, 1>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.tab,
+        k3_tile<NC, 1>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin,
                        sm.tb0 + warp * (kJ1 * NC * 32), out, em, feas, cand);
       }
       if (__syncthreads_or(feas != feas0) && !(pb.debug_flags & 2)) {
-        tables_finalize(sm.tab, NC, nb, warp, kWarps);
         if (tid == 0) {
           s_slot = atomicAdd(&out.counters[3], 1ull);
           if (s_slot < out.hot_cap) out.hot[s_slot] = make_uint4(ml, k2, k3, bi);
         }
         __syncthreads();
-        if (s_slot < out.hot_cap) {
-          uint64_t* dst = out.hot_tab + s_slot * (unsigned long long)ntab;
-          for (int i = tid; i < ntab; i += 32 * kWarps) dst[i] = sm.tab[i];
-        }
+        if (s_slot < out.hot_cap)  // finalized tables straight to the unit's global slot
+          tables_finalize(sm.raw, reinterpret_cast<uint2*>(out.hot_tab) + s_slot * (unsigned long long)ntab, NC, nb,
+                          cx.sh, warp, kWarps);
       }
       __syncthreads();
-      reset_tables(sm.tab, ntab, tid, 32 * kWarps);
+      reset_raw(sm.raw, ntab, tid, 32 * kWarps);
       __syncthreads();
     }
   }
@@ -729,8 +753,8 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
     CtaCtx<NC> cx;
     make_ctx(cx, pb, md, k2, bi, nb);
     const K3Range r = k3_range(md);
-    const uint64_t* src = out.hot_tab + u * (unsigned long long)ntab;
-    for (int i = tid; i < ntab; i += 32 * kWarps) sm.tab[i] = src[i];
+    const uint2* src = reinterpret_cast<const uint2*>(out.hot_tab) + u * (unsigned long long)ntab;
+    for (int i = tid; i < ntab; i += 32 * kWarps) sm.fin[i] = src[i];
     stage_rows(cx, sm, k3, r.c2_from, r.c2_to, true);
     if (tid == 0) s_tile = 0;
     __syncthreads();
@@ -740,7 +764,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
       if (lane == 0) t = atomicAdd(&s_tile, 1);
       t = __shfl_sync(FULL_MASK, t, 0);
       if (t >= r.ntiles) break;
-      k3_tile<NC, 2>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.tab,
+      k3_tile<NC, 2>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin,
                      sm.tb0 + warp * (kJ1 * NC * 32), out, em, feas, cand);
     }
     __syncthreads();
@@ -761,7 +785,8 @@ static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaS
   const size_t smem = score_smem_bytes<NC>(1 << nb_log2, row_len);
   const unsigned grid = (unsigned)pb.n_local * NC * pb.B;
   cudaError_t e;
-  e = cudaFuncSetAttribute(score12_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem12 = score12_smem_bytes<NC>(1 << nb_log2);
+  e = cudaFuncSetAttribute(score12_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem12);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(score3a_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -772,7 +797,7 @@ static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaS
     score3b_kernel<NC><<<148 * (16 / kWarps), 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
     *n_launches += 2;
   }
-  score12_kernel<NC><<<grid, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
+  score12_kernel<NC><<<grid, 32 * kWarps, smem12, s>>>(pb, out, nb_log2);
   ++*n_launches;
   return cudaGetLastError();
 }
