@@ -366,12 +366,13 @@ template <int NC, int pass>
 __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, int c1_hi,
                         const int32_t* Bs, const int32_t* Qs, const int32_t* Rs, uint32_t* raw, const uint2* fin,
                         uint16_t* tb0, const ScoreOut& out, Emitter& em, unsigned long long& feas,
-                        unsigned long long& cand) {
+                        unsigned long long& cand, int Bmin = 0) {
   const int lane = threadIdx.x & 31;
   const int nb = cx.nb;
   int thr[kJ1][NC];
   int c1r[kJ1][NC];
   int p1[kJ1];
+  int wlo = INT_MAX, whi = -1;  // pass 2: c2 range that can hold survivors
 #pragma unroll
   for (int j = 0; j < kJ1; ++j) {
     const int c1 = c1_base + 32 * j + lane;
@@ -383,11 +384,50 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
       const int y = valid ? __ldg(cx.Yrow(k1, cx.k2) + c1) : 0;
       // E = A + B(c2) with A = C1 + Y1 - P[k2][c1]  =>  feasible iff B(c2) <= T - A
       int t = valid ? cx.T - (C1 + y - p1[j]) : kInvalidThr;
-      if (pass == 2 && valid) {
-        // U is nonincreasing; from bucket b0 on U <= C1 <= Cmax, so nothing there
-        // survives: only E < b0 << sh can  =>  B <= (b0 << sh) - 1 - A.
-        const int b0 = min(first_bucket_le(fin + (size_t)k1 * (nb + 2), nb, C1, cx.q), nb);
-        if (b0 < nb) t = t + min(0, (b0 << cx.sh) - 1 - cx.T);
+      if (pass == 2) {
+        int b0 = nb;
+        if (valid) {
+          const uint2* frow = fin + (size_t)k1 * (nb + 2);
+          // A survivor needs Cmax < U(E) <= U(E_min) with E_min = A + min_c2 B(c2) (U is
+          // nonincreasing), so C_1, C_2 = Q(c2) - P[k2][c1] and C_3 = R(c2) must each stay
+          // below Umax = U(E_min): with Q nondecreasing and R nonincreasing in c2 that
+          // leaves one c2 interval [lo, hi] per slot; outside it nothing is emitted.
+          const int Emin = max(0, cx.T - t + Bmin);  // E >= 0 for every real candidate
+          const uint32_t ur = Emin <= cx.T ? frow[Emin >> cx.sh].x : 0u;
+          const int Umax = ur == kEmpty ? INT_MAX : (int)min(ur << cx.q, (uint32_t)INT_MAX);
+          int lo = c1 + 1, hi = cx.M - 1;
+          if (Emin > cx.T || C1 >= Umax) {
+            t = kInvalidThr;  // nothing of this slot can survive
+          } else {
+            // first c2 with R(c2) < Umax
+            int a = c1 + 1, z = cx.M;
+            while (a < z) {
+              const int m = (a + z) >> 1;
+              if (Rs[m] < Umax) z = m;
+              else a = m + 1;
+            }
+            lo = a;
+            // last c2 with Q(c2) - p1 < Umax
+            a = c1 + 1;
+            z = cx.M;
+            while (a < z) {
+              const int m = (a + z) >> 1;
+              if (Qs[m] - p1[j] >= Umax) z = m;
+              else a = m + 1;
+            }
+            hi = a - 1;
+            if (lo > hi) {
+              t = kInvalidThr;
+            } else {
+              wlo = min(wlo, lo);
+              whi = max(whi, hi);
+              // U is nonincreasing; from bucket b0 on U <= C1 <= Cmax, so nothing there
+              // survives: only E < b0 << sh can  =>  B <= (b0 << sh) - 1 - A.
+              b0 = min(first_bucket_le(frow, nb, C1, cx.q), nb);
+              if (b0 < nb) t = t + min(0, (b0 << cx.sh) - 1 - cx.T);
+            }
+          }
+        }
         tb0[(j * NC + k1) * 32 + lane] = (uint16_t)b0;  // pass-2 tightening bucket (this warp's slice)
       }
       thr[j][k1] = t;
@@ -398,8 +438,19 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
   const int m1 = cx.m1;
   const int M = cx.M;
   unsigned nfeas = 0;
+  int c2_start = c1_base + 1, c2_end = M;
+  if (pass == 2) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      wlo = min(wlo, __shfl_xor_sync(FULL_MASK, wlo, d));
+      whi = max(whi, __shfl_xor_sync(FULL_MASK, whi, d));
+    }
+    if (whi < 0) return;  // no slot of this tile can hold a survivor
+    c2_start = c1_base + 1 + (max(0, wlo - (c1_base + 1)) & ~3);  // keep groups aligned
+    c2_end = min(M, whi + 1);
+  }
 #pragma unroll 1
-  for (int c2 = c1_base + 1; c2 < M; c2 += 4) {
+  for (int c2 = c2_start; c2 < c2_end; c2 += 4) {
     const int4 b4 = *reinterpret_cast<const int4*>(Bs + c2);
     const int rel = c2 - c1_base;  // 1 mod 4; the group is rel .. rel + 3
     int h0, h1, h2, h3;
@@ -528,10 +579,12 @@ __device__ __forceinline__ ScoreSmem carve_smem(uint8_t* raw, int nb, int row_le
   return m;
 }
 
+// pass-1 kernel: tables + rows; pass-2 kernel: + emit buffers, tightening buckets and slot data.
 template <int NC>
-static size_t score_smem_bytes(int nb, int row_len) {
-  return 8 * (size_t)NC * (nb + 2) + sizeof(int32_t) * 3 * (size_t)row_len + (size_t)kWarps * kEmitBuf * 32 +
-         (size_t)kWarps * kJ1 * NC * 32 * sizeof(uint16_t);
+static size_t score_smem_bytes(int nb, int row_len, bool pass2 = true) {
+  const size_t base = 8 * (size_t)NC * (nb + 2) + sizeof(int32_t) * 3 * (size_t)row_len;
+  if (!pass2) return base;
+  return base + (size_t)kWarps * kEmitBuf * 32 + (size_t)kWarps * kJ1 * NC * 32 * sizeof(uint16_t);
 }
 
 // Stage the c2 rows of (k2, k3, b): B(c2) and R(c2) (Q(c2) is k3-independent).
@@ -566,7 +619,7 @@ __device__ __forceinline__ K3Range k3_range(const DevModel& md) {
   // tiles start at c1_base = 3 mod 4 so that every c2 group c1_base + 1 + 4i is aligned
   r.c1_base0 = r.c1lo - ((r.c1lo - 3) & 3);
   r.ntiles = (r.c1hi - r.c1_base0 + 32 * kJ1) / (32 * kJ1);
-  r.c2_from = r.c1_base0 + 1;          // >= 0
+  r.c2_from = max(0, r.c1_base0);      // rows cover every c2 > c1_base0 and every c1 (Q(c1) = P[k2][c1])
   r.c2_to = ((M + 3) & ~3) + 4;        // padded, exclusive
   return r;
 }
@@ -705,7 +758,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
         t = __shfl_sync(FULL_MASK, t, 0);
         if (t >= r.ntiles) break;
         k3_tile<NC, 1>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin,
-                       sm.tb0 + warp * (kJ1 * NC * 32), out, em, feas, cand);
+                       nullptr, out, em, feas, cand);
       }
       if (__syncthreads_or(feas != feas0) && !(pb.debug_flags & 2)) {
         if (tid == 0) {
@@ -758,6 +811,10 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
     stage_rows(cx, sm, k3, r.c2_from, r.c2_to, true);
     if (tid == 0) s_tile = 0;
     __syncthreads();
+    int Bmin = INT_MAX;  // min over the unit's c2 of B(c2) (bounds E from below)
+    for (int c2 = r.c1lo + 1 + lane; c2 < cx.M; c2 += 32) Bmin = min(Bmin, sm.Bs[c2]);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) Bmin = min(Bmin, __shfl_xor_sync(FULL_MASK, Bmin, d));
 #pragma unroll 1
     for (;;) {
       int t = 0;
@@ -765,7 +822,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
       t = __shfl_sync(FULL_MASK, t, 0);
       if (t >= r.ntiles) break;
       k3_tile<NC, 2>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin,
-                     sm.tb0 + warp * (kJ1 * NC * 32), out, em, feas, cand);
+                     sm.tb0 + warp * (kJ1 * NC * 32), out, em, feas, cand, Bmin);
     }
     __syncthreads();
   }
@@ -775,7 +832,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
 // Shared memory per CTA: the fold tables take what the budget leaves after the
 // three staged c2 rows (B, Q, R), the emit buffers and the pass-2 slot data,
 // rounded down to a power of two (128..2048 buckets).
-constexpr size_t kSmemBudget = 27 * 1024;
+constexpr size_t kSmemBudget = 27 * 1024;  // sized for the pass-2 kernel (8 CTAs per SM)
 
 template <int NC>
 static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches) {
@@ -783,17 +840,18 @@ static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaS
   int nb_log2 = 7;
   while (nb_log2 < 11 && score_smem_bytes<NC>(2 << nb_log2, row_len) <= kSmemBudget) ++nb_log2;
   const size_t smem = score_smem_bytes<NC>(1 << nb_log2, row_len);
+  const size_t smem_a = score_smem_bytes<NC>(1 << nb_log2, row_len, false);
   const unsigned grid = (unsigned)pb.n_local * NC * pb.B;
   cudaError_t e;
   const size_t smem12 = score12_smem_bytes<NC>(1 << nb_log2);
   e = cudaFuncSetAttribute(score12_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem12);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(score3a_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  e = cudaFuncSetAttribute(score3a_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(score3b_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (pb.Kmax >= 3) {
-    score3a_kernel<NC><<<grid, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
+    score3a_kernel<NC><<<grid, 32 * kWarps, smem_a, s>>>(pb, out, nb_log2, row_len);
     score3b_kernel<NC><<<148 * (16 / kWarps), 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
     *n_launches += 2;
   }
