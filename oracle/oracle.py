@@ -92,6 +92,8 @@ def run_oracle(w, model_lo: int = 0, model_hi: Optional[int] = None, only_K: int
     for i, mp in enumerate(w.models):
         lat = np.ascontiguousarray(mp.lat_us, dtype=np.uint32)
         S = np.ascontiguousarray(mp.act_bytes, dtype=np.uint64)
+        if lat.ndim != 3 or lat.shape[0] != w.n_classes or lat.shape[2] != w.n_batches or S.shape != (lat.shape[1],):
+            raise ValueError(f"model {i}: lat_us {lat.shape} / act_bytes {S.shape} do not match the workload")
         keep += [lat, S]
         models[i].n_layers = lat.shape[1]
         models[i].lat_us = _u32p(lat)

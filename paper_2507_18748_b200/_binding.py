@@ -130,13 +130,17 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
-def _models_array(lat_us, act_bytes):
+def _models_array(lat_us, act_bytes, n_classes=None, n_batches=None):
     n = len(lat_us)
     models = (_Model * n)()
     keep = []
     for i in range(n):
         lat = np.ascontiguousarray(lat_us[i], dtype=np.uint32)
         S = np.ascontiguousarray(act_bytes[i], dtype=np.uint64)
+        if lat.ndim != 3 or (n_classes is not None and lat.shape[0] != n_classes) or \
+                (n_batches is not None and lat.shape[2] != n_batches) or S.shape != (lat.shape[1],):
+            raise PPipeError(PPIPE_EINVAL, f"model {i}: lat_us must be [n_classes][n_layers][n_batches] and "
+                                           f"act_bytes [n_layers]; got {lat.shape} and {S.shape}")
         keep += [lat, S]
         models[i].n_layers = lat.shape[1]
         models[i].lat_us = _u32p(lat)
@@ -154,8 +158,8 @@ def load_profiles(lat_us: Sequence[np.ndarray], act_bytes: Sequence[np.ndarray],
                   batches: np.ndarray, bw_bits_per_us: np.ndarray, rank: int = 0, world: int = 1,
                   device: int = -1, nccl_id: Optional[bytes] = None) -> Context:
     n = len(lat_us)
-    models, keep = _models_array(lat_us, act_bytes)
     b = np.ascontiguousarray(batches, dtype=np.uint32)
+    models, keep = _models_array(lat_us, act_bytes, n_classes, len(b))
     bw = np.ascontiguousarray(bw_bits_per_us, dtype=np.uint32).reshape(-1)
     idbuf = ct.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
     dist = _Dist(rank, world, device, ct.cast(idbuf, ct.c_void_p) if idbuf is not None else None)

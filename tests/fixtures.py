@@ -15,6 +15,7 @@ def make_workload(lat_by_model, S_by_model, bw, batches, slo, margin=0, kmax=3, 
         lat = np.asarray(lat, dtype=np.uint32)
         if lat.ndim == 2:
             lat = lat[:, :, None]
+        assert lat.shape[2] == len(batches), (lat.shape, batches)
         models.append(ModelProfile(f"fx{i}", lat, np.asarray(S, dtype=np.uint64)))
     C = models[0].lat_us.shape[0]
     bw = np.asarray(bw, dtype=np.uint32)

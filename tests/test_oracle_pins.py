@@ -76,7 +76,8 @@ def test_p0b_tie_break_canonical_cut(oracle_built):
 
 def test_p1_v100_bs2_162_req_per_s(oracle_built):
     # V100, batch 2, 12.3 ms -> (2 x 1 / 0.0123) = 162 req/s; SLO 33.3 ms, 40% margin.
-    w = make_workload([[[6660, 12300]]], [[0]], 10000, [1, 2], 33300, margin=400, kmax=1)
+    w = make_workload([np.array([6660, 12300], dtype=np.uint32).reshape(1, 1, 2)], [[0]], 10000, [1, 2], 33300,
+                      margin=400, kmax=1)
     r = run_oracle(w)
     pts = seg_points(r, w, 0, 1, (0,))
     last = pts[-1]
