@@ -448,7 +448,7 @@ PPIPE_API int ppipe_load_profiles(ppipe_ctx** out, uint32_t n_models, const ppip
       fail(c, PPIPE_ECUDA, "cudaEventCreate failed");
       return bail(PPIPE_ECUDA);
     }
-  if (cudaMallocHost(&c->h_counters, 5 * sizeof(unsigned long long)) != cudaSuccess) {
+  if (cudaMallocHost(&c->h_counters, 16 * sizeof(unsigned long long)) != cudaSuccess) {
     fail(c, PPIPE_ENOMEM, "cudaMallocHost failed");
     return bail(PPIPE_ENOMEM);
   }
@@ -522,7 +522,7 @@ PPIPE_API int ppipe_load_profiles(ppipe_ctx** out, uint32_t n_models, const ppip
   CUL(c->d_bwv.reserve(c->V));
   CUL(c->d_pairv.reserve(pairv.size()));
   CUL(c->d_segbase.reserve(n_models));
-  CUL(c->d_counters.reserve(5));
+  CUL(c->d_counters.reserve(16));
   // host -> device: the profiles this rank needs
   for (size_t i = 0; i < c->local.size(); ++i) {
     const int m = c->local[i];
@@ -625,7 +625,7 @@ static int run_enumerate(ppipe_ctx* c) {
   CU(c, launch_pack(pb, c->stream));
   c->launches_i += pb.n_local ? 2 : 0;
   CU(c, cudaEventRecord(c->ev[1], c->stream));
-  CU(c, cudaMemsetAsync(c->d_counters.p, 0, 5 * sizeof(unsigned long long), c->stream));
+  CU(c, cudaMemsetAsync(c->d_counters.p, 0, 16 * sizeof(unsigned long long), c->stream));
   CU(c, launch_score(pb, so, c->stream, &c->launches_i));
   CU(c, cudaEventRecord(c->ev[2], c->stream));
   return PPIPE_OK;
@@ -660,7 +660,7 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
   CU(c, cudaSetDevice(c->device));
   // survivors; grow and re-run on overflow (deterministic, so the result is unchanged)
   for (;;) {
-    CU(c, cudaMemcpyAsync(c->h_counters, c->d_counters.p, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+    CU(c, cudaMemcpyAsync(c->h_counters, c->d_counters.p, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                           c->stream));
     CU(c, cudaStreamSynchronize(c->stream));
     const bool surv_ok = c->h_counters[0] <= c->d_surv.n;
@@ -672,6 +672,11 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
     if (rc != PPIPE_OK) return rc;
   }
   const uint64_t n_surv = c->h_counters[0];
+  if (const char* dbg = getenv("PPIPE_DEBUG_FLAGS"))
+    if (atoi(dbg) & 8)
+      fprintf(stderr, "ppipe debug: hot units %llu, pass-2 tiles %llu, visits %llu, slot-hits %llu, emit-calls %llu, "
+              "survivors %llu, feasible %llu\n", c->h_counters[3], c->h_counters[7], c->h_counters[5],
+              c->h_counters[6], c->h_counters[8], c->h_counters[0], c->h_counters[1]);
   uint64_t n_feas = c->h_counters[1], n_cand = c->h_counters[2];
   int nl = c->launches_i;
   // local frontier

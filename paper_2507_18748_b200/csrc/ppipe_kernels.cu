@@ -328,6 +328,60 @@ __device__ __forceinline__ int any_feasible(const int (&thr)[kJ1][NC], int Bv, i
   return h;
 }
 
+// Main-phase fast test for a whole aligned group of 4 c2 values: does any of this
+// lane's 4 x kJ1 x NC candidates pass? Same per-candidate split as any_feasible
+// (one ISETP or one IMAD each), but one predicate and one vote per group; the
+// per-c2 flags are recomputed only when the group hits (rare).
+template <int NC>
+__device__ __forceinline__ int any_feasible4(const int (&thr)[kJ1][NC], const int4& b4, int m1) {
+  constexpr bool kTwo = NC >= 7;
+  const int bv[4] = {b4.x, b4.y, b4.z, b4.w};
+  int acc[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    acc[u] = -1;
+#pragma unroll
+    for (int j = 0; j < kJ1; ++j) {
+#pragma unroll
+      for (int k = 1; k < (kTwo ? NC - 1 : NC); ++k) acc[u] &= mad_diff(bv[u], m1, thr[j][k]);
+    }
+  }
+  const int a = acc[0] & acc[1] & acc[2] & acc[3];
+  int h;
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.gt.s32 p, %1, -1;\n\t"
+      "setp.le.or.s32 p, %2, %6, p;\n\tsetp.le.or.s32 p, %2, %7, p;\n\t"
+      "setp.le.or.s32 p, %2, %8, p;\n\tsetp.le.or.s32 p, %2, %9, p;\n\t"
+      "setp.le.or.s32 p, %3, %6, p;\n\tsetp.le.or.s32 p, %3, %7, p;\n\t"
+      "setp.le.or.s32 p, %3, %8, p;\n\tsetp.le.or.s32 p, %3, %9, p;\n\t"
+      "setp.le.or.s32 p, %4, %6, p;\n\tsetp.le.or.s32 p, %4, %7, p;\n\t"
+      "setp.le.or.s32 p, %4, %8, p;\n\tsetp.le.or.s32 p, %4, %9, p;\n\t"
+      "setp.le.or.s32 p, %5, %6, p;\n\tsetp.le.or.s32 p, %5, %7, p;\n\t"
+      "setp.le.or.s32 p, %5, %8, p;\n\tsetp.le.or.s32 p, %5, %9, p;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(h)
+      : "r"(a), "r"(bv[0]), "r"(bv[1]), "r"(bv[2]), "r"(bv[3]), "r"(thr[0][0]), "r"(thr[1][0]), "r"(thr[2][0]),
+        "r"(thr[3][0]));
+  if (kTwo) {
+    int h2;
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.le.s32 p, %1, %5;\n\tsetp.le.or.s32 p, %1, %6, p;\n\t"
+        "setp.le.or.s32 p, %1, %7, p;\n\tsetp.le.or.s32 p, %1, %8, p;\n\t"
+        "setp.le.or.s32 p, %2, %5, p;\n\tsetp.le.or.s32 p, %2, %6, p;\n\t"
+        "setp.le.or.s32 p, %2, %7, p;\n\tsetp.le.or.s32 p, %2, %8, p;\n\t"
+        "setp.le.or.s32 p, %3, %5, p;\n\tsetp.le.or.s32 p, %3, %6, p;\n\t"
+        "setp.le.or.s32 p, %3, %7, p;\n\tsetp.le.or.s32 p, %3, %8, p;\n\t"
+        "setp.le.or.s32 p, %4, %5, p;\n\tsetp.le.or.s32 p, %4, %6, p;\n\t"
+        "setp.le.or.s32 p, %4, %7, p;\n\tsetp.le.or.s32 p, %4, %8, p;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(h2)
+        : "r"(bv[0]), "r"(bv[1]), "r"(bv[2]), "r"(bv[3]), "r"(thr[0][NC - 1]), "r"(thr[1][NC - 1]),
+          "r"(thr[2][NC - 1]), "r"(thr[3][NC - 1]));
+    h |= h2;
+  }
+  return h;
+}
+
 // Hit flags of one aligned group of 4 c2 values inside diagonal band JB: slots
 // j < JB are complete pairs, slot JB holds pairs for lanes < c2 - (c1_base + 32 JB).
 template <int NC, int JB>
@@ -455,7 +509,8 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
     const int rel = c2 - c1_base;  // 1 mod 4; the group is rel .. rel + 3
     int h0, h1, h2, h3;
     if (rel > 32 * kJ1) {
-      h0 = any_feasible<NC>(thr, b4.x, m1);
+      if (!__any_sync(FULL_MASK, any_feasible4<NC>(thr, b4, m1))) continue;
+      h0 = any_feasible<NC>(thr, b4.x, m1);  // the group hit: per-c2 flags for the slow path
       h1 = any_feasible<NC>(thr, b4.y, m1);
       h2 = any_feasible<NC>(thr, b4.z, m1);
       h3 = any_feasible<NC>(thr, b4.w, m1);
