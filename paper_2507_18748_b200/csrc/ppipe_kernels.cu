@@ -710,64 +710,72 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   Emitter em{ebuf + warp * 2 * kEmitBuf, 0};
   const int ntab = NC * (nb + 2);
+  // CTA = (model, k2); it loops over the batches (the K <= 2 work per batch is small).
   const int k2 = blockIdx.x % NC;
-  const int ml = (blockIdx.x / NC) % pb.n_local;
-  const int bi = blockIdx.x / (NC * pb.n_local);
+  const int ml = blockIdx.x / NC;
   const DevModel md = pb.models[ml];
-  CtaCtx<NC> cx;
-  make_ctx(cx, pb, md, k2, bi, nb);
-  const int M = cx.M, T = cx.T, sh = cx.sh, q = cx.q;
   unsigned long long feas = 0, cand = 0;
-
-  // K = 1: segment (k2), whole model on class k2
-  if (warp == 0 && md.row_lo == 0) {
-    const int E = cx.P2[M];
-    if (lane == 0) ++cand;
-    const bool f = lane == 0 && E <= T;
-    if (f) ++feas;
-    if (__any_sync(FULL_MASK, f)) emit_warp(out, em, f, make_rec(md.model, 1, 0, 0, k2, 0xFF, 0xFF, cx.b, E, E, 0, 0));
-  }
-  // K = 2: segments (k1, k2); c1 in this rank's rows
-  if (pb.Kmax >= 2 && M >= 2) {
+  bool dirty = true;
+#pragma unroll 1
+  for (int bi = 0; bi < pb.B; ++bi) {
+    CtaCtx<NC> cx;
+    make_ctx(cx, pb, md, k2, bi, nb);
+    const int M = cx.M, T = cx.T, sh = cx.sh, q = cx.q;
+    // K = 1: segment (k2), whole model on class k2
+    if (warp == 0 && md.row_lo == 0) {
+      const int E = cx.P2[M];
+      if (lane == 0) ++cand;
+      const bool f = lane == 0 && E <= T;
+      if (f) ++feas;
+      if (__any_sync(FULL_MASK, f))
+        emit_warp(out, em, f, make_rec(md.model, 1, 0, 0, k2, 0xFF, 0xFF, cx.b, E, E, 0, 0));
+    }
+    // K = 2: segments (k1, k2); c1 in this rank's rows
+    if (pb.Kmax < 2 || M < 2) continue;
     const int lo = max(1, (int)md.row_lo), hi = min(M - 1, (int)md.row_hi - 1);
-    if (lo <= hi) {
+    if (lo > hi) continue;
+    if (dirty) {
       reset_raw(raw, ntab, tid, 32 * kWarps);
       __syncthreads();
-      const int P2M = cx.P2[M];
-      int anyf = 0;
+      dirty = false;
+    }
+    const int P2M = cx.P2[M];
+    int anyf = 0;
 #pragma unroll 1
-      for (int pass = 1; pass <= 2; ++pass) {
+    for (int pass = 1; pass <= 2; ++pass) {
 #pragma unroll 1
-        for (int base = lo; base <= hi; base += 32 * kWarps) {
-          const int c1 = base + tid;
-          const bool valid = c1 <= hi;
-          const int C2 = valid ? P2M - __ldg(cx.P2 + c1) : 0;
+      for (int base = lo; base <= hi; base += 32 * kWarps) {
+        const int c1 = base + tid;
+        const bool valid = c1 <= hi;
+        const int C2 = valid ? P2M - __ldg(cx.P2 + c1) : 0;
 #pragma unroll
-          for (int k1 = 0; k1 < NC; ++k1) {
-            const int C1 = valid ? __ldg(cx.Prow(k1) + c1) : 0;
-            const int y = valid ? __ldg(cx.Yrow(k1, k2) + c1) : 0;
-            const int E = C1 + y + C2;
-            const bool f = valid && E <= T;
-            const int Cmax = max(C1, C2);
-            if (pass == 1) {
-              if (valid) ++cand;
-              if (f) {
-                ++feas;
-                anyf = 1;
-                atomicMin(raw + (size_t)k1 * (nb + 2) + (E >> sh), pack_key(E, Cmax, sh, q));
-              }
-            } else {
-              const bool cond = f && survives(fin + (size_t)k1 * (nb + 2), f ? (E >> sh) : 0, E, Cmax, sh, q);
-              if (__any_sync(FULL_MASK, cond))
-                emit_warp(out, em, cond, make_rec(md.model, 2, c1, 0, k1, k2, 0xFF, cx.b, E, C1, C2, 0));
+        for (int k1 = 0; k1 < NC; ++k1) {
+          const int C1 = valid ? __ldg(cx.Prow(k1) + c1) : 0;
+          const int y = valid ? __ldg(cx.Yrow(k1, k2) + c1) : 0;
+          const int E = C1 + y + C2;
+          const bool f = valid && E <= T;
+          const int Cmax = max(C1, C2);
+          if (pass == 1) {
+            if (valid) ++cand;
+            if (f) {
+              ++feas;
+              anyf = 1;
+              atomicMin(raw + (size_t)k1 * (nb + 2) + (E >> sh), pack_key(E, Cmax, sh, q));
             }
+          } else {
+            const bool cond = f && survives(fin + (size_t)k1 * (nb + 2), f ? (E >> sh) : 0, E, Cmax, sh, q);
+            if (__any_sync(FULL_MASK, cond))
+              emit_warp(out, em, cond, make_rec(md.model, 2, c1, 0, k1, k2, 0xFF, cx.b, E, C1, C2, 0));
           }
         }
-        if (pass == 1) {
-          if (!__syncthreads_or(anyf)) break;
-          tables_finalize(raw, fin, NC, nb, sh, warp, kWarps);
-          __syncthreads();
-        }
+      }
+      if (pass == 1) {
+        if (!__syncthreads_or(anyf)) break;
+        dirty = true;
+        tables_finalize(raw, fin, NC, nb, sh, warp, kWarps);
+        __syncthreads();
+      } else {
+        __syncthreads();
       }
     }
   }
@@ -910,7 +918,7 @@ static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaS
     score3b_kernel<NC><<<148 * (16 / kWarps), 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
     *n_launches += 2;
   }
-  score12_kernel<NC><<<grid, 32 * kWarps, smem12, s>>>(pb, out, nb_log2);
+  score12_kernel<NC><<<(unsigned)pb.n_local * NC, 32 * kWarps, smem12, s>>>(pb, out, nb_log2);
   ++*n_launches;
   return cudaGetLastError();
 }
