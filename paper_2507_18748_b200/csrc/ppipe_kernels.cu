@@ -419,8 +419,8 @@ __device__ __forceinline__ void band_hits(const int (&thr)[kJ1][NC], const int4&
 template <int NC, int pass>
 __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, int c1_hi,
                         const int32_t* Bs, const int32_t* Qs, const int32_t* Rs, uint32_t* raw, const uint2* fin,
-                        uint16_t* tb0, const ScoreOut& out, Emitter& em, unsigned long long& feas,
-                        unsigned long long& cand, int Bmin = 0) {
+                        uint16_t* tb0, uint32_t* nb16, const ScoreOut& out, Emitter& em,
+                        unsigned long long& feas, unsigned long long& cand, int Bmin = 0) {
   const int lane = threadIdx.x & 31;
   const int nb = cx.nb;
   int thr[kJ1][NC];
@@ -503,8 +503,55 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
     c2_start = c1_base + 1 + (max(0, wlo - (c1_base + 1)) & ~3);  // keep groups aligned
     c2_end = min(M, whi + 1);
   }
+  // ---- 16-bit prefilter ----
+  // Every candidate is first tested in a 16-bit lane: thresholds and B(c2) are
+  // offset by L = min_c2 B(c2) + 16383 and saturated to 15 bits, so one
+  // VIADD.16x2 computes thr - B for two candidates and LOP3 AND-reduces the sign
+  // bits. Saturation can only turn a "no" into a "yes" (B never saturates low by
+  // the choice of L), so a group passing here is re-tested exactly in 32 bits
+  // below; a group failing here has no feasible candidate.
+  constexpr int kPairs = (kJ1 * NC + 1) / 2;
+  unsigned thr16[kPairs];
+  {
+    int bmin = INT_MAX;
+    for (int c2 = c2_start + lane; c2 < c2_end; c2 += 32) bmin = min(bmin, Bs[c2]);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) bmin = min(bmin, __shfl_xor_sync(FULL_MASK, bmin, d));
+    const long long L = (long long)bmin + 16383;
+    for (int c2 = c2_start + lane; c2 < c2_end + 4; c2 += 32) {
+      const long long v = (long long)Bs[c2] - L;
+      const int sv = (int)max(-16383ll, min(16383ll, v));
+      nb16[c2] = ((unsigned)(-sv) & 0xffffu) * 0x10001u;  // (-s, -s)
+    }
+#pragma unroll
+    for (int p = 0; p < kPairs; ++p) {
+      unsigned w = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = 2 * p + h;
+        int tv = -16384;  // unused half: never passes
+        if (i < kJ1 * NC) tv = (int)max(-16384ll, min(16383ll, (long long)thr[i / NC][i % NC] - L));
+        w |= ((unsigned)tv & 0xffffu) << (16 * h);
+      }
+      thr16[p] = w;
+    }
+    __syncwarp();
+  }
 #pragma unroll 1
   for (int c2 = c2_start; c2 < c2_end; c2 += 4) {
+    {
+      const uint4 n4 = *reinterpret_cast<const uint4*>(nb16 + c2);
+      unsigned a0 = 0xffffffffu, a1 = 0xffffffffu, a2 = 0xffffffffu, a3 = 0xffffffffu;
+#pragma unroll
+      for (int p = 0; p < kPairs; ++p) {
+        a0 &= __vadd2(thr16[p], n4.x);
+        a1 &= __vadd2(thr16[p], n4.y);
+        a2 &= __vadd2(thr16[p], n4.z);
+        a3 &= __vadd2(thr16[p], n4.w);
+      }
+      const unsigned a = a0 & a1 & a2 & a3;
+      if (!__any_sync(FULL_MASK, (a & 0x80008000u) != 0x80008000u)) continue;
+    }
     const int4 b4 = *reinterpret_cast<const int4*>(Bs + c2);
     const int rel = c2 - c1_base;  // 1 mod 4; the group is rel .. rel + 3
     int h0, h1, h2, h3;
@@ -619,6 +666,7 @@ struct ScoreSmem {
   int32_t* Rs;    // [row_len] R(c2) = C_3 for the current k3
   int4* ebuf;     // [kWarps][kEmitBuf][2] survivor records
   uint16_t* tb0;  // [kWarps][kJ1 * NC][32] pass-2 tightening buckets
+  uint32_t* nb16; // [kWarps][row_len] per-warp packed 16-bit (-B, -B) rows of the prefilter
 };
 
 template <int NC>
@@ -629,7 +677,8 @@ __device__ __forceinline__ ScoreSmem carve_smem(uint8_t* raw, int nb, int row_le
   m.Bs = reinterpret_cast<int32_t*>(m.fin + (size_t)NC * (nb + 2));
   m.Qs = m.Bs + row_len;
   m.Rs = m.Qs + row_len;
-  m.ebuf = reinterpret_cast<int4*>(m.Rs + row_len);
+  m.nb16 = reinterpret_cast<uint32_t*>(m.Rs + row_len);
+  m.ebuf = reinterpret_cast<int4*>(m.nb16 + (size_t)kWarps * row_len);
   m.tb0 = reinterpret_cast<uint16_t*>(m.ebuf + kWarps * 2 * kEmitBuf);
   return m;
 }
@@ -637,7 +686,7 @@ __device__ __forceinline__ ScoreSmem carve_smem(uint8_t* raw, int nb, int row_le
 // pass-1 kernel: tables + rows; pass-2 kernel: + emit buffers, tightening buckets and slot data.
 template <int NC>
 static size_t score_smem_bytes(int nb, int row_len, bool pass2 = true) {
-  const size_t base = 8 * (size_t)NC * (nb + 2) + sizeof(int32_t) * 3 * (size_t)row_len;
+  const size_t base = 8 * (size_t)NC * (nb + 2) + sizeof(int32_t) * (3 + kWarps) * (size_t)row_len;
   if (!pass2) return base;
   return base + (size_t)kWarps * kEmitBuf * 32 + (size_t)kWarps * kJ1 * NC * 32 * sizeof(uint16_t);
 }
@@ -821,7 +870,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
         t = __shfl_sync(FULL_MASK, t, 0);
         if (t >= r.ntiles) break;
         k3_tile<NC, 1>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin,
-                       nullptr, out, em, feas, cand);
+                       nullptr, sm.nb16 + warp * row_len, out, em, feas, cand);
       }
       if (__syncthreads_or(feas != feas0) && !(pb.debug_flags & 2)) {
         if (tid == 0) {
@@ -885,7 +934,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
       t = __shfl_sync(FULL_MASK, t, 0);
       if (t >= r.ntiles) break;
       k3_tile<NC, 2>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin,
-                     sm.tb0 + warp * (kJ1 * NC * 32), out, em, feas, cand, Bmin);
+                     sm.tb0 + warp * (kJ1 * NC * 32), sm.nb16 + warp * row_len, out, em, feas, cand, Bmin);
     }
     __syncthreads();
   }
@@ -895,7 +944,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
 // Shared memory per CTA: the fold tables take what the budget leaves after the
 // three staged c2 rows (B, Q, R), the emit buffers and the pass-2 slot data,
 // rounded down to a power of two (128..2048 buckets).
-constexpr size_t kSmemBudget = 27 * 1024;  // sized for the pass-2 kernel (8 CTAs per SM)
+constexpr size_t kSmemBudget = 32 * 1024;  // sized for the pass-2 kernel (7 CTAs per SM)
 
 template <int NC>
 static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches) {
