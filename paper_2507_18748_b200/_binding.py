@@ -15,7 +15,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libppipe_b200.so")
+# PPIPE_LIB: load another in-tree build of the same sources (tuning experiments, scripts/variants.py)
+LIB_PATH = os.environ.get("PPIPE_LIB") or os.path.join(_PKG, "libppipe_b200.so")
 
 PPIPE_OK, PPIPE_EINVAL, PPIPE_ERANGE, PPIPE_ENOMEM, PPIPE_ECUDA, PPIPE_ENCCL, PPIPE_ESTATE = 0, -1, -2, -3, -4, -5, -6
 _CODES = {-1: "EINVAL", -2: "ERANGE", -3: "ENOMEM", -4: "ECUDA", -5: "ENCCL", -6: "ESTATE"}

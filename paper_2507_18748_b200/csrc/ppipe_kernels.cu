@@ -504,24 +504,36 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
     c2_end = min(M, whi + 1);
   }
   // ---- 16-bit prefilter ----
-  // Every candidate is first tested in a 16-bit lane: thresholds and B(c2) are
-  // offset by L = min_c2 B(c2) + 16383 and saturated to 15 bits, so one
-  // VIADD.16x2 computes thr - B for two candidates and LOP3 AND-reduces the sign
-  // bits. Saturation can only turn a "no" into a "yes" (B never saturates low by
-  // the choice of L), so a group passing here is re-tested exactly in 32 bits
-  // below; a group failing here has no feasible candidate.
+  // Every candidate is first tested in a 16-bit field: thresholds and B(c2) are
+  // offset by L = min_c2 B(c2) + 16383 and saturated to 15 bits, then stored
+  // offset-binary (t' = thr - L + 16384 in [0, 32767], n' = 16384 - (B - L) in
+  // [1, 32767]), so t' + n' never carries out of its 16-bit field and its bit 15
+  // is set exactly when thr - B >= 0. One plain 32-bit add therefore tests two
+  // candidates, and ptxas is free to issue it as IADD3 (ALU pipe) or IMAD.IADD
+  // (FMA pipe), which balances the two pipes; LOP3 OR-reduces the bits.
+  // Saturation can only turn a "no" into a "yes" (B never saturates low by the
+  // choice of L), so a group passing here is re-tested exactly in 32 bits below;
+  // a group failing here has no feasible candidate.
   constexpr int kPairs = (kJ1 * NC + 1) / 2;
+  // kQ64 64-bit words (4 candidates each) are added as IADD3 (ALU) + IMAD.X (FMA);
+  // the other words as IMAD.IADD / VIADD.16x2 (FMA). With the LOP3 reduction on the
+  // ALU pipe, (kPairs - 2) / 4 wide words balances the two half-rate pipes.
+  constexpr int kQ64 = (kPairs - 2) / 4;
   unsigned thr16[kPairs];
+  unsigned long long thr64[kQ64 > 0 ? kQ64 : 1];
   {
     int bmin = INT_MAX;
     for (int c2 = c2_start + lane; c2 < c2_end; c2 += 32) bmin = min(bmin, Bs[c2]);
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) bmin = min(bmin, __shfl_xor_sync(FULL_MASK, bmin, d));
     const long long L = (long long)bmin + 16383;
-    for (int c2 = c2_start + lane; c2 < c2_end + 4; c2 += 32) {
-      const long long v = (long long)Bs[c2] - L;
+    // entries past c2_end hold n' = 0 (never pass) so that the unrolled, prefetching
+    // scan below may read up to 16 values ahead
+    const int fill_end = ((c2_end + 3) & ~3) + 12;
+    for (int c2 = c2_start + lane; c2 < fill_end; c2 += 32) {
+      const long long v = (long long)Bs[min(c2, c2_end - 1)] - L;
       const int sv = (int)max(-16383ll, min(16383ll, v));
-      nb16[c2] = ((unsigned)(-sv) & 0xffffu) * 0x10001u;  // (-s, -s)
+      nb16[c2] = c2 < c2_end ? (unsigned)(16384 - sv) * 0x10001u : 0u;  // (n', n')
     }
 #pragma unroll
     for (int p = 0; p < kPairs; ++p) {
@@ -529,28 +541,64 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int i = 2 * p + h;
-        int tv = -16384;  // unused half: never passes
-        if (i < kJ1 * NC) tv = (int)max(-16384ll, min(16383ll, (long long)thr[i / NC][i % NC] - L));
-        w |= ((unsigned)tv & 0xffffu) << (16 * h);
+        int tv = 0;  // unused half: never passes
+        if (i < kJ1 * NC) tv = (int)max(-16384ll, min(16383ll, (long long)thr[i / NC][i % NC] - L)) + 16384;
+        w |= (unsigned)tv << (16 * h);
       }
       thr16[p] = w;
     }
+#pragma unroll
+    for (int q = 0; q < kQ64; ++q) thr64[q] = ((unsigned long long)thr16[2 * q + 1] << 32) | thr16[2 * q];
     __syncwarp();
   }
+  // Prefilter hit bits of one aligned group of 4 c2 values (bit 15 / 31 of the result).
+  auto group_bits = [&](const uint4& n4) -> unsigned {
+    unsigned a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    const unsigned n4v[4] = {n4.x, n4.y, n4.z, n4.w};
+    unsigned* const acc[4] = {&a0, &a1, &a2, &a3};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const unsigned long long nw = ((unsigned long long)n4v[u] << 32) | n4v[u];
+#pragma unroll
+      for (int q = 0; q < kQ64; ++q) {  // no field carries, so neither does the low word
+        const unsigned long long x = thr64[q] + nw;
+        *acc[u] |= (unsigned)x | (unsigned)(x >> 32);
+      }
+#pragma unroll
+      for (int p = 2 * kQ64; p < kPairs; ++p) *acc[u] |= thr16[p] + n4v[u];
+    }
+    return (a0 | a1 | a2 | a3) & 0x80008000u;
+  };
+  const uint4* const nrow = reinterpret_cast<const uint4*>(nb16);
 #pragma unroll 1
   for (int c2 = c2_start; c2 < c2_end; c2 += 4) {
-    {
-      const uint4 n4 = *reinterpret_cast<const uint4*>(nb16 + c2);
-      unsigned a0 = 0xffffffffu, a1 = 0xffffffffu, a2 = 0xffffffffu, a3 = 0xffffffffu;
-#pragma unroll
-      for (int p = 0; p < kPairs; ++p) {
-        a0 &= __vadd2(thr16[p], n4.x);
-        a1 &= __vadd2(thr16[p], n4.y);
-        a2 &= __vadd2(thr16[p], n4.z);
-        a3 &= __vadd2(thr16[p], n4.w);
+    // Fast scan: two groups per iteration, one vote, next pair prefetched; stops at
+    // the first group in which some lane's prefilter passes.
+    if (pass == 2) {  // short tightened ranges: one group per iteration
+#pragma unroll 1
+      for (;;) {
+        if (__any_sync(FULL_MASK, group_bits(nrow[c2 >> 2]) != 0u)) break;
+        c2 += 4;
+        if (c2 >= c2_end) break;
       }
-      const unsigned a = a0 & a1 & a2 & a3;
-      if (!__any_sync(FULL_MASK, (a & 0x80008000u) != 0x80008000u)) continue;
+      if (c2 >= c2_end) break;
+    } else {
+      uint4 na = nrow[c2 >> 2], nbq = nrow[(c2 >> 2) + 1];
+#pragma unroll 1
+      for (;;) {
+        const uint4 pa = nrow[(c2 >> 2) + 2], pb = nrow[(c2 >> 2) + 3];
+        const unsigned ha = group_bits(na);
+        const unsigned hb = group_bits(nbq);
+        if (__any_sync(FULL_MASK, (ha | hb) != 0u)) {
+          if (!__any_sync(FULL_MASK, ha != 0u)) c2 += 4;
+          break;
+        }
+        c2 += 8;
+        if (c2 >= c2_end) break;
+        na = pa;
+        nbq = pb;
+      }
+      if (c2 >= c2_end) break;
     }
     const int4 b4 = *reinterpret_cast<const int4*>(Bs + c2);
     const int rel = c2 - c1_base;  // 1 mod 4; the group is rel .. rel + 3
@@ -836,8 +884,16 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
 // a shared counter). Counts every candidate and feasible candidate and builds the
 // bucket-best tables of each (k_2, k_3, b) unit; units with a feasible candidate
 // are "hot": their finalized tables go to global memory for kernel 3. ----
+#ifndef PPIPE_3A_CTAS_PER_SM
+#define PPIPE_3A_CTAS_PER_SM 8
+#endif
+constexpr int k3aCtasPerSm = PPIPE_3A_CTAS_PER_SM;
+#ifndef PPIPE_3B_CTAS_PER_SM
+#define PPIPE_3B_CTAS_PER_SM 6
+#endif
+constexpr int k3bCtasPerSm = PPIPE_3B_CTAS_PER_SM;  // pass 2 holds more live state: fewer, fatter warps
 template <int NC>
-__global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
+__global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
     score3a_kernel(Problem pb, ScoreOut out, int nb_log2, int row_len) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ int s_tile;
@@ -894,7 +950,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
 // from a counter): reload the unit's tables, re-scan with tightened thresholds and
 // emit the survivors. ----
 template <int NC>
-__global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
+__global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
     score3b_kernel(Problem pb, ScoreOut out, int nb_log2, int row_len) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ int s_tile;
@@ -948,7 +1004,7 @@ constexpr size_t kSmemBudget = 32 * 1024;  // sized for the pass-2 kernel (7 CTA
 
 template <int NC>
 static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches) {
-  const int row_len = (int)((((size_t)pb.max_M + 3) & ~(size_t)3) + 4);
+  const int row_len = (int)((((size_t)pb.max_M + 3) & ~(size_t)3) + 16);
   int nb_log2 = 7;
   while (nb_log2 < 11 && score_smem_bytes<NC>(2 << nb_log2, row_len) <= kSmemBudget) ++nb_log2;
   const size_t smem = score_smem_bytes<NC>(1 << nb_log2, row_len);
@@ -964,7 +1020,7 @@ static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaS
   if (e != cudaSuccess) return e;
   if (pb.Kmax >= 3) {
     score3a_kernel<NC><<<grid, 32 * kWarps, smem_a, s>>>(pb, out, nb_log2, row_len);
-    score3b_kernel<NC><<<148 * (16 / kWarps), 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
+    score3b_kernel<NC><<<148 * k3bCtasPerSm, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
     *n_launches += 2;
   }
   score12_kernel<NC><<<(unsigned)pb.n_local * NC, 32 * kWarps, smem12, s>>>(pb, out, nb_log2);
@@ -974,7 +1030,7 @@ static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaS
 
 // Bytes of one hot unit's tables for this problem (the ABI sizes its buffer with it).
 size_t hot_unit_table_bytes(const Problem& pb) {
-  const int row_len = (int)((((size_t)pb.max_M + 3) & ~(size_t)3) + 4);
+  const int row_len = (int)((((size_t)pb.max_M + 3) & ~(size_t)3) + 16);
   int nb_log2 = 7;
   auto smem_for = [&](int nb) -> size_t {
     switch (pb.C) {

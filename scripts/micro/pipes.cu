@@ -48,6 +48,45 @@ __global__ void k_mix(unsigned* out, unsigned seed, int iters) {  // 2 VIADD.16x
   }
   out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
+
+__global__ void k_iadd(unsigned* out, unsigned seed, int iters) {
+  unsigned a[8];
+  for (int i = 0; i < 8; ++i) a[i] = seed * (threadIdx.x + i + 1);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("add.u32 %0, %0, %1;" : "+r"(a[i]) : "r"(a[(i + 3) & 7]));
+  }
+  unsigned r = 0;
+  for (int i = 0; i < 8; ++i) r ^= a[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = r;
+}
+__global__ void k_iadd3(unsigned* out, unsigned seed, int iters) {
+  unsigned a[8];
+  for (int i = 0; i < 8; ++i) a[i] = seed * (threadIdx.x + i + 1);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { unsigned t; asm volatile("add.u32 %1, %0, %2;\n\tadd.u32 %0, %1, %3;" : "+r"(a[i]), "=r"(t) : "r"(a[(i + 3) & 7]), "r"(seed)); }
+  }
+  unsigned r = 0;
+  for (int i = 0; i < 8; ++i) r ^= a[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = r;
+}
+// balanced: per 8 pairs -> 5 IMAD (fma) + 3 IADD (alu) + 4 LOP3 (alu, 2-pair OR accumulate)
+__global__ void k_bal(unsigned* out, unsigned seed, int iters) {
+  unsigned a[8], acc0 = 0, acc1 = 0;
+  for (int i = 0; i < 8; ++i) a[i] = seed * (threadIdx.x + i + 1);
+  unsigned nb = seed & 0x7fff7fffu; const unsigned one = seed >> 31 | 1u;
+  for (int it = 0; it < iters; ++it) {
+    unsigned s[8];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(s[i]) : "r"(a[i]), "r"(one), "r"(nb));
+#pragma unroll
+    for (int i = 5; i < 8; ++i) asm volatile("add.u32 %0, %1, %2;" : "=r"(s[i]) : "r"(a[i]), "r"(nb));
+    acc0 |= s[0] | s[1]; acc1 |= s[2] | s[3]; acc0 |= s[4] | s[5]; acc1 |= s[6] | s[7];
+    nb += 0x00010001u;
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc0 ^ acc1;
+}
 int main() {
   unsigned* d;
   cudaMalloc(&d, 148 * 1024 * 4 * 8);
@@ -71,5 +110,8 @@ int main() {
   run("imad", k_imad, 8);
   run("lop3", k_lop3, 8);
   run("mix", k_mix, 8 + 4 + 1);
+  run("iadd", k_iadd, 8);
+  run("iadd3", k_iadd3, 8);
+  run("bal", k_bal, 8 + 4 + 1);
   return 0;
 }

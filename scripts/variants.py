@@ -1,0 +1,27 @@
+"""Build compile-time variants of libppipe_b200.so into variants/<name>.so (tuning only).
+
+usage: python scripts/variants.py name1:-DFOO=1,-DBAR=2 name2:-DFOO=3 ...
+Run one with PPIPE_LIB=variants/<name>.so python bench.py ...
+"""
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2507_18748_b200.build import nvcc_cmd  # noqa: E402
+
+os.makedirs(os.path.join(ROOT, "variants"), exist_ok=True)
+
+
+def one(spec):
+    name, _, flags = spec.partition(":")
+    out = os.path.join(ROOT, "variants", name + ".so")
+    r = subprocess.run(nvcc_cmd(out, [f for f in flags.split(",") if f]), capture_output=True, text=True)
+    return name, r.returncode, (r.stdout + r.stderr)[-400:] if r.returncode else ""
+
+
+with ThreadPoolExecutor(4) as ex:
+    for name, rc, err in ex.map(one, sys.argv[1:]):
+        print(name, "ok" if rc == 0 else "FAILED " + err)
