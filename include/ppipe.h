@@ -106,8 +106,12 @@ typedef struct {
 /* Replace the profile values of an existing context (same model count and
  * layer counts, same classes and batches): validate and copy host -> device.
  * Profiles change as workloads drift and the planner re-runs;
- * this keeps the device buffers and the NCCL communicator. Errors as for
- * ppipe_load_profiles. Invalidates the last ppipe_enumerate. */
+ * this keeps the device buffers and the NCCL communicator. The host -> device
+ * copies overlap the host-side validation; the call returns only after both, so
+ * the caller may reuse its buffers at once (page-locked buffers copy fastest).
+ * Errors as for ppipe_load_profiles; after a failed update the context has no
+ * usable profiles and ppipe_enumerate returns PPIPE_ESTATE until an update
+ * succeeds. Invalidates the last ppipe_enumerate. */
 int ppipe_update_profiles(ppipe_ctx *ctx, uint32_t n_models, const ppipe_model *models);
 
 /* Enqueue the whole enumeration on the context's stream: pack (prefix sums,
@@ -134,8 +138,9 @@ typedef struct {
   uint64_t n_feasible;    /* all ranks: candidates with E <= T_eff */
   uint64_t n_points;      /* frontier points */
   uint64_t n_segments;    /* sum_m sum_{K <= min(Kmax, M)} C^K, canonical order (m, K, tuple lexicographic) */
-  const ppipe_point *points;     /* host copy, NULL unless copy_to_host */
-  const uint64_t *seg_offsets;   /* host [n_segments + 1] CSR, NULL unless copy_to_host */
+  const ppipe_point *points;     /* host copy in a page-locked buffer owned by ctx, valid until the
+                                    next ppipe_pareto / ppipe_free; NULL unless copy_to_host */
+  const uint64_t *seg_offsets;   /* host [n_segments + 1] CSR, same ownership; NULL unless copy_to_host */
   const ppipe_point *d_points;   /* device (this rank's GPU), same content */
   const uint64_t *d_seg_offsets; /* device [n_segments + 1] */
   uint64_t n_survivors;   /* diagnostics: this rank's pre-frontier survivor count */

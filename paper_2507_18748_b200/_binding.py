@@ -200,7 +200,10 @@ class Frontier:
     n_feasible_local: int = 0
 
 
-def pareto(ctx: Context, copy_to_host: bool = True) -> Frontier:
+def pareto(ctx: Context, copy_to_host: bool = True, zero_copy: bool = False) -> Frontier:
+    """Run the frontier pass. copy_to_host: also return host arrays. zero_copy: those
+    arrays are views of the context's page-locked result buffer (no host memcpy),
+    valid only until the next pareto() / free() on this context."""
     f = _Frontier()
     _check(lib().ppipe_pareto(ctx.handle, 1 if copy_to_host else 0, ct.byref(f)), ctx.handle)
     pts = seg = None
@@ -208,10 +211,14 @@ def pareto(ctx: Context, copy_to_host: bool = True) -> Frontier:
         n = int(f.n_points)
         if n:
             buf = (ct.c_char * (32 * n)).from_address(f.points)
-            pts = np.frombuffer(buf, dtype=POINT_DTYPE).copy()
+            pts = np.frombuffer(buf, dtype=POINT_DTYPE)
+            if not zero_copy:
+                pts = pts.copy()
         else:
             pts = np.zeros(0, dtype=POINT_DTYPE)
-        seg = np.ctypeslib.as_array(f.seg_offsets, shape=(int(f.n_segments) + 1,)).copy()
+        seg = np.ctypeslib.as_array(f.seg_offsets, shape=(int(f.n_segments) + 1,))
+        if not zero_copy:
+            seg = seg.copy()
     return Frontier(int(f.n_candidates), int(f.n_feasible), int(f.n_points), int(f.n_segments),
                     int(f.n_survivors), pts, seg, int(f.d_points or 0), int(f.d_seg_offsets or 0),
                     int(f.n_candidates_local), int(f.n_feasible_local))

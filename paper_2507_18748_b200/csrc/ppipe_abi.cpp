@@ -84,6 +84,28 @@ struct DevBuf {
   }
 };
 
+// Page-locked host buffer (grow-only): D2H results land here at full link speed.
+template <typename T>
+struct HostBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaError_t reserve(size_t want) {
+    if (want <= n && p) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    const size_t cap = std::max<size_t>(want + want / 4, 1);
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p), cap * sizeof(T), cudaHostAllocDefault);
+    if (e == cudaSuccess) n = cap;
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
 // Row weights of the partition (candidates per first-cut row, §8(e)).
 // row 0: K = 1 (C * B); row r in [1, M-1]: K = 2 (C^2 B) + K = 3 with c_1 = r (C^3 B (M-1-r)).
 inline unsigned __int128 row_weight(uint32_t M, uint32_t r, uint64_t C, uint64_t B, uint32_t kmax) {
@@ -178,8 +200,9 @@ struct ppipe_ctx {
   DevBuf<ppipe_point> d_surv, d_local, d_gather, d_union, d_final;
   DevBuf<uint64_t> d_segoff_local, d_segoff_final, d_cnt_send, d_cnt_recv;
   FrontierScratch scratch;
-  std::vector<ppipe_point> h_points;
-  std::vector<uint64_t> h_segoff;
+  HostBuf<ppipe_point> h_points;  // pinned: last copy_to_host result (valid until the next ppipe_pareto)
+  HostBuf<uint64_t> h_segoff;
+  bool profiles_ok = true;  // false after a failed ppipe_update_profiles
   unsigned long long* h_counters = nullptr;  // pinned [5]
   // enumerate state
   bool enumerated = false;
@@ -247,6 +270,8 @@ void free_ctx(ppipe_ctx* c) {
   c->d_segoff_final.release();
   c->d_cnt_send.release();
   c->d_cnt_recv.release();
+  c->h_points.release();
+  c->h_segoff.release();
   if (c->scratch.buf) cudaFree(c->scratch.buf);
   if (c->h_counters) cudaFreeHost(c->h_counters);
   for (auto& e : c->ev)
@@ -550,21 +575,33 @@ PPIPE_API int ppipe_update_profiles(ppipe_ctx* c, uint32_t n_models, const ppipe
     if (models[m].n_layers != c->Ms[m])
       return fail(c, PPIPE_EINVAL, "model %u: n_layers %u differs from the loaded %u", m, models[m].n_layers,
                   c->Ms[m]);
-  {
-    std::string verr;
-    const int vrc = validate_models(n_models, models, c->C, c->B, c->h_batches.data(), &verr);
-    if (vrc != PPIPE_OK) return fail(c, vrc, "%s", verr.c_str());
-  }
-  CU(c, cudaSetDevice(c->device));
-  for (size_t i = 0; i < c->local.size(); ++i) {
-    const int m = c->local[i];
-    const DevModel& d = c->h_models[i];
-    CU(c, cudaMemcpyAsync(c->d_lat.p + d.lat_off, models[m].lat_us, sizeof(uint32_t) * c->C * d.M * c->B,
-                          cudaMemcpyHostToDevice, c->stream));
-    CU(c, cudaMemcpyAsync(c->d_s.p + d.s_off, models[m].act_bytes, sizeof(uint64_t) * d.M, cudaMemcpyHostToDevice,
-                          c->stream));
-  }
-  CU(c, cudaStreamSynchronize(c->stream));
+  // The H2D copies (issued from a helper thread, so that pageable sources overlap
+  // too) run while the host validates the same bytes; a failed validation leaves
+  // the context without usable profiles until the next successful update.
+  c->profiles_ok = false;
+  c->enumerated = false;
+  cudaError_t copy_err = cudaSuccess;
+  std::thread copier([&] {
+    copy_err = cudaSetDevice(c->device);
+    for (size_t i = 0; i < c->local.size() && copy_err == cudaSuccess; ++i) {
+      const int m = c->local[i];
+      const DevModel& d = c->h_models[i];
+      copy_err = cudaMemcpyAsync(c->d_lat.p + d.lat_off, models[m].lat_us, sizeof(uint32_t) * c->C * d.M * c->B,
+                                 cudaMemcpyHostToDevice, c->stream);
+      if (copy_err == cudaSuccess)
+        copy_err = cudaMemcpyAsync(c->d_s.p + d.s_off, models[m].act_bytes, sizeof(uint64_t) * d.M,
+                                   cudaMemcpyHostToDevice, c->stream);
+    }
+    // the caller may release its buffers once we return
+    const cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (copy_err == cudaSuccess) copy_err = e;
+  });
+  std::string verr;
+  const int vrc = validate_models(n_models, models, c->C, c->B, c->h_batches.data(), &verr);
+  copier.join();
+  if (vrc != PPIPE_OK) return fail(c, vrc, "%s", verr.c_str());
+  CU(c, copy_err);
+  c->profiles_ok = true;
   c->enumerated = false;
   return PPIPE_OK;
 }
@@ -638,6 +675,8 @@ PPIPE_API int ppipe_enumerate(ppipe_ctx* ctx, const ppipe_enum_params* p) {
     return fail(ctx, PPIPE_EINVAL, "max_partitions %u: must be 1..3", p->max_partitions);
   if (p->margin_permille >= 1000)
     return fail(ctx, PPIPE_EINVAL, "margin_permille %u: must be < 1000", p->margin_permille);
+  if (!ctx->profiles_ok)
+    return fail(ctx, PPIPE_ESTATE, "ppipe_enumerate: the last ppipe_update_profiles failed; profiles are unusable");
   for (uint32_t m = 0; m < ctx->n_models; ++m) {
     const uint64_t T = (uint64_t)p->slo_us[m] * (1000 - p->margin_permille) / 1000;
     if (T >= (uint64_t)kRangeLimit)
@@ -754,15 +793,14 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
   out->n_candidates_local = c->h_counters[2];
   out->n_feasible_local = c->h_counters[1];
   if (copy_to_host) {
-    c->h_points.resize(n_pts);
-    c->h_segoff.resize(c->n_seg_total + 1);
+    CU(c, c->h_points.reserve(n_pts));
+    CU(c, c->h_segoff.reserve(c->n_seg_total + 1));
     if (n_pts)
-      CU(c, cudaMemcpyAsync(c->h_points.data(), d_pts, sizeof(ppipe_point) * n_pts, cudaMemcpyDeviceToHost,
-                            c->stream));
-    CU(c, cudaMemcpyAsync(c->h_segoff.data(), d_off, 8 * (c->n_seg_total + 1), cudaMemcpyDeviceToHost, c->stream));
+      CU(c, cudaMemcpyAsync(c->h_points.p, d_pts, sizeof(ppipe_point) * n_pts, cudaMemcpyDeviceToHost, c->stream));
+    CU(c, cudaMemcpyAsync(c->h_segoff.p, d_off, 8 * (c->n_seg_total + 1), cudaMemcpyDeviceToHost, c->stream));
     CU(c, cudaStreamSynchronize(c->stream));
-    out->points = c->h_points.data();
-    out->seg_offsets = c->h_segoff.data();
+    out->points = c->h_points.p;
+    out->seg_offsets = c->h_segoff.p;
   }
   return PPIPE_OK;
 }
