@@ -416,10 +416,31 @@ __device__ __forceinline__ void band_hits(const int (&thr)[kJ1][NC], const int4&
 // dominated (C_1 >= U(E)) never leave the fast loop. Q(c_2) = P[k2][c_2] and
 // R(c_2) = C_3 are shared-memory rows like B. The fast loop and the slow paths
 // each exist once in the code (one pass-generic instance).
+// Pass-2 per-warp slot data: the dense survivor pass reads any lane's slot.
+struct SlotData {
+  int32_t* As;     // [kJ1 * NC][32] A = C1 + Y1 - P[k2][c1], so E = A + B(c2)
+  int32_t* C1s;    // [kJ1 * NC][32] C_1
+  int32_t* p1s;    // [kJ1][32] P[k2][c1]
+  uint16_t* list;  // [kJ1 * NC * 32] (lane << 5 | slot) of the current c2
+};
+template <int NC>
+__host__ __device__ constexpr size_t slot_bytes() {
+  return (size_t)kJ1 * 32 * (2 * sizeof(int32_t) * NC + sizeof(int32_t) + sizeof(uint16_t) * NC);
+}
+template <int NC>
+__device__ __forceinline__ SlotData carve_slot(uint8_t* base) {
+  SlotData d;
+  d.As = reinterpret_cast<int32_t*>(base);
+  d.C1s = d.As + kJ1 * NC * 32;
+  d.p1s = d.C1s + kJ1 * NC * 32;
+  d.list = reinterpret_cast<uint16_t*>(d.p1s + kJ1 * 32);
+  return d;
+}
+
 template <int NC, int pass>
 __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, int c1_hi,
                         const int32_t* Bs, const int32_t* Qs, const int32_t* Rs, uint32_t* raw, const uint2* fin,
-                        uint16_t* tb0, uint32_t* nb16, const ScoreOut& out, Emitter& em,
+                        const SlotData& sd, uint32_t* nb16, const ScoreOut& out, Emitter& em,
                         unsigned long long& feas, unsigned long long& cand, int Bmin = 0) {
   const int lane = threadIdx.x & 31;
   const int nb = cx.nb;
@@ -482,11 +503,14 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
             }
           }
         }
-        tb0[(j * NC + k1) * 32 + lane] = (uint16_t)b0;  // pass-2 tightening bucket (this warp's slice)
+        // this lane's slot data for the dense survivor pass (E = A + B(c2) exactly)
+        sd.As[(j * NC + k1) * 32 + lane] = valid ? C1 + y - p1[j] : 0;
+        sd.C1s[(j * NC + k1) * 32 + lane] = C1;
       }
       thr[j][k1] = t;
       c1r[j][k1] = C1;
     }
+    if (pass == 2) sd.p1s[j * 32 + lane] = p1[j];
     if (pass == 1 && valid) cand += (unsigned long long)(cx.M - 1 - c1) * NC;
   }
   const int m1 = cx.m1;
@@ -650,30 +674,51 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
           }
         }
       } else {
+        // Dense survivor pass: the (lane, slot) pairs that pass the tightened
+        // threshold are listed warp-wide, then checked 32 at a time, one per lane,
+        // against the finalized tables (survives()) and emitted.
         const int c2u = c2 + u;
+        unsigned fm = 0;
 #pragma unroll
         for (int j = 0; j < kJ1; ++j) {
           const bool v = 32 * j + lane < relu;
-          bool fj = false;
 #pragma unroll
-          for (int k1 = 0; k1 < NC; ++k1) fj |= v && (Bv <= thr[j][k1]);
-          if (!__any_sync(FULL_MASK, fj)) continue;
-          const int c1 = c1_base + 32 * j + lane;
-          const int C2 = Q - p1[j];
-#pragma unroll
-          for (int k1 = 0; k1 < NC; ++k1) {
-            const int b0 = tb0[(j * NC + k1) * 32 + lane];
-            // undo the tightening to recover the exact E = T - thr_orig + B
-            const int thr_o = thr[j][k1] - (b0 < nb ? min(0, (b0 << cx.sh) - 1 - cx.T) : 0);
-            const int E = cx.T - thr_o + Bv;
-            const int Cmax = max(max(c1r[j][k1], C2), R);
-            const bool f = v && (Bv <= thr[j][k1]);
-            const bool cond =
-                f && survives(fin + (size_t)k1 * (nb + 2), E >> cx.sh, E, Cmax, cx.sh, cx.q);
-            if (__any_sync(FULL_MASK, cond))
-              emit_warp(out, em, cond, make_rec(cx.model, 3, c1, c2u, k1, cx.k2, k3, cx.b, E, c1r[j][k1], C2, R));
-          }
+          for (int k1 = 0; k1 < NC; ++k1) fm |= (v && Bv <= thr[j][k1]) ? (1u << (j * NC + k1)) : 0u;
         }
+        const int cnt = __popc(fm);
+        int incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int t = __shfl_up_sync(FULL_MASK, incl, d);
+          if (lane >= d) incl += t;
+        }
+        const int total = __shfl_sync(FULL_MASK, incl, 31);
+        int pos = incl - cnt;
+        while (fm) {
+          const int sl = __ffs(fm) - 1;
+          fm &= fm - 1;
+          sd.list[pos++] = (uint16_t)((lane << 5) | sl);
+        }
+        __syncwarp();
+#pragma unroll 1
+        for (int base = 0; base < total; base += 32) {
+          const int i = base + lane;
+          bool cond = false;
+          Rec rec{};
+          if (i < total) {
+            const unsigned e = sd.list[i];
+            const int src = (int)(e >> 5), sl = (int)(e & 31u);
+            const int j = sl / NC, k1 = sl - j * NC;
+            const int E = sd.As[sl * 32 + src] + Bv;
+            const int C1 = sd.C1s[sl * 32 + src];
+            const int C2 = Q - sd.p1s[j * 32 + src];
+            const int Cmax = max(max(C1, C2), R);
+            cond = survives(fin + (size_t)k1 * (nb + 2), E >> cx.sh, E, Cmax, cx.sh, cx.q);
+            if (cond) rec = make_rec(cx.model, 3, c1_base + 32 * j + src, c2u, k1, cx.k2, k3, cx.b, E, C1, C2, R);
+          }
+          if (__any_sync(FULL_MASK, cond)) emit_warp(out, em, cond, rec);
+        }
+        __syncwarp();  // the list is rewritten by the next u
       }
     }
   }
@@ -713,7 +758,7 @@ struct ScoreSmem {
   int32_t* Qs;    // [row_len] Q(c2) = P[k2][b][c2]
   int32_t* Rs;    // [row_len] R(c2) = C_3 for the current k3
   int4* ebuf;     // [kWarps][kEmitBuf][2] survivor records
-  uint16_t* tb0;  // [kWarps][kJ1 * NC][32] pass-2 tightening buckets
+  uint8_t* slot;  // [kWarps] SlotData regions (pass 2)
   uint32_t* nb16; // [kWarps][row_len] per-warp packed 16-bit (-B, -B) rows of the prefilter
 };
 
@@ -727,7 +772,7 @@ __device__ __forceinline__ ScoreSmem carve_smem(uint8_t* raw, int nb, int row_le
   m.Rs = m.Qs + row_len;
   m.nb16 = reinterpret_cast<uint32_t*>(m.Rs + row_len);
   m.ebuf = reinterpret_cast<int4*>(m.nb16 + (size_t)kWarps * row_len);
-  m.tb0 = reinterpret_cast<uint16_t*>(m.ebuf + kWarps * 2 * kEmitBuf);
+  m.slot = reinterpret_cast<uint8_t*>(m.ebuf + kWarps * 2 * kEmitBuf);
   return m;
 }
 
@@ -736,7 +781,15 @@ template <int NC>
 static size_t score_smem_bytes(int nb, int row_len, bool pass2 = true) {
   const size_t base = 8 * (size_t)NC * (nb + 2) + sizeof(int32_t) * (3 + kWarps) * (size_t)row_len;
   if (!pass2) return base;
-  return base + (size_t)kWarps * kEmitBuf * 32 + (size_t)kWarps * kJ1 * NC * 32 * sizeof(uint16_t);
+  return base + (size_t)kWarps * kEmitBuf * 32 + (size_t)kWarps * slot_bytes<NC>();
+}
+
+// The bucket count (table resolution) follows a fixed smem policy, independent of
+// the pass-2 slot data, so that both kernels and the ABI agree on it.
+template <int NC>
+static size_t table_policy_bytes(int nb, int row_len) {
+  return 8 * (size_t)NC * (nb + 2) + sizeof(int32_t) * (3 + kWarps) * (size_t)row_len +
+         (size_t)kWarps * kEmitBuf * 32 + (size_t)kWarps * kJ1 * NC * 32 * sizeof(uint16_t);
 }
 
 // Stage the c2 rows of (k2, k3, b): B(c2) and R(c2) (Q(c2) is k3-independent).
@@ -926,7 +979,7 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
         t = __shfl_sync(FULL_MASK, t, 0);
         if (t >= r.ntiles) break;
         k3_tile<NC, 1>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin,
-                       nullptr, sm.nb16 + warp * row_len, out, em, feas, cand);
+                       SlotData{}, sm.nb16 + warp * row_len, out, em, feas, cand);
       }
       if (__syncthreads_or(feas != feas0) && !(pb.debug_flags & 2)) {
         if (tid == 0) {
@@ -990,7 +1043,7 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
       t = __shfl_sync(FULL_MASK, t, 0);
       if (t >= r.ntiles) break;
       k3_tile<NC, 2>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin,
-                     sm.tb0 + warp * (kJ1 * NC * 32), sm.nb16 + warp * row_len, out, em, feas, cand, Bmin);
+                     carve_slot<NC>(sm.slot + warp * slot_bytes<NC>()), sm.nb16 + warp * row_len, out, em, feas, cand, Bmin);
     }
     __syncthreads();
   }
@@ -1006,7 +1059,7 @@ template <int NC>
 static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches) {
   const int row_len = (int)((((size_t)pb.max_M + 3) & ~(size_t)3) + 16);
   int nb_log2 = 7;
-  while (nb_log2 < 11 && score_smem_bytes<NC>(2 << nb_log2, row_len) <= kSmemBudget) ++nb_log2;
+  while (nb_log2 < 11 && table_policy_bytes<NC>(2 << nb_log2, row_len) <= kSmemBudget) ++nb_log2;
   const size_t smem = score_smem_bytes<NC>(1 << nb_log2, row_len);
   const size_t smem_a = score_smem_bytes<NC>(1 << nb_log2, row_len, false);
   const unsigned grid = (unsigned)pb.n_local * NC * pb.B;
@@ -1020,7 +1073,12 @@ static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaS
   if (e != cudaSuccess) return e;
   if (pb.Kmax >= 3) {
     score3a_kernel<NC><<<grid, 32 * kWarps, smem_a, s>>>(pb, out, nb_log2, row_len);
-    score3b_kernel<NC><<<148 * k3bCtasPerSm, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
+    int dev = 0, n_sm = 148, smem_sm = 227 * 1024;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    const int ctas = std::max(1, std::min(k3bCtasPerSm, smem_sm / (int)(smem + 1024)));  // persistent: fill the SMs
+    score3b_kernel<NC><<<n_sm * ctas, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
     *n_launches += 2;
   }
   score12_kernel<NC><<<(unsigned)pb.n_local * NC, 32 * kWarps, smem12, s>>>(pb, out, nb_log2);
@@ -1034,14 +1092,14 @@ size_t hot_unit_table_bytes(const Problem& pb) {
   int nb_log2 = 7;
   auto smem_for = [&](int nb) -> size_t {
     switch (pb.C) {
-      case 1: return score_smem_bytes<1>(nb, row_len);
-      case 2: return score_smem_bytes<2>(nb, row_len);
-      case 3: return score_smem_bytes<3>(nb, row_len);
-      case 4: return score_smem_bytes<4>(nb, row_len);
-      case 5: return score_smem_bytes<5>(nb, row_len);
-      case 6: return score_smem_bytes<6>(nb, row_len);
-      case 7: return score_smem_bytes<7>(nb, row_len);
-      default: return score_smem_bytes<8>(nb, row_len);
+      case 1: return table_policy_bytes<1>(nb, row_len);
+      case 2: return table_policy_bytes<2>(nb, row_len);
+      case 3: return table_policy_bytes<3>(nb, row_len);
+      case 4: return table_policy_bytes<4>(nb, row_len);
+      case 5: return table_policy_bytes<5>(nb, row_len);
+      case 6: return table_policy_bytes<6>(nb, row_len);
+      case 7: return table_policy_bytes<7>(nb, row_len);
+      default: return table_policy_bytes<8>(nb, row_len);
     }
   };
   while (nb_log2 < 11 && smem_for(2 << nb_log2) <= kSmemBudget) ++nb_log2;
