@@ -143,6 +143,10 @@ __device__ __forceinline__ Rec make_rec(uint32_t model, int K, int c1, int c2, i
   return r;
 }
 
+#ifndef PPIPE_SCAN_UNROLL
+#define PPIPE_SCAN_UNROLL 2
+#endif
+constexpr int kScanUnroll = PPIPE_SCAN_UNROLL;  // prefilter groups per vote in the pass-1 scan
 constexpr int kWarps = 2;      // warps per CTA (share the fold tables and the staged rows)
 constexpr int kEmitBuf = 32;   // survivor records staged per warp before a global flush
 
@@ -553,7 +557,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
     const long long L = (long long)bmin + 16383;
     // entries past c2_end hold n' = 0 (never pass) so that the unrolled, prefetching
     // scan below may read up to 16 values ahead
-    const int fill_end = ((c2_end + 3) & ~3) + 12;
+    const int fill_end = ((c2_end + 3) & ~3) + 8 * kScanUnroll - 4;
     for (int c2 = c2_start + lane; c2 < fill_end; c2 += 32) {
       const long long v = (long long)Bs[min(c2, c2_end - 1)] - L;
       const int sv = (int)max(-16383ll, min(16383ll, v));
@@ -607,20 +611,29 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
       }
       if (c2 >= c2_end) break;
     } else {
-      uint4 na = nrow[c2 >> 2], nbq = nrow[(c2 >> 2) + 1];
+      uint4 cur[kScanUnroll];
+#pragma unroll
+      for (int g = 0; g < kScanUnroll; ++g) cur[g] = nrow[(c2 >> 2) + g];
 #pragma unroll 1
       for (;;) {
-        const uint4 pa = nrow[(c2 >> 2) + 2], pb = nrow[(c2 >> 2) + 3];
-        const unsigned ha = group_bits(na);
-        const unsigned hb = group_bits(nbq);
-        if (__any_sync(FULL_MASK, (ha | hb) != 0u)) {
-          if (!__any_sync(FULL_MASK, ha != 0u)) c2 += 4;
+        uint4 nxt[kScanUnroll];
+#pragma unroll
+        for (int g = 0; g < kScanUnroll; ++g) nxt[g] = nrow[(c2 >> 2) + kScanUnroll + g];
+        unsigned hg[kScanUnroll], hor = 0;
+#pragma unroll
+        for (int g = 0; g < kScanUnroll; ++g) hor |= hg[g] = group_bits(cur[g]);
+        if (__any_sync(FULL_MASK, hor != 0u)) {
+#pragma unroll
+          for (int g = 0; g < kScanUnroll - 1; ++g) {
+            if (__any_sync(FULL_MASK, hg[g] != 0u)) break;
+            c2 += 4;
+          }
           break;
         }
-        c2 += 8;
+        c2 += 4 * kScanUnroll;
         if (c2 >= c2_end) break;
-        na = pa;
-        nbq = pb;
+#pragma unroll
+        for (int g = 0; g < kScanUnroll; ++g) cur[g] = nxt[g];
       }
       if (c2 >= c2_end) break;
     }
@@ -860,14 +873,14 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   Emitter em{ebuf + warp * 2 * kEmitBuf, 0};
   const int ntab = NC * (nb + 2);
-  // CTA = (model, k2); it loops over the batches (the K <= 2 work per batch is small).
-  const int k2 = blockIdx.x % NC;
-  const int ml = blockIdx.x / NC;
+  // CTA = (model, k2, batch): many small CTAs keep enough loads in flight (the
+  // K <= 2 work of one batch is a few hundred c_1 rows).
+  const int bi = blockIdx.x % pb.B;
+  const int k2 = (blockIdx.x / pb.B) % NC;
+  const int ml = blockIdx.x / (pb.B * NC);
   const DevModel md = pb.models[ml];
   unsigned long long feas = 0, cand = 0;
-  bool dirty = true;
-#pragma unroll 1
-  for (int bi = 0; bi < pb.B; ++bi) {
+  do {
     CtaCtx<NC> cx;
     make_ctx(cx, pb, md, k2, bi, nb);
     const int M = cx.M, T = cx.T, sh = cx.sh, q = cx.q;
@@ -881,14 +894,11 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
         emit_warp(out, em, f, make_rec(md.model, 1, 0, 0, k2, 0xFF, 0xFF, cx.b, E, E, 0, 0));
     }
     // K = 2: segments (k1, k2); c1 in this rank's rows
-    if (pb.Kmax < 2 || M < 2) continue;
+    if (pb.Kmax < 2 || M < 2) break;
     const int lo = max(1, (int)md.row_lo), hi = min(M - 1, (int)md.row_hi - 1);
-    if (lo > hi) continue;
-    if (dirty) {
-      reset_raw(raw, ntab, tid, 32 * kWarps);
-      __syncthreads();
-      dirty = false;
-    }
+    if (lo > hi) break;
+    reset_raw(raw, ntab, tid, 32 * kWarps);
+    __syncthreads();
     const int P2M = cx.P2[M];
     int anyf = 0;
 #pragma unroll 1
@@ -921,14 +931,11 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
       }
       if (pass == 1) {
         if (!__syncthreads_or(anyf)) break;
-        dirty = true;
         tables_finalize(raw, fin, NC, nb, sh, warp, kWarps);
-        __syncthreads();
-      } else {
         __syncthreads();
       }
     }
-  }
+  } while (false);
   emit_flush(out, em);
   flush_counters(out, feas, cand);
 }
@@ -1057,7 +1064,7 @@ constexpr size_t kSmemBudget = 32 * 1024;  // sized for the pass-2 kernel (7 CTA
 
 template <int NC>
 static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches) {
-  const int row_len = (int)((((size_t)pb.max_M + 3) & ~(size_t)3) + 16);
+  const int row_len = (int)((((size_t)pb.max_M + 3) & ~(size_t)3) + 8 * kScanUnroll);
   int nb_log2 = 7;
   while (nb_log2 < 11 && table_policy_bytes<NC>(2 << nb_log2, row_len) <= kSmemBudget) ++nb_log2;
   const size_t smem = score_smem_bytes<NC>(1 << nb_log2, row_len);
@@ -1081,14 +1088,14 @@ static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaS
     score3b_kernel<NC><<<n_sm * ctas, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
     *n_launches += 2;
   }
-  score12_kernel<NC><<<(unsigned)pb.n_local * NC, 32 * kWarps, smem12, s>>>(pb, out, nb_log2);
+  score12_kernel<NC><<<(unsigned)pb.n_local * NC * pb.B, 32 * kWarps, smem12, s>>>(pb, out, nb_log2);
   ++*n_launches;
   return cudaGetLastError();
 }
 
 // Bytes of one hot unit's tables for this problem (the ABI sizes its buffer with it).
 size_t hot_unit_table_bytes(const Problem& pb) {
-  const int row_len = (int)((((size_t)pb.max_M + 3) & ~(size_t)3) + 16);
+  const int row_len = (int)((((size_t)pb.max_M + 3) & ~(size_t)3) + 8 * kScanUnroll);
   int nb_log2 = 7;
   auto smem_for = [&](int nb) -> size_t {
     switch (pb.C) {
