@@ -861,8 +861,14 @@ static size_t score12_smem_bytes(int nb) {
   return 8 * (size_t)NC * (nb + 2) + ((4 * (size_t)NC * (nb + 2) + 15) & ~(size_t)15) + (size_t)kWarps * kEmitBuf * 32;
 }
 
+#ifndef PPIPE_12_CTAS_PER_SM
+#define PPIPE_12_CTAS_PER_SM 16
+#endif
+#ifndef PPIPE_12_NB_LOG2_MAX
+#define PPIPE_12_NB_LOG2_MAX 7
+#endif
 template <int NC>
-__global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
+__global__ void __launch_bounds__(32 * kWarps, PPIPE_12_CTAS_PER_SM)
     score12_kernel(Problem pb, ScoreOut out, int nb_log2) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int nb = 1 << nb_log2;
@@ -1071,7 +1077,10 @@ static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaS
   const size_t smem_a = score_smem_bytes<NC>(1 << nb_log2, row_len, false);
   const unsigned grid = (unsigned)pb.n_local * NC * pb.B;
   cudaError_t e;
-  const size_t smem12 = score12_smem_bytes<NC>(1 << nb_log2);
+  // K <= 2 tables live only inside score12 (never in the hot-unit buffer), so their
+  // resolution may differ from the K = 3 tables.
+  const int nb12_log2 = std::min(nb_log2, PPIPE_12_NB_LOG2_MAX);
+  const size_t smem12 = score12_smem_bytes<NC>(1 << nb12_log2);
   e = cudaFuncSetAttribute(score12_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem12);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(score3a_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a);
@@ -1088,7 +1097,7 @@ static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaS
     score3b_kernel<NC><<<n_sm * ctas, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
     *n_launches += 2;
   }
-  score12_kernel<NC><<<(unsigned)pb.n_local * NC * pb.B, 32 * kWarps, smem12, s>>>(pb, out, nb_log2);
+  score12_kernel<NC><<<(unsigned)pb.n_local * NC * pb.B, 32 * kWarps, smem12, s>>>(pb, out, nb12_log2);
   ++*n_launches;
   return cudaGetLastError();
 }
