@@ -181,6 +181,9 @@ struct ppipe_ctx {
   std::vector<uint32_t> h_batches;
   std::vector<uint32_t> rows;      // [2*n_models] this rank's row ranges
   std::vector<int> local;          // local model ids (work order)
+  std::vector<uint64_t> h_segbase; // [n_models + 1] first global segment of each model (last enumerate)
+  DevBuf<uint64_t> d_segtmp;       // merge: segment id per final point
+  DevBuf<ppipe_point> d_merged;    // merge: re-reduced frontier of the straddling models
   std::vector<DevModel> h_models;  // per local model
   uint32_t max_M = 0;
   // device inputs
@@ -270,6 +273,8 @@ void free_ctx(ppipe_ctx* c) {
   c->d_segoff_final.release();
   c->d_cnt_send.release();
   c->d_cnt_recv.release();
+  c->d_segtmp.release();
+  c->d_merged.release();
   c->h_points.release();
   c->h_segoff.release();
   if (c->scratch.buf) cudaFree(c->scratch.buf);
@@ -621,6 +626,8 @@ static int run_enumerate(ppipe_ctx* c) {
     }
   }
   c->n_seg_total = acc;
+  c->h_segbase = segbase;
+  c->h_segbase.push_back(acc);
   for (size_t i = 0; i < c->local.size(); ++i) c->h_models[i].slo_us = c->last_slo[c->local[i]];
   CU(c, cudaMemcpyAsync(c->d_segbase.p, segbase.data(), 8 * segbase.size(), cudaMemcpyHostToDevice, c->stream));
   CU(c, cudaMemcpyAsync(c->d_models.p, c->h_models.data(), sizeof(DevModel) * c->h_models.size(),
@@ -729,22 +736,42 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
   const uint64_t* d_off = c->d_segoff_local.p;
   uint64_t n_pts = n_local_pts;
   if (c->world > 1 && c->comm) {
-    // all-gather [n_points, n_cand, n_feas, n_surv] per rank
-    CU(c, c->d_cnt_send.reserve(4));
-    CU(c, c->d_cnt_recv.reserve(4 * (size_t)c->world));
-    uint64_t hs[4] = {n_local_pts, n_cand, n_feas, n_surv};
+    // Every model lies on one rank except the <= world - 1 models at range
+    // boundaries, and each rank's frontier is in canonical order, so the global
+    // frontier is the rank-ordered concatenation with only the straddling models'
+    // points re-reduced. Per rank: [n_points, n_cand, n_feas, n_surv, first model + 1,
+    // last model + 1, points of the first model, points of the last model].
+    int mf = -1, ml = -1;
+    for (int m : c->local) {
+      mf = mf < 0 ? m : std::min(mf, m);
+      ml = std::max(ml, m);
+    }
+    uint64_t nfirst = 0, nlast = 0;
+    if (mf >= 0) {
+      uint64_t b[4];
+      const uint64_t at[4] = {c->h_segbase[mf], c->h_segbase[mf + 1], c->h_segbase[ml], c->h_segbase[ml + 1]};
+      for (int i = 0; i < 4; ++i)
+        CU(c, cudaMemcpyAsync(&b[i], c->d_segoff_local.p + at[i], 8, cudaMemcpyDeviceToHost, c->stream));
+      CU(c, cudaStreamSynchronize(c->stream));
+      nfirst = b[1] - b[0];
+      nlast = b[3] - b[2];
+    }
+    constexpr int kCnt = 8;
+    CU(c, c->d_cnt_send.reserve(kCnt));
+    CU(c, c->d_cnt_recv.reserve(kCnt * (size_t)c->world));
+    uint64_t hs[kCnt] = {n_local_pts, n_cand, n_feas, n_surv, (uint64_t)(mf + 1), (uint64_t)(ml + 1), nfirst, nlast};
     CU(c, cudaMemcpyAsync(c->d_cnt_send.p, hs, sizeof hs, cudaMemcpyHostToDevice, c->stream));
-    NC_(c, g_nccl.AllGather(c->d_cnt_send.p, c->d_cnt_recv.p, 4, ncclUint64, c->comm, c->stream));
-    std::vector<uint64_t> cnts(4 * (size_t)c->world);
+    NC_(c, g_nccl.AllGather(c->d_cnt_send.p, c->d_cnt_recv.p, kCnt, ncclUint64, c->comm, c->stream));
+    std::vector<uint64_t> cnts(kCnt * (size_t)c->world);
     CU(c, cudaMemcpyAsync(cnts.data(), c->d_cnt_recv.p, 8 * cnts.size(), cudaMemcpyDeviceToHost, c->stream));
     CU(c, cudaStreamSynchronize(c->stream));
     uint64_t maxc = 1, tot = 0;
     n_cand = n_feas = 0;
     for (int r = 0; r < c->world; ++r) {
-      maxc = std::max(maxc, cnts[4 * r]);
-      tot += cnts[4 * r];
-      n_cand += cnts[4 * r + 1];
-      n_feas += cnts[4 * r + 2];
+      maxc = std::max(maxc, cnts[kCnt * r]);
+      tot += cnts[kCnt * r];
+      n_cand += cnts[kCnt * r + 1];
+      n_feas += cnts[kCnt * r + 2];
     }
     // padded all-gather of local frontiers (32-byte records as bytes)
     if (c->d_local.n < maxc) {
@@ -759,19 +786,85 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
     CU(c, c->d_gather.reserve(maxc * c->world));
     NC_(c, g_nccl.AllGather(c->d_local.p, c->d_gather.p, maxc * sizeof(ppipe_point), ncclUint8, c->comm,
                             c->stream));
-    CU(c, c->d_union.reserve(std::max<uint64_t>(tot, 1)));
-    uint64_t off = 0;
+    // pieces in rank order: (model or -1 for a run of whole models, source, count)
+    struct Piece {
+      long long model;
+      uint64_t src, n;
+    };
+    std::vector<Piece> pieces;
     for (int r = 0; r < c->world; ++r) {
-      if (cnts[4 * r])
-        CU(c, cudaMemcpyAsync(c->d_union.p + off, c->d_gather.p + (size_t)r * maxc,
-                              sizeof(ppipe_point) * cnts[4 * r], cudaMemcpyDeviceToDevice, c->stream));
-      off += cnts[4 * r];
+      const uint64_t* q = &cnts[kCnt * (size_t)r];
+      if (q[4] == 0) continue;  // no rows on rank r
+      const long long f = (long long)q[4] - 1, l = (long long)q[5] - 1;
+      const uint64_t base = (uint64_t)r * maxc, n = q[0];
+      if (f == l) {
+        pieces.push_back({f, base, n});
+      } else {
+        pieces.push_back({f, base, q[6]});
+        pieces.push_back({-1, base + q[6], n - q[6] - q[7]});
+        pieces.push_back({l, base + n - q[7], q[7]});
+      }
     }
+    // a model with pieces from two or more ranks straddles: re-reduce its points
+    std::vector<char> dirty(pieces.size(), 0);
+    std::vector<long long> straddle;
+    for (size_t i = 0; i < pieces.size(); ++i)
+      for (size_t k = i + 1; k < pieces.size() && pieces[k].model == pieces[i].model && pieces[i].model >= 0; ++k) {
+        dirty[i] = dirty[k] = 1;
+        if (straddle.empty() || straddle.back() != pieces[i].model) straddle.push_back(pieces[i].model);
+      }
+    uint64_t n_dirty = 0;
+    for (size_t i = 0; i < pieces.size(); ++i)
+      if (dirty[i]) n_dirty += pieces[i].n;
+    CU(c, c->d_union.reserve(std::max<uint64_t>(n_dirty, 1)));
+    uint64_t off = 0;
+    for (size_t i = 0; i < pieces.size(); ++i)
+      if (dirty[i] && pieces[i].n) {
+        CU(c, cudaMemcpyAsync(c->d_union.p + off, c->d_gather.p + pieces[i].src, sizeof(ppipe_point) * pieces[i].n,
+                              cudaMemcpyDeviceToDevice, c->stream));
+        off += pieces[i].n;
+      }
     CU(c, c->d_final.reserve(std::max<uint64_t>(tot, 1)));
     CU(c, c->d_segoff_final.reserve(c->n_seg_total + 1));
-    CU(c, frontier_pass(c->d_union.p, tot, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_final.p,
-                        c->d_segoff_final.p, &n_pts, &c->scratch, c->stream, &nl));
-    nl += 2;
+    CU(c, c->d_merged.reserve(std::max<uint64_t>(n_dirty, 1)));
+    uint64_t n_merged = 0;
+    std::vector<uint64_t> mcount(straddle.size(), 0);
+    if (n_dirty) {
+      CU(c, frontier_pass(c->d_union.p, n_dirty, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_merged.p,
+                          c->d_segoff_final.p, &n_merged, &c->scratch, c->stream, &nl));
+      std::vector<uint64_t> b(2 * straddle.size());
+      for (size_t i = 0; i < straddle.size(); ++i) {
+        CU(c, cudaMemcpyAsync(&b[2 * i], c->d_segoff_final.p + c->h_segbase[straddle[i]], 8,
+                              cudaMemcpyDeviceToHost, c->stream));
+        CU(c, cudaMemcpyAsync(&b[2 * i + 1], c->d_segoff_final.p + c->h_segbase[straddle[i] + 1], 8,
+                              cudaMemcpyDeviceToHost, c->stream));
+      }
+      CU(c, cudaStreamSynchronize(c->stream));
+      for (size_t i = 0; i < straddle.size(); ++i) mcount[i] = b[2 * i + 1] - b[2 * i];
+    }
+    // assemble in order: clean pieces from the gathered frontiers, each straddling
+    // model's merged block in place of its first piece
+    uint64_t w = 0, moff = 0;
+    size_t si = 0;
+    for (size_t i = 0; i < pieces.size(); ++i) {
+      const ppipe_point* src = c->d_gather.p + pieces[i].src;
+      uint64_t n = pieces[i].n;
+      if (dirty[i]) {
+        if (i > 0 && dirty[i - 1] && pieces[i - 1].model == pieces[i].model) continue;
+        src = c->d_merged.p + moff;
+        n = mcount[si];
+        moff += n;
+        ++si;
+      }
+      if (n)
+        CU(c, cudaMemcpyAsync(c->d_final.p + w, src, sizeof(ppipe_point) * n, cudaMemcpyDeviceToDevice, c->stream));
+      w += n;
+    }
+    n_pts = w;
+    CU(c, c->d_segtmp.reserve(std::max<uint64_t>(n_pts, 1)));
+    CU(c, segment_offsets(c->d_final.p, n_pts, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_segoff_final.p,
+                          c->d_segtmp.p, c->stream, &nl));
+    nl += 2;  // the two all-gathers
     d_pts = c->d_final.p;
     d_off = c->d_segoff_final.p;
   }

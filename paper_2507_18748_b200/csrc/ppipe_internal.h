@@ -75,4 +75,10 @@ cudaError_t frontier_pass(const ppipe_point* in, uint64_t n, const uint64_t* seg
                           uint64_t n_seg, ppipe_point* out, uint64_t* seg_offsets /* [n_seg+1] device */,
                           uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches);
 
+// CSR offsets [n_seg + 1] of n records already in canonical (segment-sorted)
+// order; seg_tmp holds n uint64 scratch entries.
+cudaError_t segment_offsets(const ppipe_point* pts, uint64_t n, const uint64_t* seg_base_by_model, int C,
+                            uint64_t n_seg, uint64_t* seg_offsets, uint64_t* seg_tmp, cudaStream_t s,
+                            int* n_launches);
+
 }  // namespace ppipe

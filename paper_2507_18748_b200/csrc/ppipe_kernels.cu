@@ -1333,4 +1333,31 @@ cudaError_t frontier_pass(const ppipe_point* in, uint64_t n, const uint64_t* seg
   return cudaSuccess;
 }
 
+__global__ void seg_of_kernel(const ppipe_point* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t* seg) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const ppipe_point p = in[i];
+    uint64_t off = 0, pw = 1;
+    for (int k = 1; k < p.K; ++k) {
+      pw *= (uint64_t)C;
+      off += pw;
+    }
+    uint64_t idx = 0;
+    for (int d = 0; d < p.K; ++d) idx = idx * C + p.cls[d];
+    seg[i] = seg_base[p.model] + off + idx;
+  }
+}
+
+cudaError_t segment_offsets(const ppipe_point* pts, uint64_t n, const uint64_t* seg_base_by_model, int C,
+                            uint64_t n_seg, uint64_t* seg_offsets, uint64_t* seg_tmp, cudaStream_t s,
+                            int* n_launches) {
+  if (n > 0) {
+    const int blocks = (int)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+    seg_of_kernel<<<blocks, 256, 0, s>>>(pts, n, seg_base_by_model, C, seg_tmp);
+    ++*n_launches;
+  }
+  seg_start_kernel<<<(unsigned)((n_seg + 1 + 255) / 256), 256, 0, s>>>(seg_tmp, n, n_seg, seg_offsets);
+  ++*n_launches;
+  return cudaGetLastError();
+}
+
 }  // namespace ppipe
