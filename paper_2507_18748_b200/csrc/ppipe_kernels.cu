@@ -22,6 +22,25 @@
 
 #include "ppipe_internal.h"
 
+// Debug builds (-DPPIPE_DEBUG_CHECKS, scripts/variants.py) bounds-check every
+// shared-memory index the kernels derive from data; the product build compiles
+// them away.
+#ifdef PPIPE_DEBUG_CHECKS
+#include <cstdio>
+#define PPIPE_DCHECK(c)                                                                  \
+  do {                                                                                   \
+    if (!(c)) {                                                                          \
+      printf("PPIPE_DCHECK failed at %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+             (int)blockIdx.x, (int)threadIdx.x);                                         \
+      __trap();                                                                          \
+    }                                                                                    \
+  } while (0)
+#else
+#define PPIPE_DCHECK(c) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace ppipe {
 
 #define FULL_MASK 0xffffffffu
@@ -180,6 +199,7 @@ __device__ __noinline__ void emit_warp(const ScoreOut& o, Emitter& em, bool cond
   if (em.count + n > kEmitBuf) emit_flush(o, em);
   if (cond) {
     const int idx = em.count + __popc(mask & lanemask_lt());
+    PPIPE_DCHECK(idx < kEmitBuf);
     em.sbuf[2 * idx] = make_int4((int)r.w[0], (int)r.w[1], (int)r.w[2], (int)r.w[3]);
     em.sbuf[2 * idx + 1] = make_int4((int)r.w[4], (int)r.w[5], (int)r.w[6], (int)r.w[7]);
   }
@@ -266,7 +286,7 @@ struct CtaCtx {
   const int32_t* Pm;   // P[m] base
   const int32_t* Ym;   // Y[m] base
   size_t Mp, B;
-  int bi, b, k2, M, T, sh, q, m1, nb, dbg;
+  int bi, b, k2, M, T, sh, q, m1, nb, dbg, row_len;
   uint32_t model;
   const uint8_t* pair_v;
   __device__ const int32_t* Prow(int k) const { return Pm + ((size_t)k * B + bi) * Mp; }
@@ -558,6 +578,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
     // entries past c2_end hold n' = 0 (never pass) so that the unrolled, prefetching
     // scan below may read up to 16 values ahead
     const int fill_end = ((c2_end + 3) & ~3) + 8 * kScanUnroll - 4;
+    PPIPE_DCHECK(fill_end <= cx.row_len && c2_start >= 0);
     for (int c2 = c2_start + lane; c2 < fill_end; c2 += 32) {
       const long long v = (long long)Bs[min(c2, c2_end - 1)] - L;
       const int sv = (int)max(-16383ll, min(16383ll, v));
@@ -616,6 +637,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
       for (int g = 0; g < kScanUnroll; ++g) cur[g] = nrow[(c2 >> 2) + g];
 #pragma unroll 1
       for (;;) {
+        PPIPE_DCHECK(4 * ((c2 >> 2) + 2 * kScanUnroll) <= cx.row_len);
         uint4 nxt[kScanUnroll];
 #pragma unroll
         for (int g = 0; g < kScanUnroll; ++g) nxt[g] = nrow[(c2 >> 2) + kScanUnroll + g];
@@ -637,6 +659,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
       }
       if (c2 >= c2_end) break;
     }
+    PPIPE_DCHECK(c2 + 4 <= cx.row_len && (c2 & 3) == 0);
     const int4 b4 = *reinterpret_cast<const int4*>(Bs + c2);
     const int rel = c2 - c1_base;  // 1 mod 4; the group is rel .. rel + 3
     int h0, h1, h2, h3;
@@ -681,6 +704,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
             if (v && Bv <= thr[j][k1]) {
               const int E = cx.T - thr[j][k1] + Bv;
               const int Cmax = max(max(c1r[j][k1], C2), R);
+              PPIPE_DCHECK(E >= 0 && (E >> cx.sh) < nb + 2);
               if (!(cx.dbg & 1)) atomicMin(raw + (size_t)k1 * (nb + 2) + (E >> cx.sh), pack_key(E, Cmax, cx.sh, cx.q));
               ++nfeas;
             }
@@ -710,6 +734,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
         while (fm) {
           const int sl = __ffs(fm) - 1;
           fm &= fm - 1;
+          PPIPE_DCHECK(pos < kJ1 * NC * 32);
           sd.list[pos++] = (uint16_t)((lane << 5) | sl);
         }
         __syncwarp();
@@ -726,6 +751,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
             const int C1 = sd.C1s[sl * 32 + src];
             const int C2 = Q - sd.p1s[j * 32 + src];
             const int Cmax = max(max(C1, C2), R);
+            PPIPE_DCHECK(E >= 0 && E <= cx.T && (E >> cx.sh) < nb + 2 && src < 32 && j < kJ1);
             cond = survives(fin + (size_t)k1 * (nb + 2), E >> cx.sh, E, Cmax, cx.sh, cx.q);
             if (cond) rec = make_rec(cx.model, 3, c1_base + 32 * j + src, c2u, k1, cx.k2, k3, cx.b, E, C1, C2, R);
           }
@@ -754,6 +780,7 @@ __device__ __forceinline__ void make_ctx(CtaCtx<NC>& cx, const Problem& pb, cons
   cx.m1 = pb.neg_one;
   cx.nb = nb;
   cx.dbg = pb.debug_flags;
+  cx.row_len = 0;
   cx.pair_v = pb.pair_v;
   cx.P2 = cx.Prow(k2);
   int sh = 0;
@@ -813,6 +840,7 @@ __device__ __forceinline__ void stage_rows(const CtaCtx<NC>& cx, const ScoreSmem
   const int32_t* P3 = cx.Prow(k3);
   const int32_t P3M = P3[M];
   const int32_t* Y23 = cx.Yrow(cx.k2, k3);
+  PPIPE_DCHECK(c2_to <= cx.row_len);
   for (int c2 = c2_from + (int)threadIdx.x; c2 < c2_to; c2 += 32 * kWarps) {
     const bool in = c2 < M;
     const int p2 = in ? __ldg(cx.P2 + c2) : 0;
@@ -974,6 +1002,7 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
   const DevModel md = pb.models[ml];
   CtaCtx<NC> cx;
   make_ctx(cx, pb, md, k2, bi, nb);
+  cx.row_len = row_len;
   Emitter em{sm.ebuf + warp * 2 * kEmitBuf, 0};  // unused in pass 1
   unsigned long long feas = 0, cand = 0;
   const K3Range r = k3_range(md);
@@ -1039,6 +1068,7 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
     const DevModel md = pb.models[ml];
     CtaCtx<NC> cx;
     make_ctx(cx, pb, md, k2, bi, nb);
+    cx.row_len = row_len;
     const K3Range r = k3_range(md);
     const uint2* src = reinterpret_cast<const uint2*>(out.hot_tab) + u * (unsigned long long)ntab;
     for (int i = tid; i < ntab; i += 32 * kWarps) sm.fin[i] = src[i];
