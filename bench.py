@@ -166,6 +166,7 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the SLO-sweep (frontier_at) measurement")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--models", type=int, default=None, help="config 5 only: first N models (profiling)")
     ap.add_argument("--margin", type=int, default=None, help="override margin_permille (experiments)")
@@ -299,7 +300,9 @@ def main():
     prof = os.path.join(ROOT, "profiles", "score_kernel_dram.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            pj = json.load(open(prof))
+            if int(pj.get("config", 5)) == args.config and not args.models:
+                traffic = pj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     launches_tot = int(allsum(launches))
@@ -334,6 +337,22 @@ def main():
                "path": "ppipe_update_profiles (pinned host lat/S -> HBM, overlapped with host validation) + "
                        "ppipe_enumerate + ppipe_pareto(copy_to_host) into a page-locked buffer read zero-copy"}
 
+    # ---- SLO sweep from the last enumeration: frontier_at
+    # truncates every segment to a lower latency target without re-enumerating ----
+    sweep = None
+    if not args.no_sweep:
+        scales = [0.9, 0.8, 0.7, 0.6, 0.5, 0.4, 0.3, 0.2, 0.1]
+        barrier()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        pts = [pp.frontier_at(ctx, (w.slo_us * sc).astype(np.uint32), w.margin_permille, copy_to_host=False).n_points
+               for sc in scales]
+        s1.record(stream)
+        s1.synchronize()
+        sweep = {"slo_scales": scales, "ms_per_target": s0.elapsed_time(s1) / len(scales),
+                 "frontier_points": pts, "base": "the timed enumeration's frontier (SLO scale 1.0)",
+                 "vs": "re-enumerating costs ms_per_step per target"}
     pp.free(ctx)
     if rank != 0:
         if world > 1:
@@ -369,6 +388,7 @@ def main():
         "gpu_launches": launches_tot,
         "clocks": clocks,
         "phase_ms": phase_avg,
+        "slo_sweep": sweep,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

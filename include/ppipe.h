@@ -154,6 +154,26 @@ typedef struct {
  * done. Errors: PPIPE_ESTATE (no prior ppipe_enumerate), PPIPE_ECUDA, PPIPE_ENCCL. */
 int ppipe_pareto(ppipe_ctx *ctx, int copy_to_host, ppipe_frontier *out);
 
+/* SLO sweep from one enumeration (Fig. 12a).
+ * The frontier at a lower latency target is a prefix of every segment of the
+ * frontier at a higher one (invariant I3: a point's dominators all have smaller or
+ * equal E, so they stay feasible), so this derives the frontier for new per-model
+ * SLOs slo_us[n_models] and margin_permille from the last ppipe_pareto result
+ * without re-enumerating: per segment, the points with E <= T'_m =
+ * floor(slo'_m * (1000 - margin') / 1000). Requires T'_m <= T_m of the last
+ * ppipe_enumerate for every model (else PPIPE_EINVAL: raise the base SLO and
+ * re-enumerate instead). The last ppipe_pareto result stays valid and can be swept
+ * again. out: n_points, n_segments, points / seg_offsets (host, if copy_to_host;
+ * the page-locked buffer is shared with ppipe_pareto's, so its previous host copy
+ * is overwritten), d_points / d_seg_offsets (device, valid until the next
+ * ppipe_frontier_at / ppipe_enumerate / ppipe_free); n_candidates is that of the
+ * base enumeration; n_feasible, n_survivors and the _local counts are 0 (not
+ * recomputed). Device work only (no collective), also under world > 1 where the
+ * base result is replicated. Errors: PPIPE_ESTATE (no prior ppipe_pareto),
+ * PPIPE_EINVAL, PPIPE_ECUDA. */
+int ppipe_frontier_at(ppipe_ctx *ctx, const uint32_t *slo_us, uint32_t margin_permille, int copy_to_host,
+                      ppipe_frontier *out);
+
 /* Free everything the context owns. NULL-safe. */
 void ppipe_free(ppipe_ctx *ctx);
 

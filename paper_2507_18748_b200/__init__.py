@@ -11,6 +11,7 @@ from ._binding import (  # noqa: F401
     PPipeError,
     enumerate,
     free,
+    frontier_at,
     load_profiles,
     load_workload,
     nccl_unique_id,

@@ -76,6 +76,9 @@ def lib():
         L.ppipe_enumerate.argtypes = [ct.c_void_p, ct.POINTER(_EnumParams)]
         L.ppipe_pareto.restype = ct.c_int
         L.ppipe_pareto.argtypes = [ct.c_void_p, ct.c_int, ct.POINTER(_Frontier)]
+        L.ppipe_frontier_at.restype = ct.c_int
+        L.ppipe_frontier_at.argtypes = [ct.c_void_p, ct.POINTER(ct.c_uint32), ct.c_uint32, ct.c_int,
+                                        ct.POINTER(_Frontier)]
         L.ppipe_free.restype = None
         L.ppipe_free.argtypes = [ct.c_void_p]
         L.ppipe_last_error.restype = ct.c_char_p
@@ -200,12 +203,7 @@ class Frontier:
     n_feasible_local: int = 0
 
 
-def pareto(ctx: Context, copy_to_host: bool = True, zero_copy: bool = False) -> Frontier:
-    """Run the frontier pass. copy_to_host: also return host arrays. zero_copy: those
-    arrays are views of the context's page-locked result buffer (no host memcpy),
-    valid only until the next pareto() / free() on this context."""
-    f = _Frontier()
-    _check(lib().ppipe_pareto(ctx.handle, 1 if copy_to_host else 0, ct.byref(f)), ctx.handle)
+def _frontier_from(f, copy_to_host: bool, zero_copy: bool) -> Frontier:
     pts = seg = None
     if copy_to_host:
         n = int(f.n_points)
@@ -222,6 +220,28 @@ def pareto(ctx: Context, copy_to_host: bool = True, zero_copy: bool = False) -> 
     return Frontier(int(f.n_candidates), int(f.n_feasible), int(f.n_points), int(f.n_segments),
                     int(f.n_survivors), pts, seg, int(f.d_points or 0), int(f.d_seg_offsets or 0),
                     int(f.n_candidates_local), int(f.n_feasible_local))
+
+
+def pareto(ctx: Context, copy_to_host: bool = True, zero_copy: bool = False) -> Frontier:
+    """Run the frontier pass. copy_to_host: also return host arrays. zero_copy: those
+    arrays are views of the context's page-locked result buffer (no host memcpy),
+    valid only until the next pareto() / frontier_at() / free() on this context."""
+    f = _Frontier()
+    _check(lib().ppipe_pareto(ctx.handle, 1 if copy_to_host else 0, ct.byref(f)), ctx.handle)
+    return _frontier_from(f, copy_to_host, zero_copy)
+
+
+def frontier_at(ctx: Context, slo_us: np.ndarray, margin_permille: int, copy_to_host: bool = True,
+                zero_copy: bool = False) -> Frontier:
+    """The frontier at lower per-model SLOs, truncated from the last pareto() result
+    (include/ppipe.h ppipe_frontier_at; no re-enumeration)."""
+    slo = np.ascontiguousarray(slo_us, dtype=np.uint32)
+    if slo.shape[0] != ctx.n_models:
+        raise ValueError(f"slo_us has {slo.shape[0]} entries, context has {ctx.n_models} models")
+    f = _Frontier()
+    _check(lib().ppipe_frontier_at(ctx.handle, _u32p(slo), int(margin_permille), 1 if copy_to_host else 0,
+                                   ct.byref(f)), ctx.handle)
+    return _frontier_from(f, copy_to_host, zero_copy)
 
 
 def free(ctx: Context) -> None:

@@ -209,6 +209,14 @@ struct ppipe_ctx {
   unsigned long long* h_counters = nullptr;  // pinned [5]
   // enumerate state
   bool enumerated = false;
+  // last ppipe_pareto result (base of ppipe_frontier_at)
+  bool have_result = false;
+  const ppipe_point* res_pts = nullptr;
+  const uint64_t* res_off = nullptr;
+  uint64_t res_n = 0, res_ncand = 0;
+  DevBuf<ppipe_point> d_trunc;
+  DevBuf<uint64_t> d_trunc_off;
+  DevBuf<uint32_t> d_Tnew;
   ppipe_enum_params last_params{};
   std::vector<uint32_t> last_slo;
   uint64_t n_seg_total = 0;
@@ -275,6 +283,9 @@ void free_ctx(ppipe_ctx* c) {
   c->d_cnt_recv.release();
   c->d_segtmp.release();
   c->d_merged.release();
+  c->d_trunc.release();
+  c->d_trunc_off.release();
+  c->d_Tnew.release();
   c->h_points.release();
   c->h_segoff.release();
   if (c->scratch.buf) cudaFree(c->scratch.buf);
@@ -585,6 +596,7 @@ PPIPE_API int ppipe_update_profiles(ppipe_ctx* c, uint32_t n_models, const ppipe
   // the context without usable profiles until the next successful update.
   c->profiles_ok = false;
   c->enumerated = false;
+  c->have_result = false;
   cudaError_t copy_err = cudaSuccess;
   std::thread copier([&] {
     copy_err = cudaSetDevice(c->device);
@@ -690,6 +702,7 @@ PPIPE_API int ppipe_enumerate(ppipe_ctx* ctx, const ppipe_enum_params* p) {
       return fail(ctx, PPIPE_ERANGE, "model %u: T_eff %llu us >= 2^28 (int32 envelope)", m,
                   (unsigned long long)T);
   }
+  ctx->have_result = false;
   ctx->last_params = *p;
   ctx->last_slo.assign(p->slo_us, p->slo_us + ctx->n_models);
   ctx->last_params.slo_us = ctx->last_slo.data();
@@ -885,12 +898,63 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
   out->n_survivors = n_surv;
   out->n_candidates_local = c->h_counters[2];
   out->n_feasible_local = c->h_counters[1];
+  c->have_result = true;
+  c->res_pts = d_pts;
+  c->res_off = d_off;
+  c->res_n = n_pts;
+  c->res_ncand = n_cand;
   if (copy_to_host) {
     CU(c, c->h_points.reserve(n_pts));
     CU(c, c->h_segoff.reserve(c->n_seg_total + 1));
     if (n_pts)
       CU(c, cudaMemcpyAsync(c->h_points.p, d_pts, sizeof(ppipe_point) * n_pts, cudaMemcpyDeviceToHost, c->stream));
     CU(c, cudaMemcpyAsync(c->h_segoff.p, d_off, 8 * (c->n_seg_total + 1), cudaMemcpyDeviceToHost, c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
+    out->points = c->h_points.p;
+    out->seg_offsets = c->h_segoff.p;
+  }
+  return PPIPE_OK;
+}
+
+PPIPE_API int ppipe_frontier_at(ppipe_ctx* c, const uint32_t* slo_us, uint32_t margin_permille, int copy_to_host,
+                                ppipe_frontier* out) {
+  if (!c) return fail(nullptr, PPIPE_EINVAL, "ppipe_frontier_at: NULL ctx");
+  if (!out || !slo_us) return fail(c, PPIPE_EINVAL, "ppipe_frontier_at: NULL slo_us or output");
+  if (!c->have_result) return fail(c, PPIPE_ESTATE, "ppipe_frontier_at called before ppipe_pareto");
+  if (margin_permille >= 1000) return fail(c, PPIPE_EINVAL, "margin_permille %u: must be < 1000", margin_permille);
+  std::vector<uint32_t> Tn(c->n_models);
+  for (uint32_t m = 0; m < c->n_models; ++m) {
+    const uint64_t T0 = (uint64_t)c->last_slo[m] * (1000 - c->last_params.margin_permille) / 1000;
+    const uint64_t T1 = (uint64_t)slo_us[m] * (1000 - margin_permille) / 1000;
+    if (T1 > T0)
+      return fail(c, PPIPE_EINVAL,
+                  "model %u: T_eff %llu us exceeds the enumerated %llu us (a sweep can only lower the target)", m,
+                  (unsigned long long)T1, (unsigned long long)T0);
+    Tn[m] = (uint32_t)T1;
+  }
+  CU(c, cudaSetDevice(c->device));
+  CU(c, c->d_Tnew.reserve(std::max<size_t>(c->n_models, 1)));
+  CU(c, c->d_trunc.reserve(std::max<uint64_t>(c->res_n, 1)));
+  CU(c, c->d_trunc_off.reserve(c->n_seg_total + 1));
+  CU(c, cudaMemcpyAsync(c->d_Tnew.p, Tn.data(), 4 * Tn.size(), cudaMemcpyHostToDevice, c->stream));
+  uint64_t n_pts = 0;
+  int nl = 0;
+  CU(c, truncate_frontier(c->res_pts, c->res_off, c->res_n, c->n_seg_total, c->d_Tnew.p, c->d_trunc.p,
+                          c->d_trunc_off.p, &n_pts, &c->scratch, c->stream, &nl));
+  std::memset(out, 0, sizeof *out);
+  out->n_candidates = c->res_ncand;
+  out->n_points = n_pts;
+  out->n_segments = c->n_seg_total;
+  out->d_points = c->d_trunc.p;
+  out->d_seg_offsets = c->d_trunc_off.p;
+  if (copy_to_host) {
+    CU(c, c->h_points.reserve(n_pts));
+    CU(c, c->h_segoff.reserve(c->n_seg_total + 1));
+    if (n_pts)
+      CU(c, cudaMemcpyAsync(c->h_points.p, c->d_trunc.p, sizeof(ppipe_point) * n_pts, cudaMemcpyDeviceToHost,
+                            c->stream));
+    CU(c, cudaMemcpyAsync(c->h_segoff.p, c->d_trunc_off.p, 8 * (c->n_seg_total + 1), cudaMemcpyDeviceToHost,
+                          c->stream));
     CU(c, cudaStreamSynchronize(c->stream));
     out->points = c->h_points.p;
     out->seg_offsets = c->h_segoff.p;

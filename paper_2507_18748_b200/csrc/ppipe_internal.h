@@ -81,4 +81,11 @@ cudaError_t segment_offsets(const ppipe_point* pts, uint64_t n, const uint64_t* 
                             uint64_t n_seg, uint64_t* seg_offsets, uint64_t* seg_tmp, cudaStream_t s,
                             int* n_launches);
 
+// SLO truncation of a canonical frontier: per segment keep the points with
+// E <= T_new[model] (a prefix of the segment). Writes out / seg_offsets_out and the
+// kept count (host). scratch is grown as needed.
+cudaError_t truncate_frontier(const ppipe_point* in, const uint64_t* seg_offsets_in, uint64_t n_in, uint64_t n_seg,
+                              const uint32_t* T_new, ppipe_point* out, uint64_t* seg_offsets_out,
+                              uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches);
+
 }  // namespace ppipe

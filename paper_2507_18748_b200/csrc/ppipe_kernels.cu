@@ -1390,4 +1390,80 @@ cudaError_t segment_offsets(const ppipe_point* pts, uint64_t n, const uint64_t* 
   return cudaGetLastError();
 }
 
+// Per segment: how many of its (E-ascending) points satisfy E <= T_new[model].
+__global__ void trunc_count_kernel(const ppipe_point* in, const uint64_t* off, uint64_t n_seg, const uint32_t* T_new,
+                                   uint64_t* cnt) {
+  const uint64_t sg = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (sg > n_seg) return;
+  if (sg == n_seg) {
+    cnt[sg] = 0;
+    return;
+  }
+  uint64_t lo = off[sg], hi = off[sg + 1];
+  if (lo == hi) {
+    cnt[sg] = 0;
+    return;
+  }
+  const uint32_t T = T_new[in[lo].model];
+  const uint64_t base = lo;
+  while (lo < hi) {  // first point with E > T
+    const uint64_t mid = (lo + hi) >> 1;
+    if (in[mid].e2e_us <= T) lo = mid + 1;
+    else hi = mid;
+  }
+  cnt[sg] = lo - base;
+}
+
+struct KeepBelowT {
+  const uint32_t* T_new;
+  __device__ bool operator()(const ppipe_point& p) const { return p.e2e_us <= T_new[p.model]; }
+};
+
+cudaError_t truncate_frontier(const ppipe_point* in, const uint64_t* seg_offsets_in, uint64_t n_in, uint64_t n_seg,
+                              const uint32_t* T_new, ppipe_point* out, uint64_t* seg_offsets_out,
+                              uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches) {
+  const int64_t ns = (int64_t)n_seg + 1, ni = (int64_t)n_in;
+  size_t b_scan = 0, b_sel = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, b_scan, (uint64_t*)nullptr, (uint64_t*)nullptr, ns, s);
+  if (e != cudaSuccess) return e;
+  e = cub::DeviceSelect::If(nullptr, b_sel, (const ppipe_point*)nullptr, (ppipe_point*)nullptr, (int64_t*)nullptr,
+                            ni, KeepBelowT{T_new}, s);
+  if (e != cudaSuccess) return e;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  const size_t o_cnt = take(8 * (size_t)ns), o_num = take(16), o_tmp = take(std::max(b_scan, b_sel));
+  if (scratch->bytes < off) {
+    if (scratch->buf) cudaFree(scratch->buf);
+    scratch->buf = nullptr;
+    scratch->bytes = 0;
+    e = cudaMalloc(&scratch->buf, off);
+    if (e != cudaSuccess) return e;
+    scratch->bytes = off;
+  }
+  char* base = (char*)scratch->buf;
+  uint64_t* cnt = (uint64_t*)(base + o_cnt);
+  int64_t* d_num = (int64_t*)(base + o_num);
+  void* tmp = base + o_tmp;
+  trunc_count_kernel<<<(unsigned)((ns + 255) / 256), 256, 0, s>>>(in, seg_offsets_in, n_seg, T_new, cnt);
+  e = cub::DeviceScan::ExclusiveSum(tmp, b_scan, cnt, seg_offsets_out, ns, s);
+  if (e != cudaSuccess) return e;
+  int64_t nk = 0;
+  if (n_in > 0) {
+    e = cub::DeviceSelect::If(tmp, b_sel, in, out, d_num, ni, KeepBelowT{T_new}, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyAsync(&nk, d_num, 8, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return e;
+    ++*n_launches;
+  }
+  *n_launches += 2;
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  *n_out_host = (uint64_t)nk;
+  return cudaGetLastError();
+}
+
 }  // namespace ppipe

@@ -98,7 +98,7 @@ for rep in reps:
 with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.md"), "w") as f:
     f.write("\n".join(lines) + "\n")
 if dram:
-    json.dump({"dram_bytes_per_launch": sum(dram.values()),
+    json.dump({"dram_bytes_per_launch": sum(dram.values()), "config": 5,
                "note": "score phase of one config-5 step = score3a + score3b + score12 launches; "
                        "dram__bytes_read.sum + dram__bytes_write.sum from ncu --set full",
                "per_kernel": dram, "source": [os.path.basename(r) for r in reps]},
