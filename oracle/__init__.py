@@ -10,4 +10,5 @@ from .oracle import (  # noqa: F401
     build_oracle,
     run_oracle,
     oracle_lib_path,
+    prepartition_oracle,
 )

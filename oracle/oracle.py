@@ -62,6 +62,11 @@ def _load():
                                    ct.POINTER(ct.POINTER(_Result))]
         lib.oracle_result_free.argtypes = [ct.POINTER(_Result)]
         lib.oracle_set_threads.argtypes = [ct.c_int]
+        lib.oracle_prepartition.restype = ct.c_int
+        lib.oracle_prepartition.argtypes = [ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.POINTER(ct.c_uint32),
+                                            ct.POINTER(ct.c_uint64), ct.c_uint32, ct.c_uint32, ct.c_uint32,
+                                            ct.POINTER(ct.c_uint32), ct.POINTER(ct.c_uint64),
+                                            ct.POINTER(ct.c_uint64)]
         _lib = lib
     return _lib
 
@@ -123,3 +128,24 @@ def run_oracle(w, model_lo: int = 0, model_hi: Optional[int] = None, only_K: int
     lib.oracle_result_free(out)
     del keep
     return res
+
+
+def prepartition_oracle(lat_us: np.ndarray, act_bytes: np.ndarray, n_blocks: int, ref_class: int, ref_batch: int):
+    """Greedy equal-runtime pre-partitioning (oracle_prepartition in ppipe_oracle.c).
+    Returns (bounds[N+1] uint32, block_lat[C][N][B] uint64, block_S[N] uint64)."""
+    lib = _load()
+    lat = np.ascontiguousarray(lat_us, dtype=np.uint32)
+    S = np.ascontiguousarray(act_bytes, dtype=np.uint64)
+    C, M, B = lat.shape
+    if S.shape != (M,):
+        raise ValueError("act_bytes must have one entry per layer")
+    N = int(n_blocks)
+    bounds = np.zeros(max(N, 0) + 1, dtype=np.uint32)
+    blat = np.zeros((C, max(N, 1), B), dtype=np.uint64)
+    bS = np.zeros(max(N, 1), dtype=np.uint64)
+    rc = lib.oracle_prepartition(M, C, B, _u32p(lat), S.ctypes.data_as(ct.POINTER(ct.c_uint64)), N, int(ref_class),
+                                 int(ref_batch), _u32p(bounds), blat.ctypes.data_as(ct.POINTER(ct.c_uint64)),
+                                 bS.ctypes.data_as(ct.POINTER(ct.c_uint64)))
+    if rc != 0:
+        raise ValueError(f"oracle_prepartition rejected its input (N={N}, M={M})")
+    return bounds, blat, bS

@@ -38,7 +38,10 @@
  *
  * Parity: every function here is pinned by tests/test_oracle_pins.py (hand-worked
  * fixtures P0a/P0b, printed numbers P1-P4, closed forms P5/P6/P9, the textbook
- * min-max partition P7, and the literal O(n^2) Pareto definition P8).
+ * min-max partition P7, and the literal O(n^2) Pareto definition P8);
+ * oracle_prepartition (end of file) by tests/test_prepartition_pins.py (the
+ * SPEC.md examples, closed forms for N = 1, N = M and uniform layers, and the
+ * half-layer balance bound that the greedy stopping rule implies).
  */
 #define _GNU_SOURCE
 #include <pthread.h>
@@ -421,5 +424,62 @@ int oracle_run(uint32_t n_models, const oracle_model *models, uint32_t n_classes
     pthread_mutex_destroy(&pb.mu);
   }
   *out = res;
+  return 0;
+}
+
+/*
+ * Greedy equal-runtime pre-partitioning (§5.2).
+ *
+ *   "we start from the first layer and sequentially group consecutive layers
+ *    together until their combined runtime is as close as possible to 1/N of the
+ *    runtime of the entire DNN; this process is repeated until we reach the last
+ *    layer."
+ *
+ * Runtime t_l = lat[ref_class][l][ref_b] (a selected GPU type at one batch). A block
+ * starts at the first unassigned layer with that layer, then takes the next layer
+ * while doing so brings its runtime at least as close to total/N (ties include the
+ * layer), and stops early enough to leave one layer for every
+ * remaining block; block N takes the rest. "As close as possible" is
+ * compared exactly in integers: |N*(acc + t) - total| <= |N*acc - total|.
+ * Block latency per (class, batch) = sum over member layers; block output bytes =
+ * the last member layer's. lat is [C][M][B]; outputs bounds[N+1],
+ * block_lat[C][N][B] (uint64, so sums cannot wrap), block_S[N].
+ * Returns 0, or -1 if N < 1, N > M or the reference indices are out of range.
+ */
+int oracle_prepartition(uint32_t M, uint32_t C, uint32_t B, const uint32_t *lat, const uint64_t *S, uint32_t N,
+                        uint32_t ref_class, uint32_t ref_b, uint32_t *bounds, uint64_t *block_lat, uint64_t *block_S) {
+  if (N < 1 || N > M || ref_class >= C || ref_b >= B) return -1;
+  int64_t total = 0;
+  for (uint32_t l = 0; l < M; ++l) total += lat[((size_t)ref_class * M + l) * B + ref_b];
+  uint32_t i = 0;
+  bounds[0] = 0;
+  for (uint32_t blk = 0; blk + 1 < N; ++blk) {
+    const uint32_t remaining = N - blk - 1; /* blocks still to come after this one */
+    int64_t acc = lat[((size_t)ref_class * M + i) * B + ref_b];
+    uint32_t j = i + 1;
+    while (j < M - remaining) {
+      const int64_t t = lat[((size_t)ref_class * M + j) * B + ref_b];
+      int64_t with = (int64_t)N * (acc + t) - total, without = (int64_t)N * acc - total;
+      if (with < 0) with = -with;
+      if (without < 0) without = -without;
+      if (with <= without) {
+        acc += t;
+        ++j;
+      } else {
+        break;
+      }
+    }
+    bounds[blk + 1] = j;
+    i = j;
+  }
+  bounds[N] = M;
+  for (uint32_t k = 0; k < C; ++k)
+    for (uint32_t q = 0; q < N; ++q)
+      for (uint32_t b = 0; b < B; ++b) {
+        uint64_t sum = 0;
+        for (uint32_t l = bounds[q]; l < bounds[q + 1]; ++l) sum += lat[((size_t)k * M + l) * B + b];
+        block_lat[((size_t)k * N + q) * B + b] = sum;
+      }
+  for (uint32_t q = 0; q < N; ++q) block_S[q] = S[bounds[q + 1] - 1];
   return 0;
 }
