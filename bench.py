@@ -354,6 +354,17 @@ def main():
                  "frontier_points": pts, "base": "the timed enumeration's frontier (SLO scale 1.0)",
                  "vs": "re-enumerating costs ms_per_step per target"}
     pp.free(ctx)
+    # ---- greedy pre-partitioning (§5.2) of this workload's
+    # layer-level models into 10 blocks, through the C ABI from pinned host buffers ----
+    prepart = None
+    if rank == 0 and not args.no_sweep:
+        pp.prepartition(lat_h[:1], S_h[:1], 1)  # warm
+        t0 = time.perf_counter()
+        nblk = min(10, min(m.n_layers for m in w.models))
+        bnd, _, _ = pp.prepartition(lat_h, S_h, nblk, 1 if w.n_classes > 1 else 0, 0)
+        prepart = {"models": len(lat_h), "n_blocks": nblk, "ms": (time.perf_counter() - t0) * 1e3,
+                   "ref": "class 1, batch index 0", "timing": "host wall clock around ppipe_prepartition "
+                   "(H2D of the layer profiles, two kernels, D2H of bounds and block profiles)"}
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -389,6 +400,7 @@ def main():
         "clocks": clocks,
         "phase_ms": phase_avg,
         "slo_sweep": sweep,
+        "prepartition": prepart,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -174,6 +174,24 @@ int ppipe_pareto(ppipe_ctx *ctx, int copy_to_host, ppipe_frontier *out);
 int ppipe_frontier_at(ppipe_ctx *ctx, const uint32_t *slo_us, uint32_t margin_permille, int copy_to_host,
                       ppipe_frontier *out);
 
+/* Greedy equal-runtime pre-partitioning into n_blocks blocks (PAPER.md:1005-1010,
+ * §5.2): per model, starting at layer 0, a block takes
+ * consecutive layers while that brings its runtime t_l = lat[ref_class][l][ref_batch]
+ * at least as close to total/N (ties take the layer; compared exactly as
+ * |N*acc - total|), leaving one layer for every remaining block; the last block takes
+ * the rest. Standalone device call (no context): models as for ppipe_load_profiles
+ * (validated the same way), n_blocks in 1..min(n_layers), ref_class < n_classes,
+ * ref_batch < n_batches (an index into the batch list). Host outputs, caller-owned:
+ *   bounds      [n_models][n_blocks + 1]  block q = layers [bounds[q], bounds[q+1])
+ *   block_lat   [n_models][n_classes][n_blocks][n_batches]  sums of member layers
+ *   block_bytes [n_models][n_blocks]  act_bytes of each block's last layer
+ * The outputs are block-level profiles ready for ppipe_load_profiles. device: CUDA
+ * ordinal, -1 = current. Blocks until done. Errors: PPIPE_EINVAL, PPIPE_ERANGE,
+ * PPIPE_ECUDA (message via ppipe_last_error(NULL)). */
+int ppipe_prepartition(uint32_t n_models, const ppipe_model *models, uint32_t n_classes, uint32_t n_batches,
+                       uint32_t n_blocks, uint32_t ref_class, uint32_t ref_batch, int32_t device, uint32_t *bounds,
+                       uint32_t *block_lat, uint64_t *block_bytes);
+
 /* Free everything the context owns. NULL-safe. */
 void ppipe_free(ppipe_ctx *ctx);
 

@@ -17,6 +17,7 @@ from ._binding import (  # noqa: F401
     nccl_unique_id,
     pareto,
     partition_rows,
+    prepartition,
     run,
     update_profiles,
     lib,

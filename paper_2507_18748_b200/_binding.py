@@ -76,6 +76,10 @@ def lib():
         L.ppipe_enumerate.argtypes = [ct.c_void_p, ct.POINTER(_EnumParams)]
         L.ppipe_pareto.restype = ct.c_int
         L.ppipe_pareto.argtypes = [ct.c_void_p, ct.c_int, ct.POINTER(_Frontier)]
+        L.ppipe_prepartition.restype = ct.c_int
+        L.ppipe_prepartition.argtypes = [ct.c_uint32, ct.POINTER(_Model), ct.c_uint32, ct.c_uint32, ct.c_uint32,
+                                         ct.c_uint32, ct.c_uint32, ct.c_int32, ct.POINTER(ct.c_uint32),
+                                         ct.POINTER(ct.c_uint32), ct.POINTER(ct.c_uint64)]
         L.ppipe_frontier_at.restype = ct.c_int
         L.ppipe_frontier_at.argtypes = [ct.c_void_p, ct.POINTER(ct.c_uint32), ct.c_uint32, ct.c_int,
                                         ct.POINTER(_Frontier)]
@@ -242,6 +246,27 @@ def frontier_at(ctx: Context, slo_us: np.ndarray, margin_permille: int, copy_to_
     _check(lib().ppipe_frontier_at(ctx.handle, _u32p(slo), int(margin_permille), 1 if copy_to_host else 0,
                                    ct.byref(f)), ctx.handle)
     return _frontier_from(f, copy_to_host, zero_copy)
+
+
+def prepartition(lat_us: Sequence[np.ndarray], act_bytes: Sequence[np.ndarray], n_blocks: int, ref_class: int = 0,
+                 ref_batch: int = 0, device: int = -1):
+    """Greedy equal-runtime pre-partitioning on the GPU (include/ppipe.h ppipe_prepartition).
+    Returns (bounds [n_models][n_blocks+1] uint32, block latencies: list of uint32
+    [C][n_blocks][B] arrays, block bytes [n_models][n_blocks] uint64)."""
+    n = len(lat_us)
+    if n == 0:
+        return np.zeros((0, n_blocks + 1), np.uint32), [], np.zeros((0, n_blocks), np.uint64)
+    C, _, B = np.asarray(lat_us[0]).shape
+    models, keep = _models_array(lat_us, act_bytes, C, B)
+    N = int(n_blocks)
+    bounds = np.zeros((n, N + 1), dtype=np.uint32)
+    blat = np.zeros((n, C, N, B), dtype=np.uint32)
+    bS = np.zeros((n, N), dtype=np.uint64)
+    rc = lib().ppipe_prepartition(n, models, C, B, N, int(ref_class), int(ref_batch), int(device), _u32p(bounds),
+                                  _u32p(blat), bS.ctypes.data_as(ct.POINTER(ct.c_uint64)))
+    _check(rc, None)
+    del keep
+    return bounds, [blat[m] for m in range(n)], bS
 
 
 def free(ctx: Context) -> None:

@@ -388,6 +388,88 @@ PPIPE_API int ppipe_nccl_unique_id(void* out128) {
   return PPIPE_OK;
 }
 
+PPIPE_API int ppipe_prepartition(uint32_t n_models, const ppipe_model* models, uint32_t n_classes, uint32_t n_batches,
+                                 uint32_t n_blocks, uint32_t ref_class, uint32_t ref_batch, int32_t device,
+                                 uint32_t* bounds, uint32_t* block_lat, uint64_t* block_bytes) {
+  if (n_models == 0) return PPIPE_OK;
+  if (!models || !bounds || !block_lat || !block_bytes)
+    return fail(nullptr, PPIPE_EINVAL, "ppipe_prepartition: NULL argument");
+  if (n_classes < 1 || n_classes > 8 || n_batches < 1)
+    return fail(nullptr, PPIPE_EINVAL, "ppipe_prepartition: n_classes %u / n_batches %u invalid", n_classes,
+                n_batches);
+  if (ref_class >= n_classes || ref_batch >= n_batches)
+    return fail(nullptr, PPIPE_EINVAL, "ppipe_prepartition: reference class %u / batch index %u out of range",
+                ref_class, ref_batch);
+  {
+    std::vector<uint32_t> ones(n_batches, 1);  // block bytes are layer bytes: check S alone
+    std::string verr;
+    const int vrc = validate_models(n_models, models, n_classes, n_batches, ones.data(), &verr);
+    if (vrc != PPIPE_OK) return fail(nullptr, vrc, "%s", verr.c_str());
+  }
+  for (uint32_t m = 0; m < n_models; ++m)
+    if (n_blocks < 1 || n_blocks > models[m].n_layers)
+      return fail(nullptr, PPIPE_EINVAL, "model %u: n_blocks %u must be 1..%u (its layer count)", m, n_blocks,
+                  models[m].n_layers);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(nullptr, PPIPE_ECUDA, "no CUDA device: this library has no CPU fallback");
+  if (device >= 0 && cudaSetDevice(device) != cudaSuccess)
+    return fail(nullptr, PPIPE_ECUDA, "cudaSetDevice(%d) failed", device);
+  const uint64_t C = n_classes, B = n_batches, N = n_blocks;
+  std::vector<uint64_t> lat_off(n_models), s_off(n_models);
+  std::vector<uint32_t> Ms(n_models);
+  uint64_t nl = 0, ns = 0;
+  for (uint32_t m = 0; m < n_models; ++m) {
+    lat_off[m] = nl;
+    s_off[m] = ns;
+    Ms[m] = models[m].n_layers;
+    nl += C * Ms[m] * B;
+    ns += Ms[m];
+  }
+  struct Local {
+    DevBuf<uint32_t> lat, M, bounds, blat;
+    DevBuf<uint64_t> S, lo, so, bS;
+    DevBuf<int64_t> prefix;
+    cudaStream_t s = nullptr;
+    ~Local() {
+      lat.release(); M.release(); bounds.release(); blat.release();
+      S.release(); lo.release(); so.release(); bS.release(); prefix.release();
+      if (s) cudaStreamDestroy(s);
+    }
+  } d;
+#define CUP(x)                                                                                   \
+  do {                                                                                           \
+    const cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) return fail(nullptr, PPIPE_ECUDA, "%s: %s", #x, cudaGetErrorString(e_)); \
+  } while (0)
+  CUP(cudaStreamCreateWithFlags(&d.s, cudaStreamNonBlocking));
+  CUP(d.lat.reserve(nl));
+  CUP(d.S.reserve(ns));
+  CUP(d.lo.reserve(n_models));
+  CUP(d.so.reserve(n_models));
+  CUP(d.M.reserve(n_models));
+  CUP(d.prefix.reserve(ns + n_models));
+  CUP(d.bounds.reserve((size_t)n_models * (N + 1)));
+  CUP(d.blat.reserve((size_t)n_models * C * N * B));
+  CUP(d.bS.reserve((size_t)n_models * N));
+  for (uint32_t m = 0; m < n_models; ++m) {
+    CUP(cudaMemcpyAsync(d.lat.p + lat_off[m], models[m].lat_us, 4 * C * Ms[m] * B, cudaMemcpyHostToDevice, d.s));
+    CUP(cudaMemcpyAsync(d.S.p + s_off[m], models[m].act_bytes, 8 * (size_t)Ms[m], cudaMemcpyHostToDevice, d.s));
+  }
+  CUP(cudaMemcpyAsync(d.lo.p, lat_off.data(), 8 * (size_t)n_models, cudaMemcpyHostToDevice, d.s));
+  CUP(cudaMemcpyAsync(d.so.p, s_off.data(), 8 * (size_t)n_models, cudaMemcpyHostToDevice, d.s));
+  CUP(cudaMemcpyAsync(d.M.p, Ms.data(), 4 * (size_t)n_models, cudaMemcpyHostToDevice, d.s));
+  PrepartProblem pp{d.lat.p, d.S.p, d.lo.p, d.so.p, d.M.p, d.prefix.p, d.bounds.p, d.blat.p, d.bS.p,
+                    (int)n_models, (int)C, (int)B, (int)N, (int)ref_class, (int)ref_batch};
+  CUP(launch_prepartition(pp, d.s));
+  CUP(cudaMemcpyAsync(bounds, d.bounds.p, 4 * (size_t)n_models * (N + 1), cudaMemcpyDeviceToHost, d.s));
+  CUP(cudaMemcpyAsync(block_lat, d.blat.p, 4 * (size_t)n_models * C * N * B, cudaMemcpyDeviceToHost, d.s));
+  CUP(cudaMemcpyAsync(block_bytes, d.bS.p, 8 * (size_t)n_models * N, cudaMemcpyDeviceToHost, d.s));
+  CUP(cudaStreamSynchronize(d.s));
+#undef CUP
+  return PPIPE_OK;
+}
+
 PPIPE_API int ppipe_partition_rows(uint32_t n_models, const uint32_t* n_layers, uint32_t n_classes,
                                    uint32_t n_batches, uint32_t max_partitions, int32_t rank, int32_t world,
                                    uint32_t* rows) {

@@ -88,4 +88,22 @@ cudaError_t truncate_frontier(const ppipe_point* in, const uint64_t* seg_offsets
                               const uint32_t* T_new, ppipe_point* out, uint64_t* seg_offsets_out,
                               uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches);
 
+// Greedy pre-partitioning (ppipe_prepartition). Device arrays: lat/S of all models
+// concatenated at lat_off/s_off, M per model; outputs bounds [n][N+1], block_lat
+// [n][C][N][B] at n*C*N*B stride, block_S [n][N]; prefix scratch of sum(M+1) int64 at
+// s_off + model index (one extra entry per model).
+struct PrepartProblem {
+  const uint32_t* lat;
+  const uint64_t* S;
+  const uint64_t* lat_off;
+  const uint64_t* s_off;
+  const uint32_t* M;
+  int64_t* prefix;
+  uint32_t* bounds;
+  uint32_t* block_lat;
+  uint64_t* block_S;
+  int n_models, C, B, N, ref_class, ref_b;
+};
+cudaError_t launch_prepartition(const PrepartProblem& p, cudaStream_t s);
+
 }  // namespace ppipe

@@ -1466,4 +1466,100 @@ cudaError_t truncate_frontier(const ppipe_point* in, const uint64_t* seg_offsets
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// greedy pre-partitioning (§5.2)
+// ---------------------------------------------------------------------------
+// One warp per model: prefix sums T of the reference runtimes, then per block the
+// first layer j in [i+1, guard) whose inclusion would move the block's runtime
+// strictly farther from total/N, f(j+1) > f(j) with f(j) = |N (T[j] - T[i]) - total|
+// (the greedy's stopping point; j = guard if none), found 32 candidates per ballot.
+__global__ void prepart_bounds_kernel(PrepartProblem p) {
+  const int warps = blockDim.x >> 5;
+  const int m = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (m >= p.n_models) return;
+  const int M = (int)p.M[m];
+  const int N = p.N;
+  const uint32_t* t = p.lat + p.lat_off[m] + (size_t)p.ref_class * M * p.B + p.ref_b;
+  int64_t* T = p.prefix + p.s_off[m] + m;  // M + 1 entries
+  int64_t carry = 0;
+  if (lane == 0) T[0] = 0;
+  for (int base = 0; base < M; base += 32) {
+    const int l = base + lane;
+    int64_t v = l < M ? (int64_t)t[(size_t)l * p.B] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int64_t u = __shfl_up_sync(FULL_MASK, v, d);
+      if (lane >= d) v += u;
+    }
+    if (l < M) T[l + 1] = carry + v;
+    carry += __shfl_sync(FULL_MASK, v, 31);
+  }
+  __syncwarp();
+  const int64_t total = carry;
+  uint32_t* bnd = p.bounds + (size_t)m * (N + 1);
+  int i = 0;
+  if (lane == 0) bnd[0] = 0;
+  for (int blk = 0; blk + 1 < N; ++blk) {
+    const int guard = M - (N - blk - 1);
+    const int64_t Ti = T[i];
+    int j = guard;
+    for (int base = i + 1; base < guard; base += 32) {
+      const int jj = base + lane;
+      bool stop = false;
+      if (jj < guard) {
+        int64_t without = (int64_t)N * (T[jj] - Ti) - total, with = (int64_t)N * (T[jj + 1] - Ti) - total;
+        without = without < 0 ? -without : without;
+        with = with < 0 ? -with : with;
+        stop = with > without;
+      }
+      const unsigned hit = __ballot_sync(FULL_MASK, stop);
+      if (hit) {
+        j = base + __ffs(hit) - 1;
+        break;
+      }
+    }
+    if (lane == 0) bnd[blk + 1] = (uint32_t)j;
+    i = j;
+  }
+  if (lane == 0) bnd[N] = (uint32_t)M;
+  __syncwarp();
+  const uint64_t* S = p.S + p.s_off[m];
+  for (int q = lane; q < N; q += 32) p.block_S[(size_t)m * N + q] = S[bnd[q + 1] - 1];
+}
+
+// Block sums: CTA per model, threads over (class, batch) so each layer's row is
+// read coalesced; the running sum is written out at every block boundary.
+__global__ void prepart_sum_kernel(PrepartProblem p) {
+  const int m = blockIdx.x;
+  const int M = (int)p.M[m];
+  const int N = p.N, C = p.C, B = p.B;
+  const uint32_t* lat = p.lat + p.lat_off[m];
+  const uint32_t* bnd = p.bounds + (size_t)m * (N + 1);
+  uint32_t* out = p.block_lat + (size_t)m * C * N * B;
+  for (int kb = threadIdx.x; kb < C * B; kb += blockDim.x) {
+    const int k = kb / B, b = kb - k * B;
+    const uint32_t* row = lat + (size_t)k * M * B + b;
+    int q = 0, next = (int)bnd[1];
+    uint32_t acc = 0;
+    for (int l = 0; l < M; ++l) {
+      if (l == next) {
+        out[((size_t)k * N + q) * B + b] = acc;
+        acc = 0;
+        ++q;
+        next = (int)bnd[q + 1];
+      }
+      acc += row[(size_t)l * B];
+    }
+    out[((size_t)k * N + q) * B + b] = acc;
+  }
+}
+
+cudaError_t launch_prepartition(const PrepartProblem& p, cudaStream_t s) {
+  if (p.n_models == 0) return cudaSuccess;
+  prepart_bounds_kernel<<<(p.n_models + 3) / 4, 128, 0, s>>>(p);
+  prepart_sum_kernel<<<p.n_models, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
 }  // namespace ppipe

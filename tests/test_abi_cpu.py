@@ -107,6 +107,21 @@ def test_no_cpu_fallback_without_device(pplib):
     assert e.value.code == -4 and "no CPU fallback" in str(e.value)
 
 
+def test_prepartition_validates_before_touching_a_device(pplib):
+    lat, S = [np.ones((2, 5, 3), np.uint32)], [np.zeros(5, np.uint64)]
+    with pytest.raises(pplib.PPipeError) as e:
+        pplib.prepartition(lat, S, 6)
+    assert e.value.code == -1 and "n_blocks 6 must be 1..5" in str(e.value)
+    with pytest.raises(pplib.PPipeError) as e:
+        pplib.prepartition(lat, S, 2, ref_class=2)
+    assert e.value.code == -1 and "reference class" in str(e.value)
+    import torch
+    if not torch.cuda.is_available():
+        with pytest.raises(pplib.PPipeError) as e:
+            pplib.prepartition(lat, S, 2)
+        assert e.value.code == -4 and "no CPU fallback" in str(e.value)
+
+
 def _weights(Ms, C, B, rows):
     w = 0
     for M, (lo, hi) in zip(Ms, rows):

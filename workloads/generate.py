@@ -208,7 +208,9 @@ def _prepartition(lat: np.ndarray, S: np.ndarray, n_blocks: int, ref_class: int,
     return blat.astype(np.uint32), bS, bounds
 
 
-def config3(n_models: int = 18, n_blocks: int = 10) -> Workload:
+def config3(n_models: int = 18, n_blocks: Optional[int] = 10) -> Workload:
+    """18 CNN-like models pre-partitioned into n_blocks blocks on the L4-like class at
+    batch 1; n_blocks=None gives the layer-level models ("3L")."""
     classes = ["V100", "L4", "T4", "P4"]
     batches = np.arange(1, 33, dtype=np.uint32)
     models, slos = [], []
@@ -219,8 +221,11 @@ def config3(n_models: int = 18, n_blocks: int = 10) -> Workload:
         lat = _layer_latencies(rng, M, classes, batches, t1)
         S = _act_bytes(rng, M)
         slo = _default_slo(lat, batches)
-        blat, bS, _ = _prepartition(lat, S, n_blocks, classes.index("L4"), 0)
-        models.append(ModelProfile(f"cnn{m:02d}-N{n_blocks}", blat, bS))
+        if n_blocks is None:
+            models.append(ModelProfile(f"cnn{m:02d}", lat, S))
+        else:
+            blat, bS, _ = _prepartition(lat, S, n_blocks, classes.index("L4"), 0)
+            models.append(ModelProfile(f"cnn{m:02d}-N{n_blocks}", blat, bS))
         slos.append(slo)
     return Workload(3, CONFIG_NAMES[3], classes, batches, _bw_matrix(classes), models,
                     np.array(slos, dtype=np.uint32), 400, 3)
