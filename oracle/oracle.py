@@ -62,6 +62,7 @@ def _load():
                                    ct.POINTER(ct.POINTER(_Result))]
         lib.oracle_result_free.argtypes = [ct.POINTER(_Result)]
         lib.oracle_set_threads.argtypes = [ct.c_int]
+        lib.oracle_set_vgpu.argtypes = [ct.POINTER(ct.c_uint8), ct.c_uint32]
         lib.oracle_prepartition.restype = ct.c_int
         lib.oracle_prepartition.argtypes = [ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.POINTER(ct.c_uint32),
                                             ct.POINTER(ct.c_uint64), ct.c_uint32, ct.c_uint32, ct.c_uint32,
@@ -86,10 +87,17 @@ def _u32p(a: np.ndarray):
 def run_oracle(w, model_lo: int = 0, model_hi: Optional[int] = None, only_K: int = 0,
                only_cls: Optional[Sequence[int]] = None, row_lo: int = 0, row_hi: int = 0,
                threads: int = 0, slo_us: Optional[np.ndarray] = None,
-               margin_permille: Optional[int] = None, kmax: Optional[int] = None) -> OracleResult:
-    """Run the oracle on a workloads.Workload (or a sub-range of its models)."""
+               margin_permille: Optional[int] = None, kmax: Optional[int] = None,
+               vgpu: Optional[Sequence[int]] = None) -> OracleResult:
+    """Run the oracle on a workloads.Workload (or a sub-range of its models).
+    vgpu: per-class virtual-GPU count v_k (theta = min_d v_d b / C_d); None = all 1."""
     lib = _load()
     lib.oracle_set_threads(int(threads))
+    if vgpu is not None:
+        varr = (ct.c_uint8 * w.n_classes)(*[int(v) for v in vgpu])
+        lib.oracle_set_vgpu(varr, w.n_classes)
+    else:
+        lib.oracle_set_vgpu(None, 0)
     n = len(w.models)
     model_hi = n if model_hi is None else model_hi
     keep = []

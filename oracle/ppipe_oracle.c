@@ -22,6 +22,7 @@
  *             E   = sum_d C_d + sum_d Y_d                          eq. 1.12
  *             feasible iff E <= T                                  eq. 1.12 "<= T" (reading A6)
  *             theta = b / max_d C_d  (exact rational; C = 0 => +inf) X_{ldbij} = b / C, x_l = min_d x_ld,
+ *                     (with virtual GPUs: min_d v_{k_d} b / C_d, see oracle_set_vgpu)
  *                                                                  PAPER.md:2245, 2281, 2284 (reading A11)
  *   per segment (m, K, k_1..k_K): sort feasible candidates by
  *       (E asc, theta desc, b asc, (c_1, c_2) lexicographic asc)
@@ -96,23 +97,50 @@ static void cvec_push(cvec *a, const cand *c) {
   a->v[a->n++] = *c;
 }
 
-static int64_t cmax_of(const cand *c, int K) {
-  int64_t m = c->st[0];
-  for (int d = 1; d < K; d++)
-    if (c->st[d] > m) m = c->st[d];
-  return m;
+/*
+ * Virtual GPUs (§5.1; App. A.2 L_{kvbi}):
+ * class k may be a "pseudo-class" running on 1/v_k of a physical GPU (MPS), so
+ * v_k instances share one GPU and a stage's per-physical-GPU throughput is
+ * v_k * b / C_d. The plan's throughput is its bottleneck, the minimum over stages
+ * (x_l = min_d x_ld): theta = min_d v_{k_d} * b / C_d. With every
+ * v = 1 (the default) this is b / max_d C_d. theta is kept as the exact fraction
+ * (num, den) = (v_d* b, C_d*) of the minimising stage d* (den = 0 is +inf).
+ */
+static uint8_t g_vgpu[256]; /* per class; 0 = unset = 1 */
+
+void oracle_set_vgpu(const uint8_t *v, uint32_t n_classes) {
+  memset(g_vgpu, 0, sizeof g_vgpu);
+  if (v)
+    for (uint32_t k = 0; k < n_classes && k < 256; k++) g_vgpu[k] = v[k];
 }
 
-/* theta_p > theta_q  <=>  b_p * Cmax_q > b_q * Cmax_p  (exact; Cmax = 0 is +inf). */
-static int theta_gt(int64_t bp, int64_t cp, int64_t bq, int64_t cq) { return bp * cq > bq * cp; }
+static int64_t vgpu_of(int k) { return g_vgpu[k] ? g_vgpu[k] : 1; }
+
+/* theta_p > theta_q for fractions num/den (den = 0 is +inf; two +inf tie) */
+static int theta_gt(int64_t np_, int64_t dp, int64_t nq, int64_t dq) { return np_ * dq > nq * dp; }
+
+static void theta_of(const cand *c, int K, const int *cls, int64_t *num, int64_t *den) {
+  *num = vgpu_of(cls[0]) * c->b;
+  *den = c->st[0];
+  for (int d = 1; d < K; d++) {
+    const int64_t n2 = vgpu_of(cls[d]) * c->b, d2 = c->st[d];
+    if (theta_gt(*num, *den, n2, d2)) { /* stage d is slower: it is the bottleneck so far */
+      *num = n2;
+      *den = d2;
+    }
+  }
+}
 
 static int g_sort_K; /* qsort has no context argument; sorting is single-threaded */
+static int g_sort_cls[3];
 static int cand_cmp(const void *pa, const void *pb) {
   const cand *p = (const cand *)pa, *q = (const cand *)pb;
   if (p->E != q->E) return p->E < q->E ? -1 : 1;
-  int64_t cp = cmax_of(p, g_sort_K), cq = cmax_of(q, g_sort_K);
-  if (theta_gt(p->b, cp, q->b, cq)) return -1; /* theta descending */
-  if (theta_gt(q->b, cq, p->b, cp)) return 1;
+  int64_t np_, dp, nq, dq;
+  theta_of(p, g_sort_K, g_sort_cls, &np_, &dp);
+  theta_of(q, g_sort_K, g_sort_cls, &nq, &dq);
+  if (theta_gt(np_, dp, nq, dq)) return -1; /* theta descending */
+  if (theta_gt(nq, dq, np_, dp)) return 1;
   if (p->b != q->b) return p->b < q->b ? -1 : 1;
   if (p->c1 != q->c1) return p->c1 < q->c1 ? -1 : 1;
   if (p->c2 != q->c2) return p->c2 < q->c2 ? -1 : 1;
@@ -378,14 +406,22 @@ int oracle_run(uint32_t n_models, const oracle_model *models, uint32_t n_classes
         for (int t = 0; t < nthreads; t++)
           for (size_t i = 0; i < ws[t].segs[K][s].n; i++) cvec_push(&all, &ws[t].segs[K][s].v[i]);
         g_sort_K = (int)K;
+        {
+          uint32_t t = s; /* the segment's class tuple (lexicographic index) */
+          for (int d = (int)K - 1; d >= 0; d--) {
+            g_sort_cls[d] = (int)(t % C);
+            t /= C;
+          }
+        }
         if (all.n) qsort(all.v, all.n, sizeof(cand), cand_cmp);
-        int64_t best_b = 0, best_c = 1; /* theta = 0 */
+        int64_t best_n = 0, best_d = 1; /* theta = 0 */
         for (size_t i = 0; i < all.n; i++) {
           const cand *p = &all.v[i];
-          int64_t cm = cmax_of(p, (int)K);
-          if (!theta_gt(p->b, cm, best_b, best_c)) continue; /* keep iff theta > best (strict) */
-          best_b = p->b;
-          best_c = cm;
+          int64_t tn, td;
+          theta_of(p, (int)K, g_sort_cls, &tn, &td);
+          if (!theta_gt(tn, td, best_n, best_d)) continue; /* keep iff theta > best (strict) */
+          best_n = tn;
+          best_d = td;
           if (res->n_pts == cap_pts) {
             cap_pts = cap_pts ? cap_pts * 2 : 1024;
             res->pts = (oracle_point *)realloc(res->pts, cap_pts * sizeof(oracle_point));

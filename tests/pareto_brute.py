@@ -17,8 +17,11 @@ def t_eff(slo_us: int, margin_permille: int) -> int:
     return (int(slo_us) * (1000 - int(margin_permille))) // 1000
 
 
-def enumerate_candidates(w, m: int, slo_us=None):
-    """All candidates of model m: dict segment(K, cls) -> list of candidate dicts."""
+def enumerate_candidates(w, m: int, slo_us=None, vgpu=None):
+    """All candidates of model m: dict segment(K, cls) -> list of candidate dicts.
+    vgpu: per-class virtual-GPU counts; a stage on class k with v_k instances per
+    physical GPU has per-GPU throughput v_k b / C, the plan
+    the minimum over its stages (x_l = min_d x_ld)."""
     mp = w.models[m]
     lat = mp.lat_us.astype(object)
     S = [int(x) for x in mp.act_bytes]
@@ -40,13 +43,18 @@ def enumerate_candidates(w, m: int, slo_us=None):
                     n_cand += 1
                     if E > T:
                         continue
-                    out.setdefault((K, cls), []).append(
-                        dict(E=E, b=b, cmax=max(stages), cuts=tuple(cuts) + (0,) * (2 - len(cuts)),
-                             stages=stages, trans=trans))
+                    cand = dict(E=E, b=b, cmax=max(stages), cuts=tuple(cuts) + (0,) * (2 - len(cuts)),
+                                stages=stages, trans=trans)
+                    if vgpu is not None:
+                        cand["theta"] = min(Fraction(int(vgpu[cls[d]]) * b, stages[d]) if stages[d] > 0
+                                            else Fraction(10**30) for d in range(K))
+                    out.setdefault((K, cls), []).append(cand)
     return out, n_cand
 
 
 def theta(c):
+    if "theta" in c:
+        return c["theta"]
     return Fraction(c["b"], c["cmax"]) if c["cmax"] > 0 else Fraction(10**30)
 
 

@@ -219,10 +219,10 @@ def test_p7_linear_partition_special_case(oracle_built, seed):
 
 # ---------------- P8: literal O(n^2) Pareto definition ----------------
 
-def compare_with_literal(w, r, use_np=False):
+def compare_with_literal(w, r, use_np=False, vgpu=None):
     n_cand_total = 0
     for m in range(len(w.models)):
-        segs, n_cand = pb.enumerate_candidates(w, m)
+        segs, n_cand = pb.enumerate_candidates(w, m, vgpu=vgpu)
         n_cand_total += n_cand
         C, M = w.n_classes, w.models[m].n_layers
         for K in range(1, min(w.kmax, M) + 1):
@@ -257,6 +257,51 @@ def test_p8_literal_pareto_config1(oracle_built):
 def test_p8_literal_pareto_config2(oracle_built):
     w = config2()
     compare_with_literal(w, run_oracle(w), use_np=True)
+
+
+# ---------------- P10: virtual GPUs (App. A.2) ----------------
+# A pseudo-class k on 1/v_k of a GPU: per-GPU stage throughput v_k b / C_d, plan
+# throughput min over stages. Pinned by the literal definition with Fractions.
+
+@pytest.mark.parametrize("seed", range(40))
+def test_p10_vgpu_literal_pareto_fuzz(oracle_built, seed):
+    w = random_tiny(seed, n_models=1 + seed % 2)
+    rng = np.random.default_rng(seed)
+    v = [int(x) for x in rng.integers(1, 5, size=w.n_classes)]
+    compare_with_literal(w, run_oracle(w, threads=1 + seed % 2, vgpu=v), vgpu=v)
+
+
+def test_p10_vgpu_uniform_scaling_is_neutral(oracle_built):
+    """Scaling every v by the same factor scales every theta alike: same frontier."""
+    w = config2()
+    base = run_oracle(w)
+    for v in (2, 3, 4):
+        r = run_oracle(w, vgpu=[v] * w.n_classes)
+        assert np.array_equal(r.points.view(np.uint8), base.points.view(np.uint8)), v
+
+
+def test_p10_vgpu_hand_worked_bottleneck_moves(oracle_built):
+    """M = 3 layers of 10, 20, 30 us on two classes with identical profiles, b = 1, no
+    transfer cost, K = 2. Both cuts have E = 60: c = 1 gives C = (10, 50), c = 2 gives
+    C = (30, 30), so one point per segment survives, the one with the larger theta.
+    All v = 1: theta(c=1) = 1/50 < theta(c=2) = 1/30 -> c = 2 everywhere.
+    v = (1, 2): segment (0, 1): c=1 runs its stages at 1/10 and 2/50 per GPU -> 1/25,
+    c=2 at 1/30 and 2/30 -> 1/30, so c = 1 wins; segment (1, 0): c=1 -> min(2/10, 1/50)
+    = 1/50, c=2 -> min(2/30, 1/30) = 1/30, so c = 2 stays."""
+    from tests.fixtures import make_workload
+    lat = np.array([[[10], [20], [30]], [[10], [20], [30]]], dtype=np.uint32)
+    w = make_workload([lat], [[0, 0, 0]], 1000, [1], 10**6, margin=0, kmax=2)
+
+    def k2_cut(r, cls):
+        pts = [p for p in r.points if int(p["K"]) == 2 and tuple(int(c) for c in p["cls"][:2]) == cls]
+        assert len(pts) == 1 and int(pts[0]["e2e_us"]) == 60
+        return int(pts[0]["cut"][0])
+
+    base = run_oracle(w)
+    assert [k2_cut(base, c) for c in [(0, 0), (0, 1), (1, 0), (1, 1)]] == [2, 2, 2, 2]
+    r = run_oracle(w, vgpu=[1, 2])
+    assert [k2_cut(r, c) for c in [(0, 0), (0, 1), (1, 0), (1, 1)]] == [2, 1, 2, 2]
+    compare_with_literal(w, r, vgpu=[1, 2])
 
 
 # ---------------- invariants on the oracle ----------------
