@@ -154,6 +154,17 @@ typedef struct {
  * done. Errors: PPIPE_ESTATE (no prior ppipe_enumerate), PPIPE_ECUDA, PPIPE_ENCCL. */
 int ppipe_pareto(ppipe_ctx *ctx, int copy_to_host, ppipe_frontier *out);
 
+/* Virtual GPUs (§5.1; App. A.2 L_{kvbi}): declare
+ * class k a pseudo-class that runs on 1/vgpu[k] of a physical GPU (MPS), vgpu[k] in
+ * 1..4 (NULL = all 1, the default). Its profile is the caller's lat_us for that
+ * fraction; a stage on it then delivers vgpu[k] * b / C_d per physical GPU, and a
+ * plan's throughput is the minimum over its stages: theta = min_d v_{k_d} b / C_d
+ * (exact; implemented as b / max_d (L / v_{k_d}) C_d with L the lcm of the v's in
+ * use). Applies from the next ppipe_enumerate; invalidates the last results.
+ * Envelope: T_eff * L / min v < 2^31 (else PPIPE_ERANGE at ppipe_enumerate).
+ * Errors: PPIPE_EINVAL. */
+int ppipe_set_vgpu(ppipe_ctx *ctx, const uint8_t *vgpu);
+
 /* SLO sweep from one enumeration (Fig. 12a).
  * The frontier at a lower latency target is a prefix of every segment of the
  * frontier at a higher one (invariant I3: a point's dominators all have smaller or

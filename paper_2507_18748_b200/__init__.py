@@ -19,6 +19,7 @@ from ._binding import (  # noqa: F401
     partition_rows,
     prepartition,
     run,
+    set_vgpu,
     update_profiles,
     lib,
     LIB_PATH,

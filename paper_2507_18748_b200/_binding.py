@@ -80,6 +80,8 @@ def lib():
         L.ppipe_prepartition.argtypes = [ct.c_uint32, ct.POINTER(_Model), ct.c_uint32, ct.c_uint32, ct.c_uint32,
                                          ct.c_uint32, ct.c_uint32, ct.c_int32, ct.POINTER(ct.c_uint32),
                                          ct.POINTER(ct.c_uint32), ct.POINTER(ct.c_uint64)]
+        L.ppipe_set_vgpu.restype = ct.c_int
+        L.ppipe_set_vgpu.argtypes = [ct.c_void_p, ct.POINTER(ct.c_uint8)]
         L.ppipe_frontier_at.restype = ct.c_int
         L.ppipe_frontier_at.argtypes = [ct.c_void_p, ct.POINTER(ct.c_uint32), ct.c_uint32, ct.c_int,
                                         ct.POINTER(_Frontier)]
@@ -269,6 +271,15 @@ def prepartition(lat_us: Sequence[np.ndarray], act_bytes: Sequence[np.ndarray], 
     return bounds, [blat[m] for m in range(n)], bS
 
 
+def set_vgpu(ctx: Context, vgpu: Optional[Sequence[int]]) -> None:
+    """Per-class virtual-GPU counts (include/ppipe.h ppipe_set_vgpu); None = all 1."""
+    if vgpu is None:
+        _check(lib().ppipe_set_vgpu(ctx.handle, None), ctx.handle)
+        return
+    arr = (ct.c_uint8 * len(vgpu))(*[int(v) for v in vgpu])
+    _check(lib().ppipe_set_vgpu(ctx.handle, arr), ctx.handle)
+
+
 def free(ctx: Context) -> None:
     if ctx is not None and ctx.handle:
         lib().ppipe_free(ctx.handle)
@@ -285,10 +296,12 @@ def partition_rows(n_layers: Sequence[int], n_classes: int, n_batches: int, max_
 
 
 def run(w, rank: int = 0, world: int = 1, device: int = -1, nccl_id: Optional[bytes] = None,
-        copy_to_host: bool = True) -> Frontier:
-    """One full pass: load, enumerate, pareto, free."""
+        copy_to_host: bool = True, vgpu: Optional[Sequence[int]] = None) -> Frontier:
+    """One full pass: load, (set_vgpu), enumerate, pareto, free."""
     ctx = load_workload(w, rank, world, device, nccl_id)
     try:
+        if vgpu is not None:
+            set_vgpu(ctx, vgpu)
         enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
         return pareto(ctx, copy_to_host)
     finally:

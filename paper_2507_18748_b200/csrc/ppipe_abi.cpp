@@ -209,6 +209,9 @@ struct ppipe_ctx {
   unsigned long long* h_counters = nullptr;  // pinned [5]
   // enumerate state
   bool enumerated = false;
+  uint32_t wpack = 0x11111111u;  // per-class virtual-GPU weights (ppipe_set_vgpu), 4 bits each
+  int w_bits = 0;
+  uint32_t w_max = 1;
   // last ppipe_pareto result (base of ppipe_frontier_at)
   bool have_result = false;
   const ppipe_point* res_pts = nullptr;
@@ -736,6 +739,8 @@ static int run_enumerate(ppipe_ctx* c) {
   pb.batches = c->d_batches.p;
   pb.bw_v = c->d_bwv.p;
   pb.pair_v = c->d_pairv.p;
+  pb.wpack = c->wpack;
+  pb.w_bits = c->w_bits;
   pb.models = c->d_models.p;
   pb.n_local = (int)c->local.size();
   pb.raw_lat = c->d_lat.p;
@@ -783,6 +788,9 @@ PPIPE_API int ppipe_enumerate(ppipe_ctx* ctx, const ppipe_enum_params* p) {
     if (T >= (uint64_t)kRangeLimit)
       return fail(ctx, PPIPE_ERANGE, "model %u: T_eff %llu us >= 2^28 (int32 envelope)", m,
                   (unsigned long long)T);
+    if (T * ctx->w_max >= (1ull << 31))
+      return fail(ctx, PPIPE_ERANGE, "model %u: T_eff %llu us x virtual-GPU weight %u >= 2^31 (int32 envelope)", m,
+                  (unsigned long long)T, ctx->w_max);
   }
   ctx->have_result = false;
   ctx->last_params = *p;
@@ -825,7 +833,7 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
   CU(c, c->d_segoff_local.reserve(c->n_seg_total + 1));
   uint64_t n_local_pts = 0;
   CU(c, frontier_pass(c->d_surv.p, n_surv, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_local.p,
-                      c->d_segoff_local.p, &n_local_pts, &c->scratch, c->stream, &nl));
+                      c->d_segoff_local.p, &n_local_pts, &c->scratch, c->stream, &nl, c->wpack));
   CU(c, cudaEventRecord(c->ev[3], c->stream));
   const ppipe_point* d_pts = c->d_local.p;
   const uint64_t* d_off = c->d_segoff_local.p;
@@ -926,7 +934,7 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
     std::vector<uint64_t> mcount(straddle.size(), 0);
     if (n_dirty) {
       CU(c, frontier_pass(c->d_union.p, n_dirty, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_merged.p,
-                          c->d_segoff_final.p, &n_merged, &c->scratch, c->stream, &nl));
+                          c->d_segoff_final.p, &n_merged, &c->scratch, c->stream, &nl, c->wpack));
       std::vector<uint64_t> b(2 * straddle.size());
       for (size_t i = 0; i < straddle.size(); ++i) {
         CU(c, cudaMemcpyAsync(&b[2 * i], c->d_segoff_final.p + c->h_segbase[straddle[i]], 8,
@@ -995,6 +1003,33 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
     out->points = c->h_points.p;
     out->seg_offsets = c->h_segoff.p;
   }
+  return PPIPE_OK;
+}
+
+PPIPE_API int ppipe_set_vgpu(ppipe_ctx* c, const uint8_t* vgpu) {
+  if (!c) return fail(nullptr, PPIPE_EINVAL, "ppipe_set_vgpu: NULL ctx");
+  uint32_t v[8] = {1, 1, 1, 1, 1, 1, 1, 1};
+  if (vgpu)
+    for (uint32_t k = 0; k < c->C; ++k) {
+      if (vgpu[k] < 1 || vgpu[k] > 4)
+        return fail(c, PPIPE_EINVAL, "class %u: vgpu %u must be 1..4 (1/v of a GPU per instance)", k, vgpu[k]);
+      v[k] = vgpu[k];
+    }
+  uint32_t L = 1;  // lcm of the v's in use: weights L / v are integers <= 12
+  for (uint32_t k = 0; k < c->C; ++k) L = L * v[k] / std::gcd(L, v[k]);
+  uint32_t pack = 0, wmax = 1;
+  for (uint32_t k = 0; k < 8; ++k) {
+    const uint32_t w = k < c->C ? L / v[k] : 1;
+    pack |= w << (4 * k);
+    wmax = std::max(wmax, w);
+  }
+  int bits = 0;
+  while ((1u << bits) < wmax) ++bits;
+  c->wpack = pack;
+  c->w_max = wmax;
+  c->w_bits = bits;
+  c->enumerated = false;
+  c->have_result = false;
   return PPIPE_OK;
 }
 

@@ -46,6 +46,10 @@ struct Problem {
   const uint64_t* seg_base;  // [n_models_total] global segment id base per model (device)
   uint32_t max_M;
   int neg_one;                // -1, passed at run time (keeps IMAD on the FMA pipe)
+  // Virtual GPUs (ppipe_set_vgpu): 4-bit throughput weight w_k = L / v_k per class
+  // (L = lcm of the v's in use); theta = b / max_d(w_{k_d} C_d). All 1 by default.
+  uint32_t wpack;
+  int w_bits;                 // bits of max_k w_k (widens the fold keys' Cmax)
   int debug_flags;            // timing experiments only (PPIPE_DEBUG_FLAGS); 0 in production
 };
 
@@ -73,7 +77,8 @@ struct FrontierScratch {
 };
 cudaError_t frontier_pass(const ppipe_point* in, uint64_t n, const uint64_t* seg_base_by_model, int C,
                           uint64_t n_seg, ppipe_point* out, uint64_t* seg_offsets /* [n_seg+1] device */,
-                          uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches);
+                          uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches,
+                          uint32_t wpack /* Problem::wpack */);
 
 // CSR offsets [n_seg + 1] of n records already in canonical (segment-sorted)
 // order; seg_tmp holds n uint64 scratch entries.

@@ -232,6 +232,15 @@ __device__ __forceinline__ uint32_t pack_key(int E, int Cmax, int sh, int q) {
   return (cr << sh) | ((uint32_t)E & ((1u << sh) - 1u));
 }
 
+// Virtual-GPU throughput weight of class k (Problem::wpack) and a weighted stage
+// latency w * C, clamped at INT_MAX (only non-feasible values can reach it: a
+// feasible candidate has C <= T_eff and w * T_eff < 2^31 is checked on the host).
+__host__ __device__ __forceinline__ int wt(uint32_t wpack, int k) { return (int)((wpack >> (4 * k)) & 15u); }
+__device__ __forceinline__ int wmul(int w, int c) {
+  const long long v = (long long)w * c;
+  return v > INT_MAX ? INT_MAX : (int)v;
+}
+
 // raw [nc][nb + 2] -> fin [nc][nb + 2] (fin may be global memory). One warp per k_1.
 __device__ __noinline__ void tables_finalize(const uint32_t* raw, uint2* fin, int nc, int nb, int sh, int warp,
                                              int nwarps) {
@@ -286,7 +295,8 @@ struct CtaCtx {
   const int32_t* Pm;   // P[m] base
   const int32_t* Ym;   // Y[m] base
   size_t Mp, B;
-  int bi, b, k2, M, T, sh, q, m1, nb, dbg, row_len;
+  int bi, b, k2, M, T, sh, q, m1, nb, dbg, row_len, w2;
+  uint32_t wpack;
   uint32_t model;
   const uint8_t* pair_v;
   __device__ const int32_t* Prow(int k) const { return Pm + ((size_t)k * B + bi) * Mp; }
@@ -494,15 +504,16 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
           const int Emin = max(0, cx.T - t + Bmin);  // E >= 0 for every real candidate
           const uint32_t ur = Emin <= cx.T ? frow[Emin >> cx.sh].x : 0u;
           const int Umax = ur == kEmpty ? INT_MAX : (int)min(ur << cx.q, (uint32_t)INT_MAX);
+          const int C1w = wmul(wt(cx.wpack, k1), C1), w3 = wt(cx.wpack, k3);
           int lo = c1 + 1, hi = cx.M - 1;
-          if (Emin > cx.T || C1 >= Umax) {
+          if (Emin > cx.T || C1w >= Umax) {
             t = kInvalidThr;  // nothing of this slot can survive
           } else {
             // first c2 with R(c2) < Umax
             int a = c1 + 1, z = cx.M;
             while (a < z) {
               const int m = (a + z) >> 1;
-              if (Rs[m] < Umax) z = m;
+              if (wmul(w3, Rs[m]) < Umax) z = m;
               else a = m + 1;
             }
             lo = a;
@@ -511,7 +522,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
             z = cx.M;
             while (a < z) {
               const int m = (a + z) >> 1;
-              if (Qs[m] - p1[j] >= Umax) z = m;
+              if (wmul(cx.w2, Qs[m] - p1[j]) >= Umax) z = m;
               else a = m + 1;
             }
             hi = a - 1;
@@ -522,7 +533,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
               whi = max(whi, hi);
               // U is nonincreasing; from bucket b0 on U <= C1 <= Cmax, so nothing there
               // survives: only E < b0 << sh can  =>  B <= (b0 << sh) - 1 - A.
-              b0 = min(first_bucket_le(frow, nb, C1, cx.q), nb);
+              b0 = min(first_bucket_le(frow, nb, C1w, cx.q), nb);
               if (b0 < nb) t = t + min(0, (b0 << cx.sh) - 1 - cx.T);
             }
           }
@@ -532,7 +543,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
         sd.C1s[(j * NC + k1) * 32 + lane] = C1;
       }
       thr[j][k1] = t;
-      c1r[j][k1] = C1;
+      c1r[j][k1] = wmul(wt(cx.wpack, k1), C1);  // weighted: only Cmax uses it
     }
     if (pass == 2) sd.p1s[j * 32 + lane] = p1[j];
     if (pass == 1 && valid) cand += (unsigned long long)(cx.M - 1 - c1) * NC;
@@ -696,14 +707,15 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
       const int relu = rel + u;
       if (pass == 1) {
 #pragma unroll
+        const int Rw = wmul(wt(cx.wpack, k3), R);
         for (int j = 0; j < kJ1; ++j) {
           const bool v = 32 * j + lane < relu;
-          const int C2 = Q - p1[j];
+          const int C2w = wmul(cx.w2, Q - p1[j]);
 #pragma unroll
           for (int k1 = 0; k1 < NC; ++k1) {
             if (v && Bv <= thr[j][k1]) {
               const int E = cx.T - thr[j][k1] + Bv;
-              const int Cmax = max(max(c1r[j][k1], C2), R);
+              const int Cmax = max(max(c1r[j][k1], C2w), Rw);
               PPIPE_DCHECK(E >= 0 && (E >> cx.sh) < nb + 2);
               if (!(cx.dbg & 1)) atomicMin(raw + (size_t)k1 * (nb + 2) + (E >> cx.sh), pack_key(E, Cmax, cx.sh, cx.q));
               ++nfeas;
@@ -750,7 +762,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
             const int E = sd.As[sl * 32 + src] + Bv;
             const int C1 = sd.C1s[sl * 32 + src];
             const int C2 = Q - sd.p1s[j * 32 + src];
-            const int Cmax = max(max(C1, C2), R);
+            const int Cmax = max(max(wmul(wt(cx.wpack, k1), C1), wmul(cx.w2, C2)), wmul(wt(cx.wpack, k3), R));
             PPIPE_DCHECK(E >= 0 && E <= cx.T && (E >> cx.sh) < nb + 2 && src < 32 && j < kJ1);
             cond = survives(fin + (size_t)k1 * (nb + 2), E >> cx.sh, E, Cmax, cx.sh, cx.q);
             if (cond) rec = make_rec(cx.model, 3, c1_base + 32 * j + src, c2u, k1, cx.k2, k3, cx.b, E, C1, C2, R);
@@ -787,7 +799,9 @@ __device__ __forceinline__ void make_ctx(CtaCtx<NC>& cx, const Problem& pb, cons
   while ((cx.T >> sh) >= nb) ++sh;
   cx.sh = sh;
   const int bits_t = 32 - __clz(cx.T | 1);
-  cx.q = max(0, bits_t + 1 - (32 - sh));
+  cx.wpack = pb.wpack;
+  cx.w2 = wt(pb.wpack, k2);
+  cx.q = max(0, bits_t + pb.w_bits + 1 - (32 - sh));
 }
 
 // Shared-memory layout common to the score kernels (2 warps per CTA).
@@ -948,7 +962,7 @@ __global__ void __launch_bounds__(32 * kWarps, PPIPE_12_CTAS_PER_SM)
           const int y = valid ? __ldg(cx.Yrow(k1, k2) + c1) : 0;
           const int E = C1 + y + C2;
           const bool f = valid && E <= T;
-          const int Cmax = max(C1, C2);
+          const int Cmax = max(wmul(wt(cx.wpack, k1), C1), wmul(cx.w2, C2));
           if (pass == 1) {
             if (valid) ++cand;
             if (f) {
@@ -1202,10 +1216,11 @@ __global__ void seg_start_kernel(const uint64_t* keys, uint64_t n, uint64_t n_se
   start[s] = lo;
 }
 
-__device__ __forceinline__ uint32_t cmax_of(const ppipe_point& p) {
-  uint32_t m = p.stage_us[0];
-  if (p.K >= 2) m = max(m, p.stage_us[1]);
-  if (p.K >= 3) m = max(m, p.stage_us[2]);
+// Weighted bottleneck max_d w_{k_d} C_d (virtual GPUs; w = 1 by default). < 2^32.
+__device__ __forceinline__ uint32_t cmax_of(const ppipe_point& p, uint32_t wpack) {
+  uint32_t m = (uint32_t)wt(wpack, p.cls[0]) * p.stage_us[0];
+  if (p.K >= 2) m = max(m, (uint32_t)wt(wpack, p.cls[1]) * p.stage_us[1]);
+  if (p.K >= 3) m = max(m, (uint32_t)wt(wpack, p.cls[2]) * p.stage_us[2]);
   return m;
 }
 
@@ -1216,8 +1231,8 @@ __device__ __forceinline__ bool theta_gt(uint64_t bp, uint64_t cp, uint64_t bq, 
 
 // Is p canonically better than q among records with the same (segment, E)?
 // theta desc, then batch asc, then (c_1, c_2) asc: a strict total order on candidates.
-__device__ __forceinline__ bool better(const ppipe_point& p, const ppipe_point& q) {
-  const uint64_t cp = cmax_of(p), cq = cmax_of(q);
+__device__ __forceinline__ bool better(const ppipe_point& p, const ppipe_point& q, uint32_t wpack) {
+  const uint64_t cp = cmax_of(p, wpack), cq = cmax_of(q, wpack);
   if (theta_gt(p.batch, cp, q.batch, cq)) return true;
   if (theta_gt(q.batch, cq, p.batch, cp)) return false;
   if (p.batch != q.batch) return p.batch < q.batch;
@@ -1226,8 +1241,9 @@ __device__ __forceinline__ bool better(const ppipe_point& p, const ppipe_point& 
 }
 
 struct PickBetter {  // associative and commutative: "the better of two" under a total order
+  uint32_t wpack;
   __device__ __forceinline__ ppipe_point operator()(const ppipe_point& a, const ppipe_point& b) const {
-    return better(b, a) ? b : a;
+    return better(b, a, wpack) ? b : a;
   }
 };
 
@@ -1247,10 +1263,10 @@ __global__ void gather_kernel(const ppipe_point* in, const uint32_t* idx, uint64
 }
 
 __global__ void group_theta_kernel(const uint64_t* gkeys, const ppipe_point* best, uint64_t ng, uint64_t* segk,
-                                   Theta* th) {
+                                   Theta* th, uint32_t wpack) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ng; i += (uint64_t)gridDim.x * blockDim.x) {
     segk[i] = gkeys[i] >> kEBits;
-    th[i] = Theta{best[i].batch, cmax_of(best[i])};
+    th[i] = Theta{best[i].batch, cmax_of(best[i], wpack)};
   }
 }
 
@@ -1267,7 +1283,7 @@ static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; 
 // segment]; compact; CSR offsets by binary search. All stages are data-parallel.
 cudaError_t frontier_pass(const ppipe_point* in, uint64_t n, const uint64_t* seg_base_by_model, int C,
                           uint64_t n_seg, ppipe_point* out, uint64_t* seg_offsets, uint64_t* n_out_host,
-                          FrontierScratch* scratch, cudaStream_t s, int* n_launches) {
+                          FrontierScratch* scratch, cudaStream_t s, int* n_launches, uint32_t wpack) {
   int seg_bits = 1;
   while ((1ull << seg_bits) <= n_seg) ++seg_bits;
   const int end_bit = kEBits + seg_bits;
@@ -1278,7 +1294,7 @@ cudaError_t frontier_pass(const ppipe_point* in, uint64_t n, const uint64_t* seg
                                       (uint32_t*)nullptr, ni, 0, end_bit, s);
   if (e != cudaSuccess) return e;
   e = cub::DeviceReduce::ReduceByKey(nullptr, b_red, (uint64_t*)nullptr, (uint64_t*)nullptr, (ppipe_point*)nullptr,
-                                     (ppipe_point*)nullptr, (int64_t*)nullptr, PickBetter(), ni, s);
+                                     (ppipe_point*)nullptr, (int64_t*)nullptr, PickBetter{wpack}, ni, s);
   if (e != cudaSuccess) return e;
   e = cub::DeviceScan::ExclusiveScanByKey(nullptr, b_scan, (uint64_t*)nullptr, (Theta*)nullptr, (Theta*)nullptr,
                                           MaxTheta(), Theta{0, 1}, ni, cub::Equality(), s);
@@ -1332,14 +1348,14 @@ cudaError_t frontier_pass(const ppipe_point* in, uint64_t n, const uint64_t* seg
     e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, keys, keys2, vals, vals2, ni, 0, end_bit, s);
     if (e != cudaSuccess) return e;
     gather_kernel<<<blocks, 256, 0, s>>>(in, vals2, n, rec);
-    e = cub::DeviceReduce::ReduceByKey(tmp, b_red, keys2, gkeys, rec, best, d_num, PickBetter(), ni, s);
+    e = cub::DeviceReduce::ReduceByKey(tmp, b_red, keys2, gkeys, rec, best, d_num, PickBetter{wpack}, ni, s);
     if (e != cudaSuccess) return e;
     e = cudaMemcpyAsync(&ng, d_num, 8, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return e;
     e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return e;
     const int gb = (int)std::min<int64_t>((ng + 255) / 256, 148 * 16);
-    group_theta_kernel<<<gb, 256, 0, s>>>(gkeys, best, (uint64_t)ng, segk, th);
+    group_theta_kernel<<<gb, 256, 0, s>>>(gkeys, best, (uint64_t)ng, segk, th, wpack);
     e = cub::DeviceScan::ExclusiveScanByKey(tmp, b_scan, segk, th, pre, MaxTheta(), Theta{0, 1}, ng,
                                             cub::Equality(), s);
     if (e != cudaSuccess) return e;
