@@ -122,7 +122,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     from oracle import run_oracle
-    from workloads import config5, make_config
+    from workloads import CONFIG_NAMES, config5, make_config
     threads = _host_threads()
     w = config5(model_ids=[0]) if args.config == 5 else make_config(args.config)
     M = w.models[0].n_layers
@@ -150,7 +150,8 @@ def run_reference(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic", "config": {"workload": f"config {args.config}", "sample": sample},
+            "data": "synthetic", "config": {"workload": f"config {args.config}: {CONFIG_NAMES[args.config]}",
+                                            "sample": sample},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
