@@ -727,6 +727,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
         // threshold are listed warp-wide, then checked 32 at a time, one per lane,
         // against the finalized tables (survives()) and emitted.
         const int c2u = c2 + u;
+        const int Rw = wmul(wt(cx.wpack, k3), R);  // per c2 (may exceed T_eff for unlisted ones)
         unsigned fm = 0;
 #pragma unroll
         for (int j = 0; j < kJ1; ++j) {
@@ -762,7 +763,8 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
             const int E = sd.As[sl * 32 + src] + Bv;
             const int C1 = sd.C1s[sl * 32 + src];
             const int C2 = Q - sd.p1s[j * 32 + src];
-            const int Cmax = max(max(wmul(wt(cx.wpack, k1), C1), wmul(cx.w2, C2)), wmul(wt(cx.wpack, k3), R));
+            // listed candidates are feasible: C_1, C_2 <= E <= T_eff and w * T_eff < 2^31
+            const int Cmax = max(max(wt(cx.wpack, k1) * C1, cx.w2 * C2), Rw);
             PPIPE_DCHECK(E >= 0 && E <= cx.T && (E >> cx.sh) < nb + 2 && src < 32 && j < kJ1);
             cond = survives(fin + (size_t)k1 * (nb + 2), E >> cx.sh, E, Cmax, cx.sh, cx.q);
             if (cond) rec = make_rec(cx.model, 3, c1_base + 32 * j + src, c2u, k1, cx.k2, k3, cx.b, E, C1, C2, R);
