@@ -236,6 +236,8 @@ __device__ __forceinline__ uint32_t pack_key(int E, int Cmax, int sh, int q) {
 // latency w * C, clamped at INT_MAX (only non-feasible values can reach it: a
 // feasible candidate has C <= T_eff and w * T_eff < 2^31 is checked on the host).
 __host__ __device__ __forceinline__ int wt(uint32_t wpack, int k) { return (int)((wpack >> (4 * k)) & 15u); }
+template <bool W>
+__device__ __forceinline__ int wtw(uint32_t wpack, int k) { return W ? wt(wpack, k) : 1; }
 __device__ __forceinline__ int wmul(int w, int c) {
   const long long v = (long long)w * c;
   return v > INT_MAX ? INT_MAX : (int)v;
@@ -471,13 +473,16 @@ __device__ __forceinline__ SlotData carve_slot(uint8_t* base) {
   return d;
 }
 
-template <int NC, int pass>
+template <int NC, int pass, bool W>
 __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, int c1_hi,
                         const int32_t* Bs, const int32_t* Qs, const int32_t* Rs, uint32_t* raw, const uint2* fin,
                         const SlotData& sd, uint32_t* nb16, const ScoreOut& out, Emitter& em,
                         unsigned long long& feas, unsigned long long& cand, int Bmin = 0) {
   const int lane = threadIdx.x & 31;
   const int nb = cx.nb;
+  // virtual-GPU weights: compile-time 1 unless the context set some (W)
+  const uint32_t wp = W ? cx.wpack : 0x11111111u;
+  const int w2 = W ? cx.w2 : 1;
   int thr[kJ1][NC];
   int c1r[kJ1][NC];
   int p1[kJ1];
@@ -504,7 +509,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
           const int Emin = max(0, cx.T - t + Bmin);  // E >= 0 for every real candidate
           const uint32_t ur = Emin <= cx.T ? frow[Emin >> cx.sh].x : 0u;
           const int Umax = ur == kEmpty ? INT_MAX : (int)min(ur << cx.q, (uint32_t)INT_MAX);
-          const int C1w = wmul(wt(cx.wpack, k1), C1), w3 = wt(cx.wpack, k3);
+          const int C1w = wmul(wtw<W>(wp, k1), C1), w3 = wtw<W>(wp, k3);
           int lo = c1 + 1, hi = cx.M - 1;
           if (Emin > cx.T || C1w >= Umax) {
             t = kInvalidThr;  // nothing of this slot can survive
@@ -522,7 +527,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
             z = cx.M;
             while (a < z) {
               const int m = (a + z) >> 1;
-              if (wmul(cx.w2, Qs[m] - p1[j]) >= Umax) z = m;
+              if (wmul(w2, Qs[m] - p1[j]) >= Umax) z = m;
               else a = m + 1;
             }
             hi = a - 1;
@@ -543,7 +548,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
         sd.C1s[(j * NC + k1) * 32 + lane] = C1;
       }
       thr[j][k1] = t;
-      c1r[j][k1] = wmul(wt(cx.wpack, k1), C1);  // weighted: only Cmax uses it
+      c1r[j][k1] = wmul(wtw<W>(wp, k1), C1);  // weighted: only Cmax uses it
     }
     if (pass == 2) sd.p1s[j * 32 + lane] = p1[j];
     if (pass == 1 && valid) cand += (unsigned long long)(cx.M - 1 - c1) * NC;
@@ -706,11 +711,11 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
       const int R = u == 0 ? r4.x : (u == 1 ? r4.y : (u == 2 ? r4.z : r4.w));
       const int relu = rel + u;
       if (pass == 1) {
+        const int Rw = wmul(wtw<W>(wp, k3), R);
 #pragma unroll
-        const int Rw = wmul(wt(cx.wpack, k3), R);
         for (int j = 0; j < kJ1; ++j) {
           const bool v = 32 * j + lane < relu;
-          const int C2w = wmul(cx.w2, Q - p1[j]);
+          const int C2w = wmul(w2, Q - p1[j]);
 #pragma unroll
           for (int k1 = 0; k1 < NC; ++k1) {
             if (v && Bv <= thr[j][k1]) {
@@ -727,7 +732,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
         // threshold are listed warp-wide, then checked 32 at a time, one per lane,
         // against the finalized tables (survives()) and emitted.
         const int c2u = c2 + u;
-        const int Rw = wmul(wt(cx.wpack, k3), R);  // per c2 (may exceed T_eff for unlisted ones)
+        const int Rw = wmul(wtw<W>(wp, k3), R);  // per c2 (may exceed T_eff for unlisted ones)
         unsigned fm = 0;
 #pragma unroll
         for (int j = 0; j < kJ1; ++j) {
@@ -764,7 +769,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
             const int C1 = sd.C1s[sl * 32 + src];
             const int C2 = Q - sd.p1s[j * 32 + src];
             // listed candidates are feasible: C_1, C_2 <= E <= T_eff and w * T_eff < 2^31
-            const int Cmax = max(max(wt(cx.wpack, k1) * C1, cx.w2 * C2), Rw);
+            const int Cmax = max(max(wtw<W>(wp, k1) * C1, w2 * C2), Rw);
             PPIPE_DCHECK(E >= 0 && E <= cx.T && (E >> cx.sh) < nb + 2 && src < 32 && j < kJ1);
             cond = survives(fin + (size_t)k1 * (nb + 2), E >> cx.sh, E, Cmax, cx.sh, cx.q);
             if (cond) rec = make_rec(cx.model, 3, c1_base + 32 * j + src, c2u, k1, cx.k2, k3, cx.b, E, C1, C2, R);
@@ -778,7 +783,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
   feas += nfeas;
 }
 
-template <int NC>
+template <int NC, bool W>
 __device__ __forceinline__ void make_ctx(CtaCtx<NC>& cx, const Problem& pb, const DevModel& md, int k2, int bi,
                                          int nb) {
   cx.Pm = pb.P + md.p_off;
@@ -801,9 +806,10 @@ __device__ __forceinline__ void make_ctx(CtaCtx<NC>& cx, const Problem& pb, cons
   while ((cx.T >> sh) >= nb) ++sh;
   cx.sh = sh;
   const int bits_t = 32 - __clz(cx.T | 1);
-  cx.wpack = pb.wpack;
-  cx.w2 = wt(pb.wpack, k2);
-  cx.q = max(0, bits_t + pb.w_bits + 1 - (32 - sh));
+  // virtual-GPU weights only in the W instantiation (the plain one keeps constant 1s)
+  cx.wpack = W ? pb.wpack : 0x11111111u;
+  cx.w2 = W ? wt(pb.wpack, k2) : 1;
+  cx.q = max(0, bits_t + (W ? pb.w_bits : 0) + 1 - (32 - sh));
 }
 
 // Shared-memory layout common to the score kernels (2 warps per CTA).
@@ -911,7 +917,7 @@ static size_t score12_smem_bytes(int nb) {
 #ifndef PPIPE_12_NB_LOG2_MAX
 #define PPIPE_12_NB_LOG2_MAX 7
 #endif
-template <int NC>
+template <int NC, bool W>
 __global__ void __launch_bounds__(32 * kWarps, PPIPE_12_CTAS_PER_SM)
     score12_kernel(Problem pb, ScoreOut out, int nb_log2) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -932,7 +938,7 @@ __global__ void __launch_bounds__(32 * kWarps, PPIPE_12_CTAS_PER_SM)
   unsigned long long feas = 0, cand = 0;
   do {
     CtaCtx<NC> cx;
-    make_ctx(cx, pb, md, k2, bi, nb);
+    make_ctx<NC, W>(cx, pb, md, k2, bi, nb);
     const int M = cx.M, T = cx.T, sh = cx.sh, q = cx.q;
     // K = 1: segment (k2), whole model on class k2
     if (warp == 0 && md.row_lo == 0) {
@@ -964,7 +970,7 @@ __global__ void __launch_bounds__(32 * kWarps, PPIPE_12_CTAS_PER_SM)
           const int y = valid ? __ldg(cx.Yrow(k1, k2) + c1) : 0;
           const int E = C1 + y + C2;
           const bool f = valid && E <= T;
-          const int Cmax = max(wmul(wt(cx.wpack, k1), C1), wmul(cx.w2, C2));
+          const int Cmax = W ? max(wmul(wt(cx.wpack, k1), C1), wmul(cx.w2, C2)) : max(C1, C2);
           if (pass == 1) {
             if (valid) ++cand;
             if (f) {
@@ -1002,7 +1008,7 @@ constexpr int k3aCtasPerSm = PPIPE_3A_CTAS_PER_SM;
 #define PPIPE_3B_CTAS_PER_SM 6
 #endif
 constexpr int k3bCtasPerSm = PPIPE_3B_CTAS_PER_SM;  // pass 2 holds more live state: fewer, fatter warps
-template <int NC>
+template <int NC, bool W>
 __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
     score3a_kernel(Problem pb, ScoreOut out, int nb_log2, int row_len) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -1017,7 +1023,7 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
   const int bi = blockIdx.x / (NC * pb.n_local);
   const DevModel md = pb.models[ml];
   CtaCtx<NC> cx;
-  make_ctx(cx, pb, md, k2, bi, nb);
+  make_ctx<NC, W>(cx, pb, md, k2, bi, nb);
   cx.row_len = row_len;
   Emitter em{sm.ebuf + warp * 2 * kEmitBuf, 0};  // unused in pass 1
   unsigned long long feas = 0, cand = 0;
@@ -1036,7 +1042,7 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
         if (lane == 0) t = atomicAdd(&s_tile, 1);
         t = __shfl_sync(FULL_MASK, t, 0);
         if (t >= r.ntiles) break;
-        k3_tile<NC, 1>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin,
+        k3_tile<NC, 1, W>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin,
                        SlotData{}, sm.nb16 + warp * row_len, out, em, feas, cand);
       }
       if (__syncthreads_or(feas != feas0) && !(pb.debug_flags & 2)) {
@@ -1060,7 +1066,7 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
 // ---- kernel 3: K = 3 pass 2 over the hot units only (persistent CTAs pull units
 // from a counter): reload the unit's tables, re-scan with tightened thresholds and
 // emit the survivors. ----
-template <int NC>
+template <int NC, bool W>
 __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
     score3b_kernel(Problem pb, ScoreOut out, int nb_log2, int row_len) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -1083,7 +1089,7 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
     const int ml = (int)hu.x, k2 = (int)hu.y, k3 = (int)hu.z, bi = (int)hu.w;
     const DevModel md = pb.models[ml];
     CtaCtx<NC> cx;
-    make_ctx(cx, pb, md, k2, bi, nb);
+    make_ctx<NC, W>(cx, pb, md, k2, bi, nb);
     cx.row_len = row_len;
     const K3Range r = k3_range(md);
     const uint2* src = reinterpret_cast<const uint2*>(out.hot_tab) + u * (unsigned long long)ntab;
@@ -1101,7 +1107,7 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
       if (lane == 0) t = atomicAdd(&s_tile, 1);
       t = __shfl_sync(FULL_MASK, t, 0);
       if (t >= r.ntiles) break;
-      k3_tile<NC, 2>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin,
+      k3_tile<NC, 2, W>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin,
                      carve_slot<NC>(sm.slot + warp * slot_bytes<NC>()), sm.nb16 + warp * row_len, out, em, feas, cand, Bmin);
     }
     __syncthreads();
@@ -1114,8 +1120,8 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
 // rounded down to a power of two (128..2048 buckets).
 constexpr size_t kSmemBudget = 32 * 1024;  // sized for the pass-2 kernel (7 CTAs per SM)
 
-template <int NC>
-static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches) {
+template <int NC, bool W>
+static cudaError_t launch_score_w(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches) {
   const int row_len = (int)((((size_t)pb.max_M + 3) & ~(size_t)3) + 8 * kScanUnroll);
   int nb_log2 = 7;
   while (nb_log2 < 11 && table_policy_bytes<NC>(2 << nb_log2, row_len) <= kSmemBudget) ++nb_log2;
@@ -1127,25 +1133,31 @@ static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaS
   // resolution may differ from the K = 3 tables.
   const int nb12_log2 = std::min(nb_log2, PPIPE_12_NB_LOG2_MAX);
   const size_t smem12 = score12_smem_bytes<NC>(1 << nb12_log2);
-  e = cudaFuncSetAttribute(score12_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem12);
+  e = cudaFuncSetAttribute(score12_kernel<NC, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem12);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(score3a_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a);
+  e = cudaFuncSetAttribute(score3a_kernel<NC, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(score3b_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  e = cudaFuncSetAttribute(score3b_kernel<NC, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (pb.Kmax >= 3) {
-    score3a_kernel<NC><<<grid, 32 * kWarps, smem_a, s>>>(pb, out, nb_log2, row_len);
+    score3a_kernel<NC, W><<<grid, 32 * kWarps, smem_a, s>>>(pb, out, nb_log2, row_len);
     int dev = 0, n_sm = 148, smem_sm = 227 * 1024;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     const int ctas = std::max(1, std::min(k3bCtasPerSm, smem_sm / (int)(smem + 1024)));  // persistent: fill the SMs
-    score3b_kernel<NC><<<n_sm * ctas, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
+    score3b_kernel<NC, W><<<n_sm * ctas, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
     *n_launches += 2;
   }
-  score12_kernel<NC><<<(unsigned)pb.n_local * NC * pb.B, 32 * kWarps, smem12, s>>>(pb, out, nb12_log2);
+  score12_kernel<NC, W><<<(unsigned)pb.n_local * NC * pb.B, 32 * kWarps, smem12, s>>>(pb, out, nb12_log2);
   ++*n_launches;
   return cudaGetLastError();
+}
+
+template <int NC>
+static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches) {
+  return pb.wpack == 0x11111111u ? launch_score_w<NC, false>(pb, out, s, n_launches)
+                                 : launch_score_w<NC, true>(pb, out, s, n_launches);
 }
 
 // Bytes of one hot unit's tables for this problem (the ABI sizes its buffer with it).
@@ -1220,6 +1232,12 @@ __global__ void seg_start_kernel(const uint64_t* keys, uint64_t n, uint64_t n_se
 
 // Weighted bottleneck max_d w_{k_d} C_d (virtual GPUs; w = 1 by default). < 2^32.
 __device__ __forceinline__ uint32_t cmax_of(const ppipe_point& p, uint32_t wpack) {
+  if (wpack == 0x11111111u) {  // no virtual GPUs (uniform branch)
+    uint32_t m = p.stage_us[0];
+    if (p.K >= 2) m = max(m, p.stage_us[1]);
+    if (p.K >= 3) m = max(m, p.stage_us[2]);
+    return m;
+  }
   uint32_t m = (uint32_t)wt(wpack, p.cls[0]) * p.stage_us[0];
   if (p.K >= 2) m = max(m, (uint32_t)wt(wpack, p.cls[1]) * p.stage_us[1]);
   if (p.K >= 3) m = max(m, (uint32_t)wt(wpack, p.cls[2]) * p.stage_us[2]);

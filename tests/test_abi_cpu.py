@@ -107,6 +107,16 @@ def test_no_cpu_fallback_without_device(pplib):
     assert e.value.code == -4 and "no CPU fallback" in str(e.value)
 
 
+def test_build_has_no_compiler_warnings(pplib):
+    """A warning such as a misplaced '#pragma unroll' silently changes the kernels."""
+    import os
+    log = os.path.join(os.path.dirname(pplib.LIB_PATH), "build_ptxas.log")
+    if not os.path.exists(log):
+        pytest.skip("library not built in this checkout")
+    bad = [l for l in open(log) if "warning" in l.lower()]
+    assert not bad, "".join(bad[:5])
+
+
 def test_prepartition_validates_before_touching_a_device(pplib):
     lat, S = [np.ones((2, 5, 3), np.uint32)], [np.zeros(5, np.uint64)]
     with pytest.raises(pplib.PPipeError) as e:
