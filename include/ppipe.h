@@ -106,9 +106,12 @@ typedef struct {
 /* Replace the profile values of an existing context (same model count and
  * layer counts, same classes and batches): validate and copy host -> device.
  * Profiles change as workloads drift and the planner re-runs;
- * this keeps the device buffers and the NCCL communicator. The host -> device
- * copies overlap the host-side validation; the call returns only after both, so
- * the caller may reuse its buffers at once (page-locked buffers copy fastest).
+ * this keeps the device buffers and the NCCL communicator. The values are
+ * validated on the device right after the host -> device copy (same envelope and
+ * messages as ppipe_load_profiles; ranks with NCCL agree on the first failing
+ * model; in shard mode a rank checks its own models). The call returns after
+ * both, so the caller may reuse its buffers at once (page-locked buffers copy
+ * fastest).
  * Errors as for ppipe_load_profiles; after a failed update the context has no
  * usable profiles and ppipe_enumerate returns PPIPE_ESTATE until an update
  * succeeds. Invalidates the last ppipe_enumerate. */

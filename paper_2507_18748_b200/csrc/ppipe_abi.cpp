@@ -676,33 +676,55 @@ PPIPE_API int ppipe_update_profiles(ppipe_ctx* c, uint32_t n_models, const ppipe
     if (models[m].n_layers != c->Ms[m])
       return fail(c, PPIPE_EINVAL, "model %u: n_layers %u differs from the loaded %u", m, models[m].n_layers,
                   c->Ms[m]);
-  // The H2D copies (issued from a helper thread, so that pageable sources overlap
-  // too) run while the host validates the same bytes; a failed validation leaves
-  // the context without usable profiles until the next successful update.
+  // Copy, then validate on the device (the values are there anyway): one pass over
+  // the profiles at HBM speed instead of a host pass over the caller's memory. A
+  // failed validation leaves the context without usable profiles until the next
+  // successful update. Ranks with NCCL agree on the first failing model.
   c->profiles_ok = false;
   c->enumerated = false;
   c->have_result = false;
-  cudaError_t copy_err = cudaSuccess;
-  std::thread copier([&] {
-    copy_err = cudaSetDevice(c->device);
-    for (size_t i = 0; i < c->local.size() && copy_err == cudaSuccess; ++i) {
-      const int m = c->local[i];
-      const DevModel& d = c->h_models[i];
-      copy_err = cudaMemcpyAsync(c->d_lat.p + d.lat_off, models[m].lat_us, sizeof(uint32_t) * c->C * d.M * c->B,
-                                 cudaMemcpyHostToDevice, c->stream);
-      if (copy_err == cudaSuccess)
-        copy_err = cudaMemcpyAsync(c->d_s.p + d.s_off, models[m].act_bytes, sizeof(uint64_t) * d.M,
-                                   cudaMemcpyHostToDevice, c->stream);
-    }
-    // the caller may release its buffers once we return
-    const cudaError_t e = cudaStreamSynchronize(c->stream);
-    if (copy_err == cudaSuccess) copy_err = e;
-  });
-  std::string verr;
-  const int vrc = validate_models(n_models, models, c->C, c->B, c->h_batches.data(), &verr);
-  copier.join();
-  if (vrc != PPIPE_OK) return fail(c, vrc, "%s", verr.c_str());
-  CU(c, copy_err);
+  CU(c, cudaSetDevice(c->device));
+  for (size_t i = 0; i < c->local.size(); ++i) {
+    const int m = c->local[i];
+    const DevModel& d = c->h_models[i];
+    CU(c, cudaMemcpyAsync(c->d_lat.p + d.lat_off, models[m].lat_us, sizeof(uint32_t) * c->C * d.M * c->B,
+                          cudaMemcpyHostToDevice, c->stream));
+    CU(c, cudaMemcpyAsync(c->d_s.p + d.s_off, models[m].act_bytes, sizeof(uint64_t) * d.M, cudaMemcpyHostToDevice,
+                          c->stream));
+  }
+  CU(c, c->d_models.reserve(std::max<size_t>(c->h_models.size(), 1)));
+  CU(c, cudaMemcpyAsync(c->d_models.p, c->h_models.data(), sizeof(DevModel) * c->h_models.size(),
+                        cudaMemcpyHostToDevice, c->stream));
+  CU(c, c->d_cnt_send.reserve(4));
+  const unsigned long long none = ~0ull;
+  CU(c, cudaMemcpyAsync(c->d_cnt_send.p, &none, 8, cudaMemcpyHostToDevice, c->stream));
+  const uint64_t bmax = c->h_batches[c->B - 1];
+  CU(c, launch_validate(c->d_models.p, (int)c->local.size(), c->d_lat.p, c->d_s.p, (int)c->C, (int)c->B,
+                        (uint64_t)INT64_MAX / (8 * bmax), reinterpret_cast<unsigned long long*>(c->d_cnt_send.p),
+                        c->stream));
+  unsigned long long key = none;
+  if (c->world > 1 && c->comm) {
+    CU(c, c->d_cnt_recv.reserve((size_t)c->world));
+    NC_(c, g_nccl.AllGather(c->d_cnt_send.p, c->d_cnt_recv.p, 1, ncclUint64, c->comm, c->stream));
+    std::vector<unsigned long long> keys(c->world);
+    CU(c, cudaMemcpyAsync(keys.data(), c->d_cnt_recv.p, 8 * keys.size(), cudaMemcpyDeviceToHost, c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
+    for (auto k : keys) key = std::min(key, k);
+  } else {
+    CU(c, cudaMemcpyAsync(&key, c->d_cnt_send.p, 8, cudaMemcpyDeviceToHost, c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
+  }
+  if (key != none) {  // same wording as the host check of ppipe_load_profiles
+    const uint32_t m = (uint32_t)(key >> 40), idx = (uint32_t)(key & ((1ull << 39) - 1));
+    if (key & (1ull << 39))
+      return fail(c, PPIPE_ERANGE, "model %u layer %u: act_bytes %llu too large (8*S*b >= 2^63)", m, idx,
+                  (unsigned long long)models[m].act_bytes[idx]);
+    const uint32_t k = idx / c->B, bi = idx % c->B, M = models[m].n_layers;
+    uint64_t tot = 0;
+    for (uint32_t l = 0; l < M; ++l) tot += models[m].lat_us[((size_t)k * M + l) * c->B + bi];
+    return fail(c, PPIPE_ERANGE, "model %u class %u batch %u: whole-model latency %llu us >= 2^28 (int32 envelope)",
+                m, k, c->h_batches[bi], (unsigned long long)tot);
+  }
   c->profiles_ok = true;
   c->enumerated = false;
   return PPIPE_OK;

@@ -93,6 +93,15 @@ cudaError_t truncate_frontier(const ppipe_point* in, const uint64_t* seg_offsets
                               const uint32_t* T_new, ppipe_point* out, uint64_t* seg_offsets_out,
                               uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches);
 
+// Device-side profile validation for ppipe_update_profiles (the same envelope as
+// the host check of ppipe_load_profiles): per local model, every whole-model
+// latency sum_l lat[k][l][b] < 2^28 and every act_bytes <= smax. The first failure
+// in (model, kind, index) order is folded into *err_key by atomicMin:
+// model << 40 | kind << 39 | index, kind 0 = latency (index = k * B + b), 1 = bytes
+// (index = layer); UINT64_MAX = none.
+cudaError_t launch_validate(const DevModel* models, int n_local, const uint32_t* lat, const uint64_t* S, int C,
+                            int B, uint64_t smax, unsigned long long* err_key, cudaStream_t s);
+
 // Greedy pre-partitioning (ppipe_prepartition). Device arrays: lat/S of all models
 // concatenated at lat_off/s_off, M per model; outputs bounds [n][N+1], block_lat
 // [n][C][N][B] at n*C*N*B stride, block_S [n][N]; prefix scratch of sum(M+1) int64 at

@@ -1503,6 +1503,33 @@ cudaError_t truncate_frontier(const ppipe_point* in, const uint64_t* seg_offsets
 }
 
 // ---------------------------------------------------------------------------
+// device-side profile validation (ppipe_update_profiles)
+// ---------------------------------------------------------------------------
+__global__ void validate_kernel(const DevModel* models, const uint32_t* lat, const uint64_t* S, int C, int B,
+                                uint64_t smax, unsigned long long* err_key) {
+  const int i = blockIdx.x / C, k = blockIdx.x % C;
+  const DevModel md = models[i];
+  const int M = (int)md.M;
+  const uint32_t* L = lat + md.lat_off + (size_t)k * M * B;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    unsigned long long tot = 0;
+    for (int l = 0; l < M; ++l) tot += L[(size_t)l * B + b];  // coalesced over b
+    if (tot >= (unsigned long long)kRangeLimit)
+      atomicMin(err_key, ((unsigned long long)md.model << 40) | (unsigned long long)(k * B + b));
+  }
+  if (k == 0)
+    for (int l = threadIdx.x; l < M; l += blockDim.x)
+      if (S[md.s_off + l] > smax)
+        atomicMin(err_key, ((unsigned long long)md.model << 40) | (1ull << 39) | (unsigned long long)l);
+}
+
+cudaError_t launch_validate(const DevModel* models, int n_local, const uint32_t* lat, const uint64_t* S, int C,
+                            int B, uint64_t smax, unsigned long long* err_key, cudaStream_t s) {
+  if (n_local > 0) validate_kernel<<<n_local * C, 128, 0, s>>>(models, lat, S, C, B, smax, err_key);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // greedy pre-partitioning (§5.2)
 // ---------------------------------------------------------------------------
 // One warp per model: prefix sums T of the reference runtimes, then per block the

@@ -240,3 +240,38 @@ def test_errors_on_device():
         assert e.value.code == -2
     finally:
         pp.free(ctx)
+
+
+def test_update_profiles_validates_on_device(oracle_built):
+    """ppipe_update_profiles checks the int32 envelope on the GPU after the copy; the
+    error names the same item as the host check of ppipe_load_profiles, the context
+    refuses to enumerate until a good update, and then computes the right result."""
+    w = config3()
+    lat = [m.lat_us.copy() for m in w.models]
+    S = [m.act_bytes.copy() for m in w.models]
+    ctx = pp.load_workload(w)
+    try:
+        bad = [x.copy() for x in lat]
+        bad[5][2, :, 7] = (1 << 28) // bad[5].shape[1] + 1  # class 2, batch index 7 of model 5
+        bad[9][1, :, 3] = (1 << 28) // bad[9].shape[1] + 1
+        with pytest.raises(pp.PPipeError) as e:
+            pp.update_profiles(ctx, bad, S)
+        assert e.value.code == -2
+        assert f"model 5 class 2 batch {int(w.batches[7])}: whole-model latency" in str(e.value)
+        with pytest.raises(pp.PPipeError) as e2:
+            ppl = pp.load_profiles(bad, S, w.n_classes, w.batches, w.bw)  # host check, same message
+            pp.free(ppl)
+        assert str(e2.value).split(": ", 1)[-1] == str(e.value).split(": ", 1)[-1]
+        with pytest.raises(pp.PPipeError) as e3:
+            pp.enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
+        assert e3.value.code == -6
+        badS = [x.copy() for x in S]
+        badS[4][3] = np.uint64(1 << 62)
+        with pytest.raises(pp.PPipeError) as e4:
+            pp.update_profiles(ctx, lat, badS)
+        assert "model 4 layer 3: act_bytes" in str(e4.value)
+        pp.update_profiles(ctx, lat, S)
+        pp.enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
+        assert_same_result(pp.pareto(ctx), run_oracle(w), "after a good update")
+    finally:
+        pp.free(ctx)
