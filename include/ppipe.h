@@ -117,6 +117,17 @@ typedef struct {
  * succeeds. Invalidates the last ppipe_enumerate. */
 int ppipe_update_profiles(ppipe_ctx *ctx, uint32_t n_models, const ppipe_model *models);
 
+/* Like ppipe_update_profiles, but returns at once after the shape checks: the
+ * next ppipe_enumerate uploads the values itself, in up to 8 chunks of models on a
+ * copy stream, and validates, packs and scores (K = 3 pass 1) each chunk as soon as
+ * it has arrived, so the host -> device copy overlaps the scoring of earlier
+ * chunks. The host buffers must stay valid and unchanged until the next
+ * ppipe_pareto returns. Value errors (the ppipe_load_profiles envelope, same
+ * messages) are returned by that ppipe_pareto (PPIPE_ERANGE; the context then has
+ * no usable profiles until a successful update). Best with page-locked buffers.
+ * Errors here: PPIPE_EINVAL. */
+int ppipe_update_profiles_async(ppipe_ctx *ctx, uint32_t n_models, const ppipe_model *models);
+
 /* Enqueue the whole enumeration on the context's stream: pack (prefix sums,
  * transfer tables, T_eff), then score every candidate of this rank's range and
  * fold feasible ones into per-(segment, batch) survivor sets. Asynchronous;

@@ -21,6 +21,7 @@ from ._binding import (  # noqa: F401
     run,
     set_vgpu,
     update_profiles,
+    update_profiles_async,
     lib,
     LIB_PATH,
 )

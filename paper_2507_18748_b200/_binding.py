@@ -80,6 +80,8 @@ def lib():
         L.ppipe_prepartition.argtypes = [ct.c_uint32, ct.POINTER(_Model), ct.c_uint32, ct.c_uint32, ct.c_uint32,
                                          ct.c_uint32, ct.c_uint32, ct.c_int32, ct.POINTER(ct.c_uint32),
                                          ct.POINTER(ct.c_uint32), ct.POINTER(ct.c_uint64)]
+        L.ppipe_update_profiles_async.restype = ct.c_int
+        L.ppipe_update_profiles_async.argtypes = [ct.c_void_p, ct.c_uint32, ct.POINTER(_Model)]
         L.ppipe_set_vgpu.restype = ct.c_int
         L.ppipe_set_vgpu.argtypes = [ct.c_void_p, ct.POINTER(ct.c_uint8)]
         L.ppipe_frontier_at.restype = ct.c_int
@@ -162,6 +164,15 @@ def update_profiles(ctx: Context, lat_us: Sequence[np.ndarray], act_bytes: Seque
     models, keep = _models_array(lat_us, act_bytes)
     _check(lib().ppipe_update_profiles(ctx.handle, len(lat_us), models), ctx.handle)
     del keep
+
+
+def update_profiles_async(ctx: Context, lat_us: Sequence[np.ndarray], act_bytes: Sequence[np.ndarray]) -> None:
+    """include/ppipe.h ppipe_update_profiles_async: the next enumerate() uploads the
+    values in chunks overlapped with scoring. The arrays must stay alive and unchanged
+    until the next pareto() returns (the context keeps references until then)."""
+    models, keep = _models_array(lat_us, act_bytes)
+    _check(lib().ppipe_update_profiles_async(ctx.handle, len(lat_us), models), ctx.handle)
+    ctx._pending = keep  # keep the buffers alive for the deferred copy
 
 
 def load_profiles(lat_us: Sequence[np.ndarray], act_bytes: Sequence[np.ndarray], n_classes: int,

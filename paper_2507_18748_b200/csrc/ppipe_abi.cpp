@@ -225,6 +225,14 @@ struct ppipe_ctx {
   uint64_t n_seg_total = 0;
   uint64_t surv_cap = 1ull << 22;
   cudaEvent_t ev[8] = {};
+  // ppipe_update_profiles_async: host descriptors whose copy the next enumerate
+  // issues in chunks on cstream, overlapped with scoring earlier chunks
+  static constexpr int kMaxChunks = 8;
+  bool pending_upload = false, check_err = false;
+  std::vector<ppipe_model> pending;
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t cev[kMaxChunks + 1] = {};
+  DevBuf<unsigned long long> d_err;
   float phase_ms[4] = {0, 0, 0, 0};
   uint64_t launches = 0;
   int launches_i = 0;
@@ -297,6 +305,10 @@ void free_ctx(ppipe_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->cstream) cudaStreamDestroy(c->cstream);
+  for (auto& e : c->cev)
+    if (e) cudaEventDestroy(e);
+  c->d_err.release();
   delete c;
 }
 
@@ -574,6 +586,15 @@ PPIPE_API int ppipe_load_profiles(ppipe_ctx** out, uint32_t n_models, const ppip
       fail(c, PPIPE_ECUDA, "cudaEventCreate failed");
       return bail(PPIPE_ECUDA);
     }
+  if (cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking) != cudaSuccess) {
+    fail(c, PPIPE_ECUDA, "cudaStreamCreate failed");
+    return bail(PPIPE_ECUDA);
+  }
+  for (auto& e : c->cev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      fail(c, PPIPE_ECUDA, "cudaEventCreate failed");
+      return bail(PPIPE_ECUDA);
+    }
   if (cudaMallocHost(&c->h_counters, 16 * sizeof(unsigned long long)) != cudaSuccess) {
     fail(c, PPIPE_ENOMEM, "cudaMallocHost failed");
     return bail(PPIPE_ENOMEM);
@@ -668,6 +689,8 @@ PPIPE_API int ppipe_load_profiles(ppipe_ctx** out, uint32_t n_models, const ppip
   return PPIPE_OK;
 }
 
+static int report_validation(ppipe_ctx* c, unsigned long long key, const ppipe_model* models);
+
 PPIPE_API int ppipe_update_profiles(ppipe_ctx* c, uint32_t n_models, const ppipe_model* models) {
   if (!c) return fail(nullptr, PPIPE_EINVAL, "ppipe_update_profiles: NULL ctx");
   if (n_models != c->n_models || !models)
@@ -683,6 +706,7 @@ PPIPE_API int ppipe_update_profiles(ppipe_ctx* c, uint32_t n_models, const ppipe
   c->profiles_ok = false;
   c->enumerated = false;
   c->have_result = false;
+  c->pending_upload = false;  // a synchronous update supersedes a pending asynchronous one
   CU(c, cudaSetDevice(c->device));
   for (size_t i = 0; i < c->local.size(); ++i) {
     const int m = c->local[i];
@@ -714,20 +738,42 @@ PPIPE_API int ppipe_update_profiles(ppipe_ctx* c, uint32_t n_models, const ppipe
     CU(c, cudaMemcpyAsync(&key, c->d_cnt_send.p, 8, cudaMemcpyDeviceToHost, c->stream));
     CU(c, cudaStreamSynchronize(c->stream));
   }
-  if (key != none) {  // same wording as the host check of ppipe_load_profiles
-    const uint32_t m = (uint32_t)(key >> 40), idx = (uint32_t)(key & ((1ull << 39) - 1));
-    if (key & (1ull << 39))
-      return fail(c, PPIPE_ERANGE, "model %u layer %u: act_bytes %llu too large (8*S*b >= 2^63)", m, idx,
-                  (unsigned long long)models[m].act_bytes[idx]);
-    const uint32_t k = idx / c->B, bi = idx % c->B, M = models[m].n_layers;
-    uint64_t tot = 0;
-    for (uint32_t l = 0; l < M; ++l) tot += models[m].lat_us[((size_t)k * M + l) * c->B + bi];
-    return fail(c, PPIPE_ERANGE, "model %u class %u batch %u: whole-model latency %llu us >= 2^28 (int32 envelope)",
-                m, k, c->h_batches[bi], (unsigned long long)tot);
-  }
+  if (key != none) return report_validation(c, key, models);  // same wording as ppipe_load_profiles
+
   c->profiles_ok = true;
   c->enumerated = false;
   return PPIPE_OK;
+}
+
+PPIPE_API int ppipe_update_profiles_async(ppipe_ctx* c, uint32_t n_models, const ppipe_model* models) {
+  if (!c) return fail(nullptr, PPIPE_EINVAL, "ppipe_update_profiles_async: NULL ctx");
+  if (n_models != c->n_models || !models)
+    return fail(c, PPIPE_EINVAL, "ppipe_update_profiles_async: %u models, context has %u", n_models, c->n_models);
+  for (uint32_t m = 0; m < n_models; ++m) {
+    if (models[m].n_layers != c->Ms[m])
+      return fail(c, PPIPE_EINVAL, "model %u: n_layers %u differs from the loaded %u", m, models[m].n_layers,
+                  c->Ms[m]);
+    if (!models[m].lat_us || !models[m].act_bytes) return fail(c, PPIPE_EINVAL, "model %u: NULL profile pointer", m);
+  }
+  c->pending.assign(models, models + n_models);
+  c->pending_upload = true;
+  c->profiles_ok = true;  // values are checked on the device; errors surface in ppipe_pareto
+  c->enumerated = false;
+  c->have_result = false;
+  return PPIPE_OK;
+}
+
+// First failing (model, kind, index) of a device validation key -> the host check's message.
+static int report_validation(ppipe_ctx* c, unsigned long long key, const ppipe_model* models) {
+  const uint32_t m = (uint32_t)(key >> 40), idx = (uint32_t)(key & ((1ull << 39) - 1));
+  if (key & (1ull << 39))
+    return fail(c, PPIPE_ERANGE, "model %u layer %u: act_bytes %llu too large (8*S*b >= 2^63)", m, idx,
+                (unsigned long long)models[m].act_bytes[idx]);
+  const uint32_t k = idx / c->B, bi = idx % c->B, M = models[m].n_layers;
+  uint64_t tot = 0;
+  for (uint32_t l = 0; l < M; ++l) tot += models[m].lat_us[((size_t)k * M + l) * c->B + bi];
+  return fail(c, PPIPE_ERANGE, "model %u class %u batch %u: whole-model latency %llu us >= 2^28 (int32 envelope)", m,
+              k, c->h_batches[bi], (unsigned long long)tot);
 }
 
 static int run_enumerate(ppipe_ctx* c) {
@@ -786,6 +832,53 @@ static int run_enumerate(ppipe_ctx* c) {
   ScoreOut so{c->d_surv.p, c->d_counters.p, (unsigned long long)c->d_surv.n, c->d_hot.p, c->d_hot_tab.p,
               (unsigned long long)c->hot_cap};
   c->launches_i = 0;
+  pb.model_base = 0;
+  pb.n_chunk = pb.n_local;
+  if (c->pending_upload && pb.n_local == 0) c->pending_upload = false;  // nothing of it lives on this rank
+  if (c->pending_upload) {
+    // Chunked pipeline: the copy stream uploads chunk i + 1 while the compute stream
+    // validates, packs and scores (score3a) chunk i; score3b / score12 follow once.
+    const int nch = std::min<int>(ppipe_ctx::kMaxChunks, pb.n_local);
+    CU(c, c->d_err.reserve(1));
+    const unsigned long long none = ~0ull;
+    CU(c, cudaMemcpyAsync(c->d_err.p, &none, 8, cudaMemcpyHostToDevice, c->stream));
+    CU(c, cudaEventRecord(c->cev[ppipe_ctx::kMaxChunks], c->stream));  // earlier readers of the buffers
+    CU(c, cudaStreamWaitEvent(c->cstream, c->cev[ppipe_ctx::kMaxChunks], 0));
+    std::vector<int> lo(nch + 1);
+    for (int ch = 0; ch <= nch; ++ch) lo[ch] = (int)((int64_t)pb.n_local * ch / nch);
+    for (int ch = 0; ch < nch; ++ch) {
+      for (int i = lo[ch]; i < lo[ch + 1]; ++i) {
+        const int m = c->local[i];
+        const DevModel& d = c->h_models[i];
+        CU(c, cudaMemcpyAsync(c->d_lat.p + d.lat_off, c->pending[m].lat_us, sizeof(uint32_t) * c->C * d.M * c->B,
+                              cudaMemcpyHostToDevice, c->cstream));
+        CU(c, cudaMemcpyAsync(c->d_s.p + d.s_off, c->pending[m].act_bytes, sizeof(uint64_t) * d.M,
+                              cudaMemcpyHostToDevice, c->cstream));
+      }
+      CU(c, cudaEventRecord(c->cev[ch], c->cstream));
+    }
+    CU(c, cudaEventRecord(c->ev[0], c->stream));
+    CU(c, cudaMemsetAsync(c->d_counters.p, 0, 16 * sizeof(unsigned long long), c->stream));
+    const uint64_t bmax = c->h_batches[c->B - 1];
+    for (int ch = 0; ch < nch; ++ch) {
+      CU(c, cudaStreamWaitEvent(c->stream, c->cev[ch], 0));
+      pb.model_base = lo[ch];
+      pb.n_chunk = lo[ch + 1] - lo[ch];
+      CU(c, launch_validate(c->d_models.p + lo[ch], pb.n_chunk, c->d_lat.p, c->d_s.p, (int)c->C, (int)c->B,
+                            (uint64_t)INT64_MAX / (8 * bmax), c->d_err.p, c->stream));
+      CU(c, launch_pack(pb, c->stream));
+      CU(c, launch_score_part(pb, so, c->stream, &c->launches_i, 1));
+      c->launches_i += 3;
+    }
+    CU(c, cudaEventRecord(c->ev[1], c->stream));  // phase 0 = upload + pack + score3a, interleaved
+    pb.model_base = 0;
+    pb.n_chunk = pb.n_local;
+    CU(c, launch_score_part(pb, so, c->stream, &c->launches_i, 2));
+    CU(c, cudaEventRecord(c->ev[2], c->stream));
+    c->pending_upload = false;
+    c->check_err = true;
+    return PPIPE_OK;
+  }
   CU(c, cudaEventRecord(c->ev[0], c->stream));
   CU(c, launch_pack(pb, c->stream));
   c->launches_i += pb.n_local ? 2 : 0;
@@ -829,6 +922,26 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
   if (!out) return fail(c, PPIPE_EINVAL, "ppipe_pareto: NULL output");
   if (!c->enumerated) return fail(c, PPIPE_ESTATE, "ppipe_pareto called before ppipe_enumerate");
   CU(c, cudaSetDevice(c->device));
+  if (c->check_err) {  // values uploaded by ppipe_update_profiles_async were validated on the device
+    c->check_err = false;
+    unsigned long long key = ~0ull;
+    if (c->world > 1 && c->comm) {  // every rank fails alike
+      CU(c, c->d_cnt_recv.reserve((size_t)c->world));
+      NC_(c, g_nccl.AllGather(c->d_err.p, c->d_cnt_recv.p, 1, ncclUint64, c->comm, c->stream));
+      std::vector<unsigned long long> keys(c->world);
+      CU(c, cudaMemcpyAsync(keys.data(), c->d_cnt_recv.p, 8 * keys.size(), cudaMemcpyDeviceToHost, c->stream));
+      CU(c, cudaStreamSynchronize(c->stream));
+      for (auto k : keys) key = std::min(key, k);
+    } else {
+      CU(c, cudaMemcpyAsync(&key, c->d_err.p, 8, cudaMemcpyDeviceToHost, c->stream));
+      CU(c, cudaStreamSynchronize(c->stream));
+    }
+    if (key != ~0ull) {
+      c->profiles_ok = false;
+      c->enumerated = false;
+      return report_validation(c, key, c->pending.data());
+    }
+  }
   // survivors; grow and re-run on overflow (deterministic, so the result is unchanged)
   for (;;) {
     CU(c, cudaMemcpyAsync(c->h_counters, c->d_counters.p, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,

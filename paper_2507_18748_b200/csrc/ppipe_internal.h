@@ -39,6 +39,7 @@ struct Problem {
   const uint8_t* pair_v;     // [C][C] -> index into bw_v (device)
   DevModel* models;          // [n_local] (device)
   int n_local;
+  int model_base, n_chunk;    // pack / score3a launches cover local models [base, base + n_chunk)
   const uint32_t* raw_lat;   // device
   const uint64_t* raw_s;     // device
   int32_t* P;                // device
@@ -67,6 +68,9 @@ size_t hot_unit_table_bytes(const Problem& pb);
 // Launchers (stream-ordered). Return cudaError_t of the launch.
 cudaError_t launch_pack(const Problem& pb, cudaStream_t s);
 cudaError_t launch_score(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches);
+// The same work in parts: score3a over the chunk [model_base, model_base + n_chunk)
+// (part 1), then score3b and score12 over all local models (part 2).
+cudaError_t launch_score_part(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches, int part);
 
 // Frontier pass over n records: sort by (segment, E), per-(segment, E) best,
 // strict staircase over theta, compaction. seg_base_by_model gives each model's

@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(256) pack_p_kernel(Problem pb, int n_btiles) {
   __shared__ int32_t carry[kPackBT];
   const int bt = blockIdx.x % n_btiles;
   const int k = (blockIdx.x / n_btiles) % pb.C;
-  const int ml = blockIdx.x / (n_btiles * pb.C);
+  const int ml = pb.model_base + blockIdx.x / (n_btiles * pb.C);
   DevModel* mdp = &pb.models[ml];
   const uint32_t M = mdp->M, Mp = mdp->Mp;
   const int B = pb.B;
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(256) pack_p_kernel(Problem pb, int n_btiles) {
 __global__ void __launch_bounds__(256) pack_y_kernel(Problem pb) {
   const int bi = blockIdx.x % pb.B;
   const int v = (blockIdx.x / pb.B) % pb.V;
-  const int ml = blockIdx.x / (pb.B * pb.V);
+  const int ml = pb.model_base + blockIdx.x / (pb.B * pb.V);
   const DevModel md = pb.models[ml];
   const uint64_t b = pb.batches[bi];
   const uint64_t bw = pb.bw_v[v];
@@ -126,12 +126,12 @@ __global__ void __launch_bounds__(256) pack_y_kernel(Problem pb) {
 }
 
 cudaError_t launch_pack(const Problem& pb, cudaStream_t s) {
-  if (pb.n_local == 0) return cudaSuccess;
+  if (pb.n_chunk == 0) return cudaSuccess;
   const int n_btiles = (pb.B + kPackBT - 1) / kPackBT;
-  pack_p_kernel<<<pb.n_local * pb.C * n_btiles, 256, 0, s>>>(pb, n_btiles);
+  pack_p_kernel<<<pb.n_chunk * pb.C * n_btiles, 256, 0, s>>>(pb, n_btiles);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  pack_y_kernel<<<pb.n_local * pb.V * pb.B, 256, 0, s>>>(pb);
+  pack_y_kernel<<<pb.n_chunk * pb.V * pb.B, 256, 0, s>>>(pb);
   return cudaGetLastError();
 }
 
@@ -1019,8 +1019,8 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ntab = NC * (nb + 2);
   const int k2 = blockIdx.x % NC;
-  const int ml = (blockIdx.x / NC) % pb.n_local;
-  const int bi = blockIdx.x / (NC * pb.n_local);
+  const int ml = pb.model_base + (blockIdx.x / NC) % pb.n_chunk;
+  const int bi = blockIdx.x / (NC * pb.n_chunk);
   const DevModel md = pb.models[ml];
   CtaCtx<NC> cx;
   make_ctx<NC, W>(cx, pb, md, k2, bi, nb);
@@ -1121,13 +1121,14 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
 constexpr size_t kSmemBudget = 32 * 1024;  // sized for the pass-2 kernel (7 CTAs per SM)
 
 template <int NC, bool W>
-static cudaError_t launch_score_w(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches) {
+static cudaError_t launch_score_w(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches,
+                                  int part) {
   const int row_len = (int)((((size_t)pb.max_M + 3) & ~(size_t)3) + 8 * kScanUnroll);
   int nb_log2 = 7;
   while (nb_log2 < 11 && table_policy_bytes<NC>(2 << nb_log2, row_len) <= kSmemBudget) ++nb_log2;
   const size_t smem = score_smem_bytes<NC>(1 << nb_log2, row_len);
   const size_t smem_a = score_smem_bytes<NC>(1 << nb_log2, row_len, false);
-  const unsigned grid = (unsigned)pb.n_local * NC * pb.B;
+  const unsigned grid = (unsigned)pb.n_chunk * NC * pb.B;
   cudaError_t e;
   // K <= 2 tables live only inside score12 (never in the hot-unit buffer), so their
   // resolution may differ from the K = 3 tables.
@@ -1139,15 +1140,20 @@ static cudaError_t launch_score_w(const Problem& pb, const ScoreOut& out, cudaSt
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(score3b_kernel<NC, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (pb.Kmax >= 3) {
+  // part 0: everything; 1: score3a over the chunk; 2: score3b + score12 over all local models
+  if (pb.Kmax >= 3 && part != 2 && pb.n_chunk > 0) {
     score3a_kernel<NC, W><<<grid, 32 * kWarps, smem_a, s>>>(pb, out, nb_log2, row_len);
+    ++*n_launches;
+  }
+  if (part == 1) return cudaGetLastError();
+  if (pb.Kmax >= 3) {
     int dev = 0, n_sm = 148, smem_sm = 227 * 1024;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     const int ctas = std::max(1, std::min(k3bCtasPerSm, smem_sm / (int)(smem + 1024)));  // persistent: fill the SMs
     score3b_kernel<NC, W><<<n_sm * ctas, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
-    *n_launches += 2;
+    ++*n_launches;
   }
   score12_kernel<NC, W><<<(unsigned)pb.n_local * NC * pb.B, 32 * kWarps, smem12, s>>>(pb, out, nb12_log2);
   ++*n_launches;
@@ -1155,9 +1161,10 @@ static cudaError_t launch_score_w(const Problem& pb, const ScoreOut& out, cudaSt
 }
 
 template <int NC>
-static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches) {
-  return pb.wpack == 0x11111111u ? launch_score_w<NC, false>(pb, out, s, n_launches)
-                                 : launch_score_w<NC, true>(pb, out, s, n_launches);
+static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches,
+                                  int part) {
+  return pb.wpack == 0x11111111u ? launch_score_w<NC, false>(pb, out, s, n_launches, part)
+                                 : launch_score_w<NC, true>(pb, out, s, n_launches, part);
 }
 
 // Bytes of one hot unit's tables for this problem (the ABI sizes its buffer with it).
@@ -1180,19 +1187,23 @@ size_t hot_unit_table_bytes(const Problem& pb) {
   return 8 * (size_t)pb.C * ((1 << nb_log2) + 2);
 }
 
-cudaError_t launch_score(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches) {
+cudaError_t launch_score_part(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches, int part) {
   if (pb.n_local == 0) return cudaSuccess;
   switch (pb.C) {
-    case 1: return launch_score_nc<1>(pb, out, s, n_launches);
-    case 2: return launch_score_nc<2>(pb, out, s, n_launches);
-    case 3: return launch_score_nc<3>(pb, out, s, n_launches);
-    case 4: return launch_score_nc<4>(pb, out, s, n_launches);
-    case 5: return launch_score_nc<5>(pb, out, s, n_launches);
-    case 6: return launch_score_nc<6>(pb, out, s, n_launches);
-    case 7: return launch_score_nc<7>(pb, out, s, n_launches);
-    case 8: return launch_score_nc<8>(pb, out, s, n_launches);
+    case 1: return launch_score_nc<1>(pb, out, s, n_launches, part);
+    case 2: return launch_score_nc<2>(pb, out, s, n_launches, part);
+    case 3: return launch_score_nc<3>(pb, out, s, n_launches, part);
+    case 4: return launch_score_nc<4>(pb, out, s, n_launches, part);
+    case 5: return launch_score_nc<5>(pb, out, s, n_launches, part);
+    case 6: return launch_score_nc<6>(pb, out, s, n_launches, part);
+    case 7: return launch_score_nc<7>(pb, out, s, n_launches, part);
+    case 8: return launch_score_nc<8>(pb, out, s, n_launches, part);
     default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t launch_score(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches) {
+  return launch_score_part(pb, out, s, n_launches, 0);
 }
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,73 @@
+"""ppipe_update_profiles_async: the upload happens inside the next enumerate, in
+chunks overlapped with scoring (include/ppipe.h). Same bar as the main path:
+bit-exact against the oracle / a fresh synchronous run."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2507_18748_b200 as pp
+from oracle import run_oracle
+from tests.helpers import assert_same_result
+from workloads import config3, config5
+
+pytestmark = pytest.mark.gpu
+
+
+def _scaled(w, f):
+    return [np.minimum(m.lat_us.astype(np.uint64) * f // 4, 1 << 20).astype(np.uint32) for m in w.models]
+
+
+def test_async_upload_replaces_the_loaded_values(oracle_built):
+    w = config3()
+    ctx = pp.load_profiles(_scaled(w, 7), [m.act_bytes for m in w.models], w.n_classes, w.batches, w.bw)
+    try:
+        pp.update_profiles_async(ctx, [m.lat_us for m in w.models], [m.act_bytes for m in w.models])
+        pp.enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
+        assert_same_result(pp.pareto(ctx), run_oracle(w), "config 3 after async upload")
+        # the uploaded values stay: a second enumerate needs no new upload
+        pp.enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
+        assert_same_result(pp.pareto(ctx), run_oracle(w), "config 3 again")
+    finally:
+        pp.free(ctx)
+
+
+def test_async_upload_chunks_config5_slice():
+    w = config5(n_models=24)  # 8 chunks of 3 models
+    ref = pp.run(w)
+    ctx = pp.load_profiles(_scaled(w, 3), [m.act_bytes for m in w.models], w.n_classes, w.batches, w.bw)
+    try:
+        pp.update_profiles_async(ctx, [m.lat_us for m in w.models], [m.act_bytes for m in w.models])
+        pp.enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
+        g = pp.pareto(ctx)
+        assert g.n_candidates == ref.n_candidates and g.n_feasible == ref.n_feasible
+        assert np.array_equal(g.points.view(np.uint8), ref.points.view(np.uint8))
+        assert np.array_equal(g.seg_offsets, ref.seg_offsets)
+    finally:
+        pp.free(ctx)
+
+
+def test_async_upload_errors_surface_in_pareto(oracle_built):
+    w = config3()
+    lat = [m.lat_us.copy() for m in w.models]
+    S = [m.act_bytes.copy() for m in w.models]
+    bad = [x.copy() for x in lat]
+    bad[11][3, :, 2] = (1 << 28) // bad[11].shape[1] + 1
+    ctx = pp.load_workload(w)
+    try:
+        pp.update_profiles_async(ctx, bad, S)
+        pp.enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
+        with pytest.raises(pp.PPipeError) as e:
+            pp.pareto(ctx)
+        assert e.value.code == -2
+        assert f"model 11 class 3 batch {int(w.batches[2])}: whole-model latency" in str(e.value)
+        with pytest.raises(pp.PPipeError) as e2:
+            pp.enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
+        assert e2.value.code == -6
+        # a synchronous update after a pending asynchronous one wins
+        pp.update_profiles_async(ctx, bad, S)
+        pp.update_profiles(ctx, lat, S)
+        pp.enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
+        assert_same_result(pp.pareto(ctx), run_oracle(w), "recovered")
+    finally:
+        pp.free(ctx)
