@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--models", type=int, default=None)
     ap.add_argument("--oracle", action="store_true", help="also compare with the CPU oracle (small configs)")
+    ap.add_argument("--vgpu", type=str, default=None, help="comma-separated per-class virtual-GPU counts")
+    ap.add_argument("--async-upload", action="store_true", help="load scaled values, then update_profiles_async")
     args = ap.parse_args()
 
     import numpy as np
@@ -47,7 +49,21 @@ def main():
         t.copy_(torch.frombuffer(bytearray(pp.nccl_unique_id()), dtype=torch.uint8))
     dist.broadcast(t, 0)
     nid = bytes(t.cpu().numpy().tobytes())
-    g = pp.run(w, rank=rank, world=world, device=local, nccl_id=nid)
+    vgpu = [int(x) for x in args.vgpu.split(",")] if args.vgpu else None
+    if args.async_upload:
+        scaled = [np.minimum(m.lat_us.astype(np.uint64) * 5 // 4, 1 << 20).astype(np.uint32) for m in w.models]
+        ctx = pp.load_profiles(scaled, [m.act_bytes for m in w.models], w.n_classes, w.batches, w.bw, rank=rank,
+                               world=world, device=local, nccl_id=nid)
+        try:
+            if vgpu:
+                pp.set_vgpu(ctx, vgpu)
+            pp.update_profiles_async(ctx, [m.lat_us for m in w.models], [m.act_bytes for m in w.models])
+            pp.enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
+            g = pp.pareto(ctx)
+        finally:
+            pp.free(ctx)
+    else:
+        g = pp.run(w, rank=rank, world=world, device=local, nccl_id=nid, vgpu=vgpu)
     digest = hashlib.sha256(g.points.tobytes() + g.seg_offsets.tobytes()).hexdigest()
     digests = [None] * world
     dist.all_gather_object(digests, (digest, g.n_candidates, g.n_feasible, g.n_points))
@@ -56,7 +72,7 @@ def main():
         if len(set(digests)) != 1:
             print("ranks disagree:", digests)
             ok = False
-        single = pp.run(w, device=local)
+        single = pp.run(w, device=local, vgpu=vgpu)
         if not (np.array_equal(single.points.view(np.uint8), g.points.view(np.uint8))
                 and np.array_equal(single.seg_offsets, g.seg_offsets)
                 and single.n_candidates == g.n_candidates and single.n_feasible == g.n_feasible):
@@ -65,7 +81,7 @@ def main():
             ok = False
         if args.oracle:
             from oracle import run_oracle
-            o = run_oracle(w)
+            o = run_oracle(w, vgpu=vgpu)
             if not (np.array_equal(o.points.view(np.uint8), g.points.view(np.uint8))
                     and o.n_candidates == g.n_candidates and o.n_feasible == g.n_feasible):
                 print("multi-GPU result differs from the oracle")
