@@ -63,6 +63,7 @@ def _load():
         lib.oracle_result_free.argtypes = [ct.POINTER(_Result)]
         lib.oracle_set_threads.argtypes = [ct.c_int]
         lib.oracle_set_vgpu.argtypes = [ct.POINTER(ct.c_uint8), ct.c_uint32]
+        lib.oracle_set_frontier.argtypes = [ct.c_int]
         lib.oracle_prepartition.restype = ct.c_int
         lib.oracle_prepartition.argtypes = [ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.POINTER(ct.c_uint32),
                                             ct.POINTER(ct.c_uint64), ct.c_uint32, ct.c_uint32, ct.c_uint32,
@@ -88,11 +89,14 @@ def run_oracle(w, model_lo: int = 0, model_hi: Optional[int] = None, only_K: int
                only_cls: Optional[Sequence[int]] = None, row_lo: int = 0, row_hi: int = 0,
                threads: int = 0, slo_us: Optional[np.ndarray] = None,
                margin_permille: Optional[int] = None, kmax: Optional[int] = None,
-               vgpu: Optional[Sequence[int]] = None) -> OracleResult:
+               vgpu: Optional[Sequence[int]] = None, frontier: int = 1) -> OracleResult:
     """Run the oracle on a workloads.Workload (or a sub-range of its models).
-    vgpu: per-class virtual-GPU count v_k (theta = min_d v_d b / C_d); None = all 1."""
+    vgpu: per-class virtual-GPU count v_k (theta = min_d v_d b / C_d); None = all 1.
+    frontier: 1 = the (E, theta) staircase, 2 = F2, the MILP-lossless per-stage
+    throughput frontier (ppipe_oracle.c, f2_beats)."""
     lib = _load()
     lib.oracle_set_threads(int(threads))
+    lib.oracle_set_frontier(int(frontier))
     if vgpu is not None:
         varr = (ct.c_uint8 * w.n_classes)(*[int(v) for v in vgpu])
         lib.oracle_set_vgpu(varr, w.n_classes)

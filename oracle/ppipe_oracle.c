@@ -42,7 +42,11 @@
  * min-max partition P7, and the literal O(n^2) Pareto definition P8);
  * oracle_prepartition (end of file) by tests/test_prepartition_pins.py (the
  * SPEC.md examples, closed forms for N = 1, N = M and uniform layers, and the
- * half-layer balance bound that the greedy stopping rule implies).
+ * half-layer balance bound that the greedy stopping rule implies); the F2
+ * reduction (oracle_set_frontier(2), below) by tests/test_f2_pins.py (an
+ * independent Fraction-based literal definition on random tiny inputs, a
+ * hand-worked fixture, the K = 1 closed form, the single-batch all-kept case and
+ * the MILP-losslessness property).
  */
 #define _GNU_SOURCE
 #include <pthread.h>
@@ -145,6 +149,90 @@ static int cand_cmp(const void *pa, const void *pb) {
   if (p->c1 != q->c1) return p->c1 < q->c1 ? -1 : 1;
   if (p->c2 != q->c2) return p->c2 < q->c2 ? -1 : 1;
   return 0;
+}
+
+/*
+ * F2, the MILP-lossless frontier (DESIGN.md §3 readings
+ * F2-1..F2-4). PPipe's MILP gives a chosen pipeline g_d GPUs in stage d and its
+ * throughput is x_l = min_d g_d * X_d with X_d = b / C_d the per-GPU throughput of
+ * stage d (eqs. 1.10, 1.13); E only has to meet the SLO
+ * (eq. 1.12). So per segment the objective is the per-stage vector
+ * x = (X_1, .., X_K) (with virtual GPUs X_d = v_{k_d} b / C_d),
+ * and a feasible candidate q makes p redundant iff x_q >= x_p in every stage and
+ * either x_q != x_p (strict Pareto dominance) or x_q == x_p and q comes first in
+ * (E, b, c_1, c_2) ascending (E is the tie-break only). Kept points are listed in
+ * (b, c_1, c_2) ascending order. Below is that definition as written: every pair.
+ */
+static int g_frontier = 1; /* 1 = (E, theta) staircase (A1), 2 = F2 */
+
+void oracle_set_frontier(int kind) { g_frontier = kind == 2 ? 2 : 1; }
+
+/* q makes p redundant under F2 (see above). X_q,d >= X_p,d  <=>  v b_q C_p,d >= v b_p C_q,d
+ * (C = 0 reads as +inf: two +inf are equal). */
+static int f2_beats(const cand *q, const cand *p, int K, const int *cls) {
+  int all_eq = 1;
+  for (int d = 0; d < K; d++) {
+    const int64_t v = vgpu_of(cls[d]);
+    const int64_t lhs = v * q->b * p->st[d], rhs = v * p->b * q->st[d];
+    if (lhs < rhs) return 0;
+    if (lhs != rhs) all_eq = 0;
+  }
+  if (!all_eq) return 1;
+  if (q->E != p->E) return q->E < p->E;
+  if (q->b != p->b) return q->b < p->b;
+  if (q->c1 != p->c1) return q->c1 < p->c1;
+  return q->c2 < p->c2; /* p itself: not redundant */
+}
+
+static int f2_out_cmp(const void *pa, const void *pb) {
+  const cand *p = (const cand *)pa, *q = (const cand *)pb;
+  if (p->b != q->b) return p->b < q->b ? -1 : 1;
+  if (p->c1 != q->c1) return p->c1 < q->c1 ? -1 : 1;
+  if (p->c2 != q->c2) return p->c2 < q->c2 ? -1 : 1;
+  return 0;
+}
+
+typedef struct {
+  const cand *v;
+  size_t n;
+  int K;
+  const int *cls;
+  uint8_t *keep;
+  int t, nt;
+} f2_job;
+
+static void *f2_worker(void *arg) {
+  f2_job *j = (f2_job *)arg;
+  for (size_t i = (size_t)j->t; i < j->n; i += (size_t)j->nt) {
+    int redundant = 0;
+    for (size_t q = 0; q < j->n && !redundant; q++) redundant = f2_beats(&j->v[q], &j->v[i], j->K, j->cls);
+    j->keep[i] = (uint8_t)!redundant;
+  }
+  return NULL;
+}
+
+/* F2 reduction of one segment's feasible candidates, in place: returns the kept count,
+ * kept points first, in (b, c_1, c_2) order. */
+static size_t f2_reduce(cand *v, size_t n, int K, const int *cls, int nthreads) {
+  if (!n) return 0;
+  uint8_t *keep = (uint8_t *)calloc(n, 1);
+  int nt = nthreads;
+  if ((size_t)nt > n) nt = (int)n;
+  f2_job *jobs = (f2_job *)calloc((size_t)nt, sizeof(f2_job));
+  pthread_t *th = (pthread_t *)calloc((size_t)nt, sizeof(pthread_t));
+  for (int t = 0; t < nt; t++) {
+    jobs[t] = (f2_job){v, n, K, cls, keep, t, nt};
+    pthread_create(&th[t], NULL, f2_worker, &jobs[t]);
+  }
+  for (int t = 0; t < nt; t++) pthread_join(th[t], NULL);
+  size_t k = 0;
+  for (size_t i = 0; i < n; i++)
+    if (keep[i]) v[k++] = v[i];
+  qsort(v, k, sizeof(cand), f2_out_cmp);
+  free(keep);
+  free(jobs);
+  free(th);
+  return k;
 }
 
 /* ---- problem description shared by the worker threads ---- */
@@ -413,15 +501,22 @@ int oracle_run(uint32_t n_models, const oracle_model *models, uint32_t n_classes
             t /= C;
           }
         }
-        if (all.n) qsort(all.v, all.n, sizeof(cand), cand_cmp);
+        size_t n_out = all.n;
+        if (g_frontier == 2) {
+          n_out = f2_reduce(all.v, all.n, (int)K, g_sort_cls, nthreads);
+        } else if (all.n) {
+          qsort(all.v, all.n, sizeof(cand), cand_cmp);
+        }
         int64_t best_n = 0, best_d = 1; /* theta = 0 */
-        for (size_t i = 0; i < all.n; i++) {
+        for (size_t i = 0; i < n_out; i++) {
           const cand *p = &all.v[i];
-          int64_t tn, td;
-          theta_of(p, (int)K, g_sort_cls, &tn, &td);
-          if (!theta_gt(tn, td, best_n, best_d)) continue; /* keep iff theta > best (strict) */
-          best_n = tn;
-          best_d = td;
+          if (g_frontier != 2) {
+            int64_t tn, td;
+            theta_of(p, (int)K, g_sort_cls, &tn, &td);
+            if (!theta_gt(tn, td, best_n, best_d)) continue; /* keep iff theta > best (strict) */
+            best_n = tn;
+            best_d = td;
+          }
           if (res->n_pts == cap_pts) {
             cap_pts = cap_pts ? cap_pts * 2 : 1024;
             res->pts = (oracle_point *)realloc(res->pts, cap_pts * sizeof(oracle_point));

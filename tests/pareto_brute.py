@@ -7,6 +7,7 @@ literal O(n^2) non-domination test (SURVEY.md §8(c) pin P8), not a sort+scan.
 from __future__ import annotations
 
 import itertools
+import math
 from fractions import Fraction
 
 import numpy as np
@@ -101,4 +102,62 @@ def literal_frontier_np(cands):
         if not dom.any():
             keep.append(cands[i])
     keep.sort(key=lambda c: c["E"])
+    return keep
+
+
+# ---------------- F2: the MILP-lossless per-stage frontier ----------------
+
+def stage_vector(c, cls, vgpu=None):
+    """x = (X_1, .., X_K), X_d = v_{k_d} b / C_d as exact Fractions (per-GPU throughput of
+    stage d, PAPER.md:2245 X_{ldbij} = b / C; virtual GPUs PAPER.md:1107-1126); C_d = 0 is +inf."""
+    out = []
+    for d, C in enumerate(c["stages"]):
+        v = 1 if vgpu is None else int(vgpu[cls[d]])
+        out.append(Fraction(v * c["b"], C) if C > 0 else math.inf)
+    return tuple(out)
+
+
+def literal_f2(cands, cls, vgpu=None):
+    """Keep p iff no feasible q of the segment has x_q >= x_p in every stage and either
+    x_q != x_p, or x_q == x_p and (E, b, cuts)_q < (E, b, cuts)_p. Output in (b, cuts) order."""
+    xs = [stage_vector(c, cls, vgpu) for c in cands]
+    keep = []
+    for i, p in enumerate(cands):
+        redundant = False
+        for j, q in enumerate(cands):
+            if j == i:
+                continue
+            if all(a >= b for a, b in zip(xs[j], xs[i])):
+                if xs[j] != xs[i] or (q["E"], q["b"], q["cuts"]) < (p["E"], p["b"], p["cuts"]):
+                    redundant = True
+                    break
+        if not redundant:
+            keep.append(p)
+    keep.sort(key=lambda c: (c["b"], c["cuts"]))
+    return keep
+
+
+def literal_f2_np(cands, cls, vgpu=None):
+    """literal_f2 vectorised with numpy (integer cross-multiplication: X_q,d >= X_p,d iff
+    v b_q C_p,d >= v b_p C_q,d; C = 0 is +inf on both sides)."""
+    if not cands:
+        return []
+    K = len(cands[0]["stages"])
+    v = np.array([1 if vgpu is None else int(vgpu[cls[d]]) for d in range(K)], dtype=np.int64)
+    b = np.array([c["b"] for c in cands], dtype=np.int64)
+    st = np.array([c["stages"] for c in cands], dtype=np.int64)
+    E = np.array([c["E"] for c in cands], dtype=np.int64)
+    rank = np.array([(c["b"] << 32) | (c["cuts"][0] << 16) | c["cuts"][1] for c in cands], dtype=np.int64)
+    keep = []
+    for i in range(len(cands)):
+        lhs = v * b[:, None] * st[i][None, :]   # v b_q C_p
+        rhs = v * b[i] * st                      # v b_p C_q
+        ge = (lhs >= rhs).all(axis=1)
+        eq = (lhs == rhs).all(axis=1)
+        tie_better = (E < E[i]) | ((E == E[i]) & (rank < rank[i]))
+        red = ge & (~eq | tie_better)
+        red[i] = False
+        if not red.any():
+            keep.append(cands[i])
+    keep.sort(key=lambda c: (c["b"], c["cuts"]))
     return keep
