@@ -168,6 +168,33 @@ typedef struct {
  * done. Errors: PPIPE_ESTATE (no prior ppipe_enumerate), PPIPE_ECUDA, PPIPE_ENCCL. */
 int ppipe_pareto(ppipe_ctx *ctx, int copy_to_host, ppipe_frontier *out);
 
+/* F2, the MILP-lossless frontier (DESIGN.md §3 F2-1..F2-4).
+ * PPipe's pooled MILP gives a chosen pipeline g_d GPUs in stage d and gets
+ * throughput min_d g_d X_d, X_d = b / C_d the per-GPU throughput of stage d
+ * (eqs. 1.10, 1.13); E only has to meet the SLO
+ * (eq. 1.12). The (E, theta) frontier of ppipe_pareto can drop a
+ * candidate the MILP needs for some g; F2 keeps, per segment, every feasible
+ * candidate whose vector x = (X_1 .. X_K) no other feasible candidate of the segment
+ * matches or beats in every stage (x_q >= x_p componentwise with x_q != x_p), and of
+ * several with an identical vector the smallest (E, b, c_1, c_2). Virtual-GPU
+ * weights scale a stage of every candidate alike and do not change F2.
+ * One blocking call: pack, enumerate every candidate of params (as ppipe_enumerate),
+ * reduce, and (world > 1 with NCCL) all-gather the per-rank frontiers; each model is
+ * computed whole by the rank holding its K = 1 row (ppipe_partition_rows row 0), so
+ * in shard mode a rank returns the F2 points of those models only.
+ * out: as ppipe_pareto, except that points are ordered by (segment, b, c_1, c_2)
+ * and n_survivors counts the candidates left after the strict-dominance pass
+ * (before equal vectors are resolved). The result shares ppipe_pareto's buffers
+ * (it invalidates the last ppipe_enumerate / ppipe_pareto) and cannot be swept by
+ * ppipe_frontier_at (F2 frontiers are not SLO prefixes).
+ * Device memory: K = 3 keeps a table of (M - 2)^2 int32 per (segment, batch) for a
+ * group of segments at a time, at most PPIPE_F2_G_BYTES (environment; default
+ * 8 GiB) or one segment's worth if that is larger.
+ * Errors: as ppipe_enumerate; PPIPE_ERANGE for a model with more than 4096 layers;
+ * PPIPE_ESTATE after ppipe_update_profiles_async (use ppipe_update_profiles);
+ * PPIPE_ENOMEM, PPIPE_ECUDA, PPIPE_ENCCL. */
+int ppipe_pareto_f2(ppipe_ctx *ctx, const ppipe_enum_params *params, int copy_to_host, ppipe_frontier *out);
+
 /* Virtual GPUs (§5.1; App. A.2 L_{kvbi}): declare
  * class k a pseudo-class that runs on 1/vgpu[k] of a physical GPU (MPS), vgpu[k] in
  * 1..4 (NULL = all 1, the default). Its profile is the caller's lat_us for that

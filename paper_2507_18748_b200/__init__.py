@@ -16,6 +16,7 @@ from ._binding import (  # noqa: F401
     load_workload,
     nccl_unique_id,
     pareto,
+    pareto_f2,
     partition_rows,
     prepartition,
     run,

@@ -84,6 +84,8 @@ def lib():
         L.ppipe_update_profiles_async.argtypes = [ct.c_void_p, ct.c_uint32, ct.POINTER(_Model)]
         L.ppipe_set_vgpu.restype = ct.c_int
         L.ppipe_set_vgpu.argtypes = [ct.c_void_p, ct.POINTER(ct.c_uint8)]
+        L.ppipe_pareto_f2.restype = ct.c_int
+        L.ppipe_pareto_f2.argtypes = [ct.c_void_p, ct.POINTER(_EnumParams), ct.c_int, ct.POINTER(_Frontier)]
         L.ppipe_frontier_at.restype = ct.c_int
         L.ppipe_frontier_at.argtypes = [ct.c_void_p, ct.POINTER(ct.c_uint32), ct.c_uint32, ct.c_int,
                                         ct.POINTER(_Frontier)]
@@ -248,6 +250,20 @@ def pareto(ctx: Context, copy_to_host: bool = True, zero_copy: bool = False) -> 
     return _frontier_from(f, copy_to_host, zero_copy)
 
 
+def pareto_f2(ctx: Context, max_partitions: int, slo_us: np.ndarray, margin_permille: int,
+              copy_to_host: bool = True, zero_copy: bool = False) -> Frontier:
+    """F2, the MILP-lossless per-stage throughput frontier (include/ppipe.h
+    ppipe_pareto_f2): pack, enumerate and reduce in one blocking call; points in
+    (segment, b, c_1, c_2) order."""
+    slo = np.ascontiguousarray(slo_us, dtype=np.uint32)
+    if slo.shape[0] != ctx.n_models:
+        raise PPipeError(PPIPE_EINVAL, f"slo_us has {slo.shape[0]} entries for {ctx.n_models} models")
+    p = _EnumParams(max_partitions, _u32p(slo), margin_permille)
+    f = _Frontier()
+    _check(lib().ppipe_pareto_f2(ctx.handle, ct.byref(p), 1 if copy_to_host else 0, ct.byref(f)), ctx.handle)
+    return _frontier_from(f, copy_to_host, zero_copy)
+
+
 def frontier_at(ctx: Context, slo_us: np.ndarray, margin_permille: int, copy_to_host: bool = True,
                 zero_copy: bool = False) -> Frontier:
     """The frontier at lower per-model SLOs, truncated from the last pareto() result
@@ -307,12 +323,14 @@ def partition_rows(n_layers: Sequence[int], n_classes: int, n_batches: int, max_
 
 
 def run(w, rank: int = 0, world: int = 1, device: int = -1, nccl_id: Optional[bytes] = None,
-        copy_to_host: bool = True, vgpu: Optional[Sequence[int]] = None) -> Frontier:
-    """One full pass: load, (set_vgpu), enumerate, pareto, free."""
+        copy_to_host: bool = True, vgpu: Optional[Sequence[int]] = None, frontier: int = 1) -> Frontier:
+    """One full pass: load, (set_vgpu), enumerate, pareto, free. frontier=2: F2 (pareto_f2)."""
     ctx = load_workload(w, rank, world, device, nccl_id)
     try:
         if vgpu is not None:
             set_vgpu(ctx, vgpu)
+        if frontier == 2:
+            return pareto_f2(ctx, w.kmax, w.slo_us, w.margin_permille, copy_to_host)
         enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
         return pareto(ctx, copy_to_host)
     finally:

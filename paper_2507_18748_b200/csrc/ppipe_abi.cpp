@@ -233,6 +233,10 @@ struct ppipe_ctx {
   cudaStream_t cstream = nullptr;
   cudaEvent_t cev[kMaxChunks + 1] = {};
   DevBuf<unsigned long long> d_err;
+  // F2 (ppipe_pareto_f2)
+  DevBuf<int32_t> d_G, d_F;
+  DevBuf<ppipe_point> d_f2surv, d_f2tmp;
+  uint64_t f2_cap = 1ull << 20;
   float phase_ms[4] = {0, 0, 0, 0};
   uint64_t launches = 0;
   int launches_i = 0;
@@ -309,6 +313,10 @@ void free_ctx(ppipe_ctx* c) {
   for (auto& e : c->cev)
     if (e) cudaEventDestroy(e);
   c->d_err.release();
+  c->d_G.release();
+  c->d_F.release();
+  c->d_f2surv.release();
+  c->d_f2tmp.release();
   delete c;
 }
 
@@ -776,9 +784,10 @@ static int report_validation(ppipe_ctx* c, unsigned long long key, const ppipe_m
               k, c->h_batches[bi], (unsigned long long)tot);
 }
 
-static int run_enumerate(ppipe_ctx* c) {
+// Segment bases, per-model SLOs and the kernel parameter block for c->last_params
+// (shared by the (E, theta) path and F2).
+static int setup_problem(ppipe_ctx* c, Problem* out) {
   const ppipe_enum_params* p = &c->last_params;
-  CU(c, cudaSetDevice(c->device));
   // global segment bases (all models; same on every rank)
   std::vector<uint64_t> segbase(c->n_models);
   uint64_t acc = 0;
@@ -797,7 +806,6 @@ static int run_enumerate(ppipe_ctx* c) {
   CU(c, cudaMemcpyAsync(c->d_segbase.p, segbase.data(), 8 * segbase.size(), cudaMemcpyHostToDevice, c->stream));
   CU(c, cudaMemcpyAsync(c->d_models.p, c->h_models.data(), sizeof(DevModel) * c->h_models.size(),
                         cudaMemcpyHostToDevice, c->stream));
-  CU(c, c->d_surv.reserve(c->surv_cap));
   Problem pb{};
   pb.C = (int)c->C;
   pb.B = (int)c->B;
@@ -822,6 +830,18 @@ static int run_enumerate(ppipe_ctx* c) {
     const char* dbg = getenv("PPIPE_DEBUG_FLAGS");
     pb.debug_flags = dbg ? atoi(dbg) : 0;
   }
+  pb.model_base = 0;
+  pb.n_chunk = pb.n_local;
+  *out = pb;
+  return PPIPE_OK;
+}
+
+static int run_enumerate(ppipe_ctx* c) {
+  CU(c, cudaSetDevice(c->device));
+  Problem pb{};
+  int rc = setup_problem(c, &pb);
+  if (rc != PPIPE_OK) return rc;
+  CU(c, c->d_surv.reserve(c->surv_cap));
   if (c->hot_cap == 0) {
     const uint64_t units = (uint64_t)c->local.size() * c->C * c->C * c->B;
     c->hot_cap = std::max<uint64_t>(1, std::min<uint64_t>(units, std::max<uint64_t>(4096, units / 8)));
@@ -889,15 +909,14 @@ static int run_enumerate(ppipe_ctx* c) {
   return PPIPE_OK;
 }
 
-PPIPE_API int ppipe_enumerate(ppipe_ctx* ctx, const ppipe_enum_params* p) {
-  if (!ctx) return fail(nullptr, PPIPE_EINVAL, "ppipe_enumerate: NULL ctx");
-  if (!p || !p->slo_us) return fail(ctx, PPIPE_EINVAL, "ppipe_enumerate: NULL params or slo_us");
+static int check_params(ppipe_ctx* ctx, const ppipe_enum_params* p, const char* who) {
+  if (!p || !p->slo_us) return fail(ctx, PPIPE_EINVAL, "%s: NULL params or slo_us", who);
   if (p->max_partitions < 1 || p->max_partitions > 3)
     return fail(ctx, PPIPE_EINVAL, "max_partitions %u: must be 1..3", p->max_partitions);
   if (p->margin_permille >= 1000)
     return fail(ctx, PPIPE_EINVAL, "margin_permille %u: must be < 1000", p->margin_permille);
   if (!ctx->profiles_ok)
-    return fail(ctx, PPIPE_ESTATE, "ppipe_enumerate: the last ppipe_update_profiles failed; profiles are unusable");
+    return fail(ctx, PPIPE_ESTATE, "%s: the last ppipe_update_profiles failed; profiles are unusable", who);
   for (uint32_t m = 0; m < ctx->n_models; ++m) {
     const uint64_t T = (uint64_t)p->slo_us[m] * (1000 - p->margin_permille) / 1000;
     if (T >= (uint64_t)kRangeLimit)
@@ -907,6 +926,13 @@ PPIPE_API int ppipe_enumerate(ppipe_ctx* ctx, const ppipe_enum_params* p) {
       return fail(ctx, PPIPE_ERANGE, "model %u: T_eff %llu us x virtual-GPU weight %u >= 2^31 (int32 envelope)", m,
                   (unsigned long long)T, ctx->w_max);
   }
+  return PPIPE_OK;
+}
+
+PPIPE_API int ppipe_enumerate(ppipe_ctx* ctx, const ppipe_enum_params* p) {
+  if (!ctx) return fail(nullptr, PPIPE_EINVAL, "ppipe_enumerate: NULL ctx");
+  int rc0 = check_params(ctx, p, "ppipe_enumerate");
+  if (rc0 != PPIPE_OK) return rc0;
   ctx->have_result = false;
   ctx->last_params = *p;
   ctx->last_slo.assign(p->slo_us, p->slo_us + ctx->n_models);
@@ -1128,6 +1154,164 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
   c->res_off = d_off;
   c->res_n = n_pts;
   c->res_ncand = n_cand;
+  if (copy_to_host) {
+    CU(c, c->h_points.reserve(n_pts));
+    CU(c, c->h_segoff.reserve(c->n_seg_total + 1));
+    if (n_pts)
+      CU(c, cudaMemcpyAsync(c->h_points.p, d_pts, sizeof(ppipe_point) * n_pts, cudaMemcpyDeviceToHost, c->stream));
+    CU(c, cudaMemcpyAsync(c->h_segoff.p, d_off, 8 * (c->n_seg_total + 1), cudaMemcpyDeviceToHost, c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
+    out->points = c->h_points.p;
+    out->seg_offsets = c->h_segoff.p;
+  }
+  return PPIPE_OK;
+}
+
+// F2: the MILP-lossless frontier (include/ppipe.h; ppipe_f2.cu). Every model is
+// scored whole by the rank that holds its row 0 (its K = 1 row), so each rank's
+// frontier is final for its models and the global one is the rank-ordered
+// concatenation.
+PPIPE_API int ppipe_pareto_f2(ppipe_ctx* c, const ppipe_enum_params* p, int copy_to_host, ppipe_frontier* out) {
+  if (!c) return fail(nullptr, PPIPE_EINVAL, "ppipe_pareto_f2: NULL ctx");
+  if (!out) return fail(c, PPIPE_EINVAL, "ppipe_pareto_f2: NULL output");
+  int rc = check_params(c, p, "ppipe_pareto_f2");
+  if (rc != PPIPE_OK) return rc;
+  if (c->pending_upload)
+    return fail(c, PPIPE_ESTATE, "ppipe_pareto_f2: profiles from ppipe_update_profiles_async are uploaded by "
+                                 "ppipe_enumerate only; use ppipe_update_profiles");
+  std::vector<int> own;  // local indices of the models this rank scores
+  for (size_t i = 0; i < c->local.size(); ++i)
+    if (c->h_models[i].row_lo == 0 && c->h_models[i].row_hi > 0) own.push_back((int)i);
+  for (int i : own)
+    if (c->h_models[i].M > kF2MaxLayers)
+      return fail(c, PPIPE_ERANGE, "model %d: %u layers; F2 supports at most %u", c->local[i], c->h_models[i].M,
+                  kF2MaxLayers);
+  CU(c, cudaSetDevice(c->device));
+  c->have_result = false;
+  c->enumerated = false;
+  c->last_params = *p;
+  c->last_slo.assign(p->slo_us, p->slo_us + c->n_models);
+  c->last_params.slo_us = c->last_slo.data();
+  Problem pb{};
+  rc = setup_problem(c, &pb);
+  if (rc != PPIPE_OK) return rc;
+  if (c->n_seg_total >= (1ull << 28)) return fail(c, PPIPE_ERANGE, "F2: %llu segments >= 2^28",
+                                                  (unsigned long long)c->n_seg_total);
+  const int Kmax = (int)p->max_partitions;
+  // G: all C^3 segments of the largest model, capped at PPIPE_F2_G_BYTES (default 8 GiB), at least one segment
+  size_t g_need = 0, f_need = 1;
+  uint64_t n_cand = 0;
+  for (int i : own) {
+    const uint32_t M = c->h_models[i].M;
+    g_need = std::max(g_need, f2_g3_elems_per_segment((int)c->B, M) * c->C * c->C * c->C);
+    f_need = std::max<size_t>(f_need, (size_t)c->C * c->C * c->B * M);
+    uint64_t pw = 1, comb = 1;  // C(M-1, K-1) * C^K * B
+    for (uint32_t K = 1; K <= (uint32_t)Kmax && K <= M; ++K) {
+      pw *= c->C;
+      n_cand += comb * pw * c->B;
+      comb = comb * (M - K) / K;
+    }
+  }
+  size_t g_budget = 8ull << 30;
+  if (const char* gb = getenv("PPIPE_F2_G_BYTES")) g_budget = (size_t)strtoull(gb, nullptr, 10);
+  size_t g_cap = std::min(g_need, g_budget / sizeof(int32_t));
+  for (int i : own) g_cap = std::max(g_cap, f2_g3_elems_per_segment((int)c->B, c->h_models[i].M));
+  if (Kmax >= 3) CU(c, c->d_G.reserve(std::max<size_t>(g_cap, 1)));
+  if (Kmax >= 2) CU(c, c->d_F.reserve(f_need));
+  int nl = 0;
+  for (int attempt = 0;; ++attempt) {
+    CU(c, c->d_f2surv.reserve(c->f2_cap));
+    F2Out fo{c->d_f2surv.p, c->d_counters.p, (unsigned long long)c->d_f2surv.n, c->d_G.p, c->d_G.n, c->d_F.p};
+    nl = 0;
+    CU(c, cudaEventRecord(c->ev[0], c->stream));
+    CU(c, launch_pack(pb, c->stream));
+    nl += pb.n_local ? 2 : 0;
+    CU(c, cudaEventRecord(c->ev[1], c->stream));
+    CU(c, cudaMemsetAsync(c->d_counters.p, 0, 16 * sizeof(unsigned long long), c->stream));
+    for (int i : own) CU(c, launch_f2_model(pb, i, c->h_models[i].M, Kmax, fo, c->stream, &nl));
+    CU(c, cudaEventRecord(c->ev[2], c->stream));
+    CU(c, cudaMemcpyAsync(c->h_counters, c->d_counters.p, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
+    if (c->h_counters[0] <= c->d_f2surv.n) break;
+    c->f2_cap = c->h_counters[0] + c->h_counters[0] / 4 + 1024;  // deterministic: re-run with room
+  }
+  const uint64_t n_surv = c->h_counters[0], n_feas_local = c->h_counters[1];
+  CU(c, c->d_f2tmp.reserve(std::max<uint64_t>(n_surv, 1)));
+  CU(c, c->d_local.reserve(std::max<uint64_t>(n_surv, 1)));
+  CU(c, c->d_segoff_local.reserve(c->n_seg_total + 1));
+  CU(c, c->d_segtmp.reserve(std::max<uint64_t>(n_surv, 1)));
+  uint64_t n_pts = 0;
+  CU(c, f2_finalize(c->d_f2surv.p, n_surv, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_local.p, c->d_f2tmp.p,
+                    c->d_segoff_local.p, c->d_segtmp.p, &n_pts, &c->scratch, c->stream, &nl));
+  CU(c, cudaEventRecord(c->ev[3], c->stream));
+  const ppipe_point* d_pts = c->d_local.p;
+  const uint64_t* d_off = c->d_segoff_local.p;
+  uint64_t n_cand_all = n_cand, n_feas_all = n_feas_local;
+  if (c->world > 1 && c->comm) {
+    constexpr int kCnt = 3;
+    CU(c, c->d_cnt_send.reserve(kCnt));
+    CU(c, c->d_cnt_recv.reserve(kCnt * (size_t)c->world));
+    uint64_t hs[kCnt] = {n_pts, n_cand, n_feas_local};
+    CU(c, cudaMemcpyAsync(c->d_cnt_send.p, hs, sizeof hs, cudaMemcpyHostToDevice, c->stream));
+    NC_(c, g_nccl.AllGather(c->d_cnt_send.p, c->d_cnt_recv.p, kCnt, ncclUint64, c->comm, c->stream));
+    std::vector<uint64_t> cnts(kCnt * (size_t)c->world);
+    CU(c, cudaMemcpyAsync(cnts.data(), c->d_cnt_recv.p, 8 * cnts.size(), cudaMemcpyDeviceToHost, c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
+    uint64_t maxc = 1, tot = 0;
+    n_cand_all = n_feas_all = 0;
+    for (int r = 0; r < c->world; ++r) {
+      maxc = std::max(maxc, cnts[kCnt * r]);
+      tot += cnts[kCnt * r];
+      n_cand_all += cnts[kCnt * r + 1];
+      n_feas_all += cnts[kCnt * r + 2];
+    }
+    if (c->d_local.n < maxc) {
+      DevBuf<ppipe_point> tmp;
+      CU(c, tmp.reserve(maxc));
+      if (n_pts)
+        CU(c, cudaMemcpyAsync(tmp.p, c->d_local.p, sizeof(ppipe_point) * n_pts, cudaMemcpyDeviceToDevice, c->stream));
+      CU(c, cudaStreamSynchronize(c->stream));
+      c->d_local.release();
+      c->d_local = tmp;
+    }
+    CU(c, c->d_gather.reserve(maxc * c->world));
+    NC_(c, g_nccl.AllGather(c->d_local.p, c->d_gather.p, maxc * sizeof(ppipe_point), ncclUint8, c->comm, c->stream));
+    CU(c, c->d_final.reserve(std::max<uint64_t>(tot, 1)));
+    uint64_t w = 0;
+    for (int r = 0; r < c->world; ++r) {
+      const uint64_t n = cnts[kCnt * r];
+      if (n)
+        CU(c, cudaMemcpyAsync(c->d_final.p + w, c->d_gather.p + (uint64_t)r * maxc, sizeof(ppipe_point) * n,
+                              cudaMemcpyDeviceToDevice, c->stream));
+      w += n;
+    }
+    n_pts = w;
+    CU(c, c->d_segoff_final.reserve(c->n_seg_total + 1));
+    CU(c, c->d_segtmp.reserve(std::max<uint64_t>(n_pts, 1)));
+    CU(c, segment_offsets(c->d_final.p, n_pts, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_segoff_final.p,
+                          c->d_segtmp.p, c->stream, &nl));
+    nl += 2;
+    d_pts = c->d_final.p;
+    d_off = c->d_segoff_final.p;
+  }
+  CU(c, cudaEventRecord(c->ev[4], c->stream));
+  CU(c, cudaEventSynchronize(c->ev[4]));
+  cudaEventElapsedTime(&c->phase_ms[0], c->ev[0], c->ev[1]);
+  cudaEventElapsedTime(&c->phase_ms[1], c->ev[1], c->ev[2]);
+  cudaEventElapsedTime(&c->phase_ms[2], c->ev[2], c->ev[3]);
+  cudaEventElapsedTime(&c->phase_ms[3], c->ev[3], c->ev[4]);
+  c->launches = (uint64_t)nl;
+  std::memset(out, 0, sizeof *out);
+  out->n_candidates = n_cand_all;
+  out->n_feasible = n_feas_all;
+  out->n_points = n_pts;
+  out->n_segments = c->n_seg_total;
+  out->d_points = d_pts;
+  out->d_seg_offsets = d_off;
+  out->n_survivors = n_surv;
+  out->n_candidates_local = n_cand;
+  out->n_feasible_local = n_feas_local;
   if (copy_to_host) {
     CU(c, c->h_points.reserve(n_pts));
     CU(c, c->h_segoff.reserve(c->n_seg_total + 1));

@@ -1,0 +1,544 @@
+// ppipe_f2.cu -- F2, the MILP-lossless frontier.
+//
+// PPipe's pooled MILP gives a chosen pipeline g_d GPUs in stage d; its
+// throughput is min_d g_d X_d with X_d = b / C_d the per-GPU throughput of stage
+// d (X_{ldbij}, eqs. 1.10 / 1.13), and E only has to
+// meet the SLO (eq. 1.12). So per segment (model, K, class tuple)
+// the candidates the MILP can need are those whose vector x = (X_1 .. X_K) is not
+// dominated by another feasible candidate's; among equal vectors the smallest
+// (E, b, c_1, c_2) stays (readings F2-1..F2-4). Virtual-GPU weights
+// scale one stage of every candidate of a segment alike, so they do not change F2.
+//
+// At one batch no two cut sets of a segment are comparable (moving a cut grows one
+// stage and shrinks its neighbour), so dominance comes from other batches b'. For a
+// feasible candidate p = (c_1, c_2, b) and a batch b', "some feasible q at b' has
+// C'_d b <= C_d b' in every stage d, one of them strictly" is a range query:
+//   C'_1 = P1'[c'_1] is non-decreasing in c'_1   ->  c'_1 <= u   (u by binary search)
+//   C'_3 = P3'[M] - P3'[c'_2] non-increasing      ->  c'_2 >= l
+//   C'_2 = P2'[c'_2] - P2'[c'_1]                   ->  G_{b'}[u][l] = min C'_2 over the
+//        feasible (c'_1 <= u, c'_2 >= l) pairs -- a 2-D prefix/suffix minimum table
+//        built per (segment, b') by f2_g3_kernel.
+// Strict dominance = OR over the stage that is strict (three lookups per b').
+// K = 2 uses prefix counts of feasible cuts (f2_g2_kernel), K = 1 compares batches
+// directly. Equal vectors are resolved afterwards (f2_finalize): sort by
+// (segment, vector reduced by gcd(b, C_1, .., C_K)), keep the best of each run,
+// sort into the canonical (segment, b, c_1, c_2) order.
+//
+// Bound: the G tables are written once and read by the queries (HBM / L2); the
+// enumeration itself is the same integer work as score3a. DESIGN.md §5.
+#include <cub/cub.cuh>
+#include <climits>
+
+#include "ppipe_internal.h"
+
+namespace ppipe {
+
+namespace {
+
+constexpr int kF2Threads = 256;
+constexpr int32_t kInf = INT32_MAX;
+
+__device__ __forceinline__ const int32_t* prow(const Problem& pb, const DevModel& md, int k, int bi) {
+  return pb.P + md.p_off + ((size_t)k * pb.B + bi) * md.Mp;
+}
+__device__ __forceinline__ const int32_t* yrow(const Problem& pb, const DevModel& md, int k, int k2, int bi) {
+  return pb.Y + md.y_off + ((size_t)pb.pair_v[k * pb.C + k2] * pb.B + bi) * md.Mp;
+}
+
+// Exclusive suffix minimum over the threads of a block (threads t' > t).
+__device__ __forceinline__ int32_t block_suffix_excl_min(int32_t v, int32_t* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int32_t inc = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int32_t o = __shfl_down_sync(0xffffffffu, inc, off);
+    if (lane + off < 32) inc = min(inc, o);
+  }
+  if (lane == 0) sh[warp] = inc;
+  int32_t excl = __shfl_down_sync(0xffffffffu, inc, 1);
+  if (lane == 31) excl = kInf;
+  __syncthreads();
+  for (int w = warp + 1; w < nw; ++w) excl = min(excl, sh[w]);
+  __syncthreads();
+  return excl;
+}
+
+// Largest i in [lo, hi] with row[i] <= thr, or lo - 1 (row non-decreasing).
+__device__ __forceinline__ int last_le(const int32_t* row, int lo, int hi, int64_t thr) {
+  int a = lo, b = hi + 1;  // answer in [a - 1, b - 1]
+  while (a < b) {
+    const int mid = (a + b) >> 1;
+    if ((int64_t)__ldg(row + mid) <= thr) a = mid + 1;
+    else b = mid;
+  }
+  return a - 1;
+}
+
+// Smallest i in [lo, hi] with row[i] >= target, or hi + 1 (row non-decreasing).
+__device__ __forceinline__ int first_ge(const int32_t* row, int lo, int hi, int64_t target) {
+  int a = lo, b = hi + 1;
+  while (a < b) {
+    const int mid = (a + b) >> 1;
+    if ((int64_t)__ldg(row + mid) >= target) b = mid;
+    else a = mid + 1;
+  }
+  return a;
+}
+
+// C' b <= r  <=>  C' <= floor(r / b);  C' b < r  <=>  C' <= floor((r - 1) / b)  (r >= 1; none for r = 0)
+__device__ __forceinline__ int64_t thr_le(uint64_t r, uint32_t b) { return (int64_t)(r / b); }
+__device__ __forceinline__ int64_t thr_lt(uint64_t r, uint32_t b) { return r ? (int64_t)((r - 1) / b) : -1; }
+
+// A G entry (kInf = no feasible pair in the quadrant) against a threshold.
+__device__ __forceinline__ bool g_le(int32_t g, int64_t t) { return g != kInf && (int64_t)g <= t; }
+
+// Warp-aggregated append of one record per lane that wants it.
+__device__ __forceinline__ void emit_point(bool want, const ppipe_point& p, const F2Out& out) {
+  const unsigned m = __ballot_sync(0xffffffffu, want);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(&out.counters[0], (unsigned long long)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (want) {
+    const unsigned long long i = base + __popc(m & ((1u << lane) - 1));
+    if (i < out.cap) out.surv[i] = p;
+  }
+}
+
+__device__ __forceinline__ ppipe_point make_point(const DevModel& md, int K, int k1, int k2, int k3, int c1, int c2,
+                                                  uint32_t b, int32_t E, int32_t C1, int32_t C2, int32_t C3) {
+  ppipe_point p;
+  p.model = md.model;
+  p.cut[0] = (uint16_t)c1;
+  p.cut[1] = (uint16_t)c2;
+  p.K = (uint8_t)K;
+  p.cls[0] = (uint8_t)k1;
+  p.cls[1] = K >= 2 ? (uint8_t)k2 : (uint8_t)0xFF;
+  p.cls[2] = K >= 3 ? (uint8_t)k3 : (uint8_t)0xFF;
+  p.batch = (uint16_t)b;
+  p.reserved = 0;
+  p.e2e_us = (uint32_t)E;
+  p.stage_us[0] = (uint32_t)C1;
+  p.stage_us[1] = (uint32_t)C2;
+  p.stage_us[2] = (uint32_t)C3;
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// K = 3: G tables. CTA per (segment in chunk, batch b'). Row u = c'_1 in 1..M-2,
+// column l = c'_2 in 2..M-1 (n = M - 2 of each). Thread t holds columns
+// j = t * IT + i (blocked); G[u][l] = min(G[u-1][l], min_{l' >= l} H[u][l']) with
+// H[u][l] = C'_2 if (u < l and feasible) else +inf.
+// E' = (P1[u] - P2[u] + Y12[u]) + (P2[l] + P3[M] - P3[l] + Y23[l]) = a(u) + e(l).
+template <int IT>
+__global__ void __launch_bounds__(kF2Threads) f2_g3_kernel(Problem pb, int ml, int seg_lo, int32_t* G) {
+  extern __shared__ int32_t row_sh[];
+  __shared__ int32_t sh[32];
+  const DevModel md = pb.models[ml];
+  const int M = (int)md.M, n = M - 2, C = pb.C, B = pb.B;
+  const int bq = blockIdx.x % B, seg = seg_lo + blockIdx.x / B;
+  const int k1 = seg / (C * C), k2 = (seg / C) % C, k3 = seg % C;
+  const int32_t *P1 = prow(pb, md, k1, bq), *P2 = prow(pb, md, k2, bq), *P3 = prow(pb, md, k3, bq);
+  const int32_t *Y12 = yrow(pb, md, k1, k2, bq), *Y23 = yrow(pb, md, k2, k3, bq);
+  const int32_t T = md.T, P3M = P3[M];
+  int32_t* Gs = G + (size_t)blockIdx.x * n * n;
+  int32_t e[IT], p2l[IT], prev[IT];
+#pragma unroll
+  for (int i = 0; i < IT; ++i) {
+    const int j = threadIdx.x * IT + i, l = j + 2;
+    e[i] = j < n ? P2[l] + (P3M - P3[l]) + Y23[l] : kInf;
+    p2l[i] = j < n ? P2[l] : 0;
+    prev[i] = kInf;
+  }
+  for (int u = 1; u <= M - 2; ++u) {
+    const int32_t a = P1[u] - P2[u] + Y12[u], p2u = P2[u];
+    int32_t h[IT], run = kInf;
+#pragma unroll
+    for (int i = IT - 1; i >= 0; --i) {
+      const int j = threadIdx.x * IT + i;
+      const bool ok = j < n && j + 2 > u && e[i] != kInf && a + e[i] <= T;
+      run = min(run, ok ? p2l[i] - p2u : kInf);
+      h[i] = run;
+    }
+    const int32_t later = block_suffix_excl_min(run, sh);
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      const int j = threadIdx.x * IT + i;
+      prev[i] = min(prev[i], min(h[i], later));
+      if (j < n) row_sh[j] = prev[i];
+    }
+    __syncthreads();
+    int32_t* out = Gs + (size_t)(u - 1) * n;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) out[j] = row_sh[j];
+    __syncthreads();
+  }
+}
+
+// K = 3 queries: CTA per (segment in chunk, batch b); warp per c_1, lanes over c_2.
+__global__ void __launch_bounds__(kF2Threads) f2_q3_kernel(Problem pb, int ml, int seg_lo, const int32_t* G,
+                                                           F2Out out) {
+  const DevModel md = pb.models[ml];
+  const int M = (int)md.M, n = M - 2, C = pb.C, B = pb.B;
+  const int bi = blockIdx.x % B, segc = blockIdx.x / B, seg = seg_lo + segc;
+  const int k1 = seg / (C * C), k2 = (seg / C) % C, k3 = seg % C;
+  const int32_t *P1 = prow(pb, md, k1, bi), *P2 = prow(pb, md, k2, bi), *P3 = prow(pb, md, k3, bi);
+  const int32_t *Y12 = yrow(pb, md, k1, k2, bi), *Y23 = yrow(pb, md, k2, k3, bi);
+  const int32_t T = md.T, P3M = P3[M];
+  const uint32_t b = pb.batches[bi];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned long long feas = 0;
+  for (int c1 = 1 + warp; c1 <= M - 2; c1 += nw) {
+    const int32_t C1 = P1[c1], a = C1 - P2[c1] + Y12[c1], p2c1 = P2[c1];
+    for (int base = c1 + 1; base <= M - 1; base += 32) {
+      const int c2 = base + lane;
+      bool keep = false;
+      int32_t E = 0, C2 = 0, C3 = 0;
+      if (c2 <= M - 1) {
+        C3 = P3M - P3[c2];
+        E = a + P2[c2] + C3 + Y23[c2];
+        if (E <= T) {
+          ++feas;
+          C2 = P2[c2] - p2c1;
+          bool dom = false;
+          for (int bq = B - 1; bq >= 0 && !dom; --bq) {
+            const uint32_t bv = pb.batches[bq];
+            const uint64_t r1 = (uint64_t)C1 * bv, r2 = (uint64_t)C2 * bv, r3 = (uint64_t)C3 * bv;
+            const int32_t *Q1 = prow(pb, md, k1, bq), *Q3 = prow(pb, md, k3, bq);
+            const int64_t Q3M = Q3[M];
+            const int u = last_le(Q1, 1, M - 2, thr_le(r1, b));
+            if (u < 1) continue;  // no c'_1 at all: nothing at b' is <= in stage 1
+            const int l = first_ge(Q3, 2, M - 1, Q3M - thr_le(r3, b));
+            if (l > M - 1) continue;
+            const int us = last_le(Q1, 1, u, thr_lt(r1, b));
+            const int ls = first_ge(Q3, l, M - 1, Q3M - thr_lt(r3, b));
+            const int32_t* Gb = G + ((size_t)segc * B + bq) * n * n;
+            const int64_t t2 = thr_le(r2, b), t2s = thr_lt(r2, b);
+            dom = g_le(Gb[(size_t)(u - 1) * n + (l - 2)], t2s) ||
+                  (us >= 1 && g_le(Gb[(size_t)(us - 1) * n + (l - 2)], t2)) ||
+                  (ls <= M - 1 && g_le(Gb[(size_t)(u - 1) * n + (ls - 2)], t2));
+          }
+          keep = !dom;
+        }
+      }
+      emit_point(keep, make_point(md, 3, k1, k2, k3, c1, c2, b, E, C1, C2, C3), out);
+    }
+  }
+  for (int off = 16; off; off >>= 1) feas += __shfl_down_sync(0xffffffffu, feas, off);
+  if (lane == 0 && feas) atomicAdd(&out.counters[1], feas);
+}
+
+// K = 2: per (segment, b') prefix counts F[c] = #feasible c'_1 in [1, c], c = 0..M-1.
+__global__ void __launch_bounds__(kF2Threads) f2_g2_kernel(Problem pb, int ml, int32_t* F) {
+  using Scan = cub::BlockScan<int32_t, kF2Threads>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int32_t carry;
+  const DevModel md = pb.models[ml];
+  const int M = (int)md.M, C = pb.C, B = pb.B;
+  const int bq = blockIdx.x % B, seg = blockIdx.x / B;
+  const int k1 = seg / C, k2 = seg % C;
+  const int32_t *P1 = prow(pb, md, k1, bq), *P2 = prow(pb, md, k2, bq), *Y12 = yrow(pb, md, k1, k2, bq);
+  const int32_t T = md.T, P2M = P2[M];
+  int32_t* Fs = F + (size_t)blockIdx.x * M;
+  if (threadIdx.x == 0) {
+    carry = 0;
+    Fs[0] = 0;
+  }
+  __syncthreads();
+  for (int c0 = 1; c0 <= M - 1; c0 += kF2Threads) {
+    const int c = c0 + threadIdx.x;
+    const int32_t f = (c <= M - 1 && P1[c] + (P2M - P2[c]) + Y12[c] <= T) ? 1 : 0;
+    int32_t inc, tot;
+    Scan(tmp).InclusiveSum(f, inc, tot);
+    if (c <= M - 1) Fs[c] = carry + inc;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+}
+
+// K = 2 queries: CTA per (segment, batch b), thread per c_1.
+__global__ void __launch_bounds__(kF2Threads) f2_q2_kernel(Problem pb, int ml, const int32_t* F, F2Out out) {
+  const DevModel md = pb.models[ml];
+  const int M = (int)md.M, C = pb.C, B = pb.B;
+  const int bi = blockIdx.x % B, seg = blockIdx.x / B;
+  const int k1 = seg / C, k2 = seg % C;
+  const int32_t *P1 = prow(pb, md, k1, bi), *P2 = prow(pb, md, k2, bi), *Y12 = yrow(pb, md, k1, k2, bi);
+  const int32_t T = md.T, P2M = P2[M];
+  const uint32_t b = pb.batches[bi];
+  unsigned long long feas = 0;
+  for (int c0 = 1; c0 <= M - 1; c0 += blockDim.x) {
+    const int c = c0 + threadIdx.x;
+    bool keep = false;
+    int32_t E = 0, C1 = 0, C2 = 0;
+    if (c <= M - 1) {
+      C1 = P1[c];
+      C2 = P2M - P2[c];
+      E = C1 + C2 + Y12[c];
+      if (E <= T) {
+        ++feas;
+        bool dom = false;
+        for (int bq = B - 1; bq >= 0 && !dom; --bq) {
+          const uint32_t bv = pb.batches[bq];
+          const uint64_t r1 = (uint64_t)C1 * bv, r2 = (uint64_t)C2 * bv;
+          const int32_t *Q1 = prow(pb, md, k1, bq), *Q2 = prow(pb, md, k2, bq);
+          const int64_t Q2M = Q2[M];
+          const int32_t* Fb = F + ((size_t)seg * B + bq) * M;
+          // stage 1: c' <= u (C'_1 non-decreasing); stage 2: c' >= l (C'_2 = Q2M - Q2[c'] non-increasing)
+          const int u = last_le(Q1, 1, M - 1, thr_le(r1, b));
+          const int l = first_ge(Q2, 1, M - 1, Q2M - thr_le(r2, b));
+          if (u < l) continue;
+          const int us = last_le(Q1, 1, u, thr_lt(r1, b));
+          const int ls = first_ge(Q2, l, M - 1, Q2M - thr_lt(r2, b));
+          dom = (us >= l && Fb[us] - Fb[l - 1] > 0) || (ls <= u && Fb[u] - Fb[ls - 1] > 0);
+        }
+        keep = !dom;
+      }
+    }
+    emit_point(keep, make_point(md, 2, k1, k2, 0, c, 0, b, E, C1, C2, 0), out);
+  }
+  for (int off = 16; off; off >>= 1) feas += __shfl_down_sync(0xffffffffu, feas, off);
+  if ((threadIdx.x & 31) == 0 && feas) atomicAdd(&out.counters[1], feas);
+}
+
+// K = 1: CTA per class, threads over batches (strict dominance only; ties in f2_finalize).
+__global__ void __launch_bounds__(kF2Threads) f2_q1_kernel(Problem pb, int ml, F2Out out) {
+  const DevModel md = pb.models[ml];
+  const int M = (int)md.M, B = pb.B;
+  const int k = blockIdx.x;
+  const int32_t T = md.T;
+  unsigned long long feas = 0;
+  for (int b0 = 0; b0 < B; b0 += blockDim.x) {
+    const int bi = b0 + threadIdx.x;
+    bool keep = false;
+    int32_t C1 = 0;
+    uint32_t b = 0;
+    if (bi < B) {
+      C1 = prow(pb, md, k, bi)[M];
+      b = pb.batches[bi];
+      if (C1 <= T) {
+        ++feas;
+        bool dom = false;
+        for (int bq = 0; bq < B && !dom; ++bq) {
+          const int32_t Cq = prow(pb, md, k, bq)[M];
+          dom = Cq <= T && (uint64_t)Cq * b < (uint64_t)C1 * pb.batches[bq];
+        }
+        keep = !dom;
+      }
+    }
+    emit_point(keep, make_point(md, 1, k, 0, 0, 0, 0, b, C1, C1, 0, 0), out);
+  }
+  for (int off = 16; off; off >>= 1) feas += __shfl_down_sync(0xffffffffu, feas, off);
+  if ((threadIdx.x & 31) == 0 && feas) atomicAdd(&out.counters[1], feas);
+}
+
+template <int IT>
+cudaError_t launch_g3(const Problem& pb, int ml, int seg_lo, int nseg, int M, int32_t* G, cudaStream_t s) {
+  const size_t smem = sizeof(int32_t) * (size_t)(M - 2);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(f2_g3_kernel<IT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  f2_g3_kernel<IT><<<nseg * pb.B, kF2Threads, smem, s>>>(pb, ml, seg_lo, G);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t f2_g3_elems_per_segment(int B, uint32_t M) {
+  const size_t n = M >= 3 ? M - 2 : 0;
+  return (size_t)B * n * n;
+}
+
+cudaError_t launch_f2_model(const Problem& pb, int ml, uint32_t M, int Kmax, const F2Out& out, cudaStream_t s,
+                            int* n_launches) {
+  cudaError_t e;
+  const int C = pb.C;
+  f2_q1_kernel<<<C, 64, 0, s>>>(pb, ml, out);
+  ++*n_launches;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (Kmax >= 2 && M >= 2) {
+    f2_g2_kernel<<<C * C * pb.B, kF2Threads, 0, s>>>(pb, ml, out.F);
+    f2_q2_kernel<<<C * C * pb.B, kF2Threads, 0, s>>>(pb, ml, out.F, out);
+    *n_launches += 2;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (Kmax >= 3 && M >= 3) {
+    const size_t per_seg = f2_g3_elems_per_segment(pb.B, M);
+    const int nseg_all = C * C * C;
+    int chunk = (int)std::min<size_t>((size_t)nseg_all, std::max<size_t>(1, out.g_cap / per_seg));
+    const int n = (int)M - 2, it = (n + kF2Threads - 1) / kF2Threads;
+    for (int lo = 0; lo < nseg_all; lo += chunk) {
+      const int ns = std::min(chunk, nseg_all - lo);
+      if (it <= 1) e = launch_g3<1>(pb, ml, lo, ns, (int)M, out.G, s);
+      else if (it <= 2) e = launch_g3<2>(pb, ml, lo, ns, (int)M, out.G, s);
+      else if (it <= 4) e = launch_g3<4>(pb, ml, lo, ns, (int)M, out.G, s);
+      else if (it <= 8) e = launch_g3<8>(pb, ml, lo, ns, (int)M, out.G, s);
+      else e = launch_g3<16>(pb, ml, lo, ns, (int)M, out.G, s);
+      if (e != cudaSuccess) return e;
+      f2_q3_kernel<<<ns * pb.B, kF2Threads, 0, s>>>(pb, ml, lo, out.G, out);
+      *n_launches += 2;
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+  }
+  return cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------
+// finalize: equal-vector runs, canonical order, CSR
+// ---------------------------------------------------------------------------
+namespace {
+
+struct K128 {
+  uint64_t hi, lo;
+  __host__ __device__ bool operator==(const K128& o) const { return hi == o.hi && lo == o.lo; }
+};
+
+__device__ __forceinline__ uint64_t seg_of(const ppipe_point& p, const uint64_t* seg_base, int C) {
+  uint64_t off = 0, pw = 1;
+  for (int k = 1; k < p.K; ++k) {
+    pw *= (uint64_t)C;
+    off += pw;
+  }
+  uint64_t idx = 0;
+  for (int d = 0; d < p.K; ++d) idx = idx * C + p.cls[d];
+  return seg_base[p.model] + off + idx;
+}
+
+__device__ __forceinline__ uint32_t gcd32(uint32_t a, uint32_t b) {
+  while (b) {
+    const uint32_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+// Equal-vector key: (segment, b/g, C_1/g, C_2/g, C_3/g), g = gcd(b, C_1..C_K) >= 1:
+// x_p == x_q  <=>  (b, C) proportional  <=>  equal reduced tuples. Bits 28|16|28|28|28.
+__global__ void f2_tie_keys_kernel(const ppipe_point* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t* hi,
+                                   uint64_t* lo, uint32_t* idx) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const ppipe_point p = in[i];
+    uint32_t g = p.batch;
+    for (int d = 0; d < p.K; ++d) g = gcd32(g, p.stage_us[d]);
+    const uint64_t c1 = p.stage_us[0] / g, c2 = p.stage_us[1] / g, c3 = p.stage_us[2] / g;
+    hi[i] = (seg_of(p, seg_base, C) << 36) | ((uint64_t)(p.batch / g) << 20) | (c1 >> 8);
+    lo[i] = ((c1 & 0xFF) << 56) | (c2 << 28) | c3;
+    idx[i] = (uint32_t)i;
+  }
+}
+
+// Canonical output key: (segment) then (b, c_1, c_2).
+__global__ void f2_out_keys_kernel(const ppipe_point* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t* hi,
+                                   uint64_t* lo, uint32_t* idx) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const ppipe_point p = in[i];
+    hi[i] = seg_of(p, seg_base, C);
+    lo[i] = ((uint64_t)p.batch << 32) | ((uint64_t)p.cut[0] << 16) | p.cut[1];
+    idx[i] = (uint32_t)i;
+  }
+}
+
+__global__ void gather_u64_kernel(const uint64_t* src, const uint32_t* idx, uint64_t n, uint64_t* dst) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+
+__global__ void make_k128_kernel(const uint64_t* hi, const uint64_t* lo_src, const uint32_t* idx, uint64_t n,
+                                 K128* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = K128{hi[i], lo_src[idx[i]]};
+}
+
+__global__ void gather_pts_kernel(const ppipe_point* in, const uint32_t* idx, uint64_t n, ppipe_point* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = in[idx[i]];
+}
+
+// Of two records with the same vector: the smaller (E, b, c_1, c_2).
+struct PickMinE {
+  const ppipe_point* r;
+  __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const {
+    const ppipe_point &p = r[a], &q = r[b];
+    if (p.e2e_us != q.e2e_us) return p.e2e_us < q.e2e_us ? a : b;
+    if (p.batch != q.batch) return p.batch < q.batch ? a : b;
+    if (p.cut[0] != q.cut[0]) return p.cut[0] < q.cut[0] ? a : b;
+    return p.cut[1] <= q.cut[1] ? a : b;
+  }
+};
+
+inline int grid_for(uint64_t n) { return (int)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 8)); }
+
+inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+}  // namespace
+
+cudaError_t f2_finalize(const ppipe_point* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t n_seg,
+                        ppipe_point* out, ppipe_point* tmp_pts, uint64_t* seg_offsets, uint64_t* seg_tmp,
+                        uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches) {
+  cudaError_t e;
+  if (n == 0) {
+    *n_out_host = 0;
+    return segment_offsets(out, 0, seg_base, C, n_seg, seg_offsets, seg_tmp, s, n_launches);
+  }
+  const int ni = (int)n;
+  // scratch: hi, lo, hi2 (u64 x n), idx, idx2, agg (u32 x n), keys, ukeys (K128 x n), nruns, cub temp
+  size_t b_sort = 0, b_red = 0;
+  e = cub::DeviceRadixSort::SortPairs(nullptr, b_sort, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
+                                      (uint32_t*)nullptr, ni, 0, 64, s);
+  if (e != cudaSuccess) return e;
+  e = cub::DeviceReduce::ReduceByKey(nullptr, b_red, (K128*)nullptr, (K128*)nullptr, (uint32_t*)nullptr,
+                                     (uint32_t*)nullptr, (uint64_t*)nullptr, PickMinE{nullptr}, ni, s);
+  if (e != cudaSuccess) return e;
+  const size_t o_hi = 0, o_lo = o_hi + align_up(8 * n), o_k2 = o_lo + align_up(8 * n), o_k3 = o_k2 + align_up(8 * n),
+               o_idx = o_k3 + align_up(8 * n), o_idx2 = o_idx + align_up(4 * n), o_agg = o_idx2 + align_up(4 * n),
+               o_keys = o_agg + align_up(4 * n), o_ukeys = o_keys + align_up(16 * n),
+               o_runs = o_ukeys + align_up(16 * n), o_tmp = o_runs + 256,
+               total = o_tmp + align_up(std::max(b_sort, b_red));
+  if (scratch->bytes < total) {
+    if (scratch->buf) cudaFree(scratch->buf);
+    scratch->buf = nullptr;
+    scratch->bytes = 0;
+    if ((e = cudaMalloc(&scratch->buf, total)) != cudaSuccess) return e;
+    scratch->bytes = total;
+  }
+  char* base = (char*)scratch->buf;
+  uint64_t *hi = (uint64_t*)(base + o_hi), *lo = (uint64_t*)(base + o_lo), *k2 = (uint64_t*)(base + o_k2),
+           *k3 = (uint64_t*)(base + o_k3);
+  uint32_t *idx = (uint32_t*)(base + o_idx), *idx2 = (uint32_t*)(base + o_idx2), *agg = (uint32_t*)(base + o_agg);
+  K128 *keys = (K128*)(base + o_keys), *ukeys = (K128*)(base + o_ukeys);
+  uint64_t* nruns = (uint64_t*)(base + o_runs);
+  void* tmp = base + o_tmp;
+  const int g = grid_for(n);
+
+  // 1) sort by the equal-vector key (lo, then hi: LSD radix sort is stable)
+  f2_tie_keys_kernel<<<g, 256, 0, s>>>(in, n, seg_base, C, hi, lo, idx);
+  if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, lo, k2, idx, idx2, ni, 0, 64, s)) != cudaSuccess) return e;
+  gather_u64_kernel<<<g, 256, 0, s>>>(hi, idx2, n, k3);
+  if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, k3, k2, idx2, idx, ni, 0, 64, s)) != cudaSuccess) return e;
+  // k2 = hi sorted, idx = record index in sorted order
+  make_k128_kernel<<<g, 256, 0, s>>>(k2, lo, idx, n, keys);
+  // 2) best record of each run of equal vectors
+  if ((e = cub::DeviceReduce::ReduceByKey(tmp, b_red, keys, ukeys, idx, agg, nruns, PickMinE{in}, ni, s)) !=
+      cudaSuccess)
+    return e;
+  uint64_t nr = 0;
+  if ((e = cudaMemcpyAsync(&nr, nruns, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  gather_pts_kernel<<<grid_for(nr), 256, 0, s>>>(in, agg, nr, tmp_pts);
+  // 3) canonical order (segment, b, c_1, c_2)
+  const int nri = (int)nr;
+  f2_out_keys_kernel<<<grid_for(nr), 256, 0, s>>>(tmp_pts, nr, seg_base, C, hi, lo, idx);
+  if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, lo, k2, idx, idx2, nri, 0, 64, s)) != cudaSuccess) return e;
+  gather_u64_kernel<<<grid_for(nr), 256, 0, s>>>(hi, idx2, nr, k3);
+  if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, k3, k2, idx2, idx, nri, 0, 64, s)) != cudaSuccess) return e;
+  gather_pts_kernel<<<grid_for(nr), 256, 0, s>>>(tmp_pts, idx, nr, out);
+  *n_launches += 13;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  *n_out_host = nr;
+  return segment_offsets(out, nr, seg_base, C, n_seg, seg_offsets, seg_tmp, s, n_launches);
+}
+
+}  // namespace ppipe

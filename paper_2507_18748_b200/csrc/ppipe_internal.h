@@ -65,6 +65,21 @@ struct ScoreOut {
 
 size_t hot_unit_table_bytes(const Problem& pb);
 
+// F2 (ppipe_f2.cu): per-model strict-dominance queries append the candidates no
+// other feasible candidate beats in every stage (ties left in) to surv.
+struct F2Out {
+  ppipe_point* surv;
+  unsigned long long* counters;  // [0] survivors appended, [1] feasible
+  unsigned long long cap;
+  int32_t* G;                    // K = 3 quadrant-minimum tables, g_cap elements
+  size_t g_cap;                  // >= f2_g3_elems_per_segment(B, M) for every model
+  int32_t* F;                    // K = 2 prefix counts, >= C * C * B * M elements
+};
+constexpr uint32_t kF2MaxLayers = 4096;  // a G row (M - 2 values) is staged in shared memory
+size_t f2_g3_elems_per_segment(int B, uint32_t M);
+cudaError_t launch_f2_model(const Problem& pb, int local_model, uint32_t M, int Kmax, const F2Out& out,
+                            cudaStream_t s, int* n_launches);
+
 // Launchers (stream-ordered). Return cudaError_t of the launch.
 cudaError_t launch_pack(const Problem& pb, cudaStream_t s);
 cudaError_t launch_score(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches);
@@ -96,6 +111,12 @@ cudaError_t segment_offsets(const ppipe_point* pts, uint64_t n, const uint64_t* 
 cudaError_t truncate_frontier(const ppipe_point* in, const uint64_t* seg_offsets_in, uint64_t n_in, uint64_t n_seg,
                               const uint32_t* T_new, ppipe_point* out, uint64_t* seg_offsets_out,
                               uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches);
+
+// F2 tail: resolve equal vectors (keep the smallest (E, b, c_1, c_2) of each run),
+// sort into (segment, b, c_1, c_2) order and build the CSR. tmp_pts holds n records.
+cudaError_t f2_finalize(const ppipe_point* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t n_seg,
+                        ppipe_point* out, ppipe_point* tmp_pts, uint64_t* seg_offsets, uint64_t* seg_tmp,
+                        uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches);
 
 // Device-side profile validation for ppipe_update_profiles (the same envelope as
 // the host check of ppipe_load_profiles): per local model, every whole-model

@@ -84,6 +84,51 @@ def test_gloo_two_rank_partition_and_merge(oracle_built, cfg):
     assert same
 
 
+def _gloo_f2_worker(rank, world, port, cfg, q):
+    """F2 placement: the rank holding a model's row 0 (its K = 1 row) owns the whole model;
+    the rank-ordered concatenation of owned frontiers is the global F2 frontier."""
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2507_18748_b200.build import build
+        build()
+        import paper_2507_18748_b200 as pp
+        from oracle import POINT_DTYPE, run_oracle
+        from workloads import make_config
+        w = make_config(cfg)
+        rows = pp.partition_rows([m.n_layers for m in w.models], w.n_classes, w.n_batches, 3, rank, world)
+        own = [m for m in range(len(w.models)) if int(rows[m, 0]) == 0 and int(rows[m, 1]) > 0]
+        parts = [run_oracle(w, model_lo=m, model_hi=m + 1, threads=2, frontier=2).points for m in own]
+        local = np.concatenate(parts) if parts else np.zeros(0, dtype=POINT_DTYPE)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (local.tobytes(), own))
+        if rank == 0:
+            owners = sorted(m for _, o in gathered for m in o)
+            union = np.concatenate([np.frombuffer(b, dtype=POINT_DTYPE) for b, _ in gathered])
+            full = run_oracle(w, threads=2, frontier=2)
+            q.put((owners == list(range(len(w.models))),
+                   np.array_equal(union.view(np.uint8), full.points.view(np.uint8))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg", [3])
+def test_gloo_two_rank_f2_owned_models(oracle_built, cfg):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_f2_worker, args=(r, 2, port, cfg, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+    assert all(p.exitcode == 0 for p in procs)
+    each_model_once, same = q.get(timeout=5)
+    assert each_model_once and same
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("cfg,extra", [(3, ["--oracle"]), (5, ["--models", "24"]),
                                        (4, []),  # one model shared by every rank
