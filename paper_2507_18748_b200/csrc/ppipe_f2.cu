@@ -63,35 +63,6 @@ __device__ __forceinline__ int32_t block_suffix_excl_min(int32_t v, int32_t* sh)
   return excl;
 }
 
-// Largest i in [lo, hi] with row[i] <= thr, or lo - 1 (row non-decreasing).
-__device__ __forceinline__ int last_le(const int32_t* row, int lo, int hi, int64_t thr) {
-  int a = lo, b = hi + 1;  // answer in [a - 1, b - 1]
-  while (a < b) {
-    const int mid = (a + b) >> 1;
-    if ((int64_t)__ldg(row + mid) <= thr) a = mid + 1;
-    else b = mid;
-  }
-  return a - 1;
-}
-
-// Smallest i in [lo, hi] with row[i] >= target, or hi + 1 (row non-decreasing).
-__device__ __forceinline__ int first_ge(const int32_t* row, int lo, int hi, int64_t target) {
-  int a = lo, b = hi + 1;
-  while (a < b) {
-    const int mid = (a + b) >> 1;
-    if ((int64_t)__ldg(row + mid) >= target) b = mid;
-    else a = mid + 1;
-  }
-  return a;
-}
-
-// C' b <= r  <=>  C' <= floor(r / b);  C' b < r  <=>  C' <= floor((r - 1) / b)  (r >= 1; none for r = 0)
-__device__ __forceinline__ int64_t thr_le(uint64_t r, uint32_t b) { return (int64_t)(r / b); }
-__device__ __forceinline__ int64_t thr_lt(uint64_t r, uint32_t b) { return r ? (int64_t)((r - 1) / b) : -1; }
-
-// A G entry (kInf = no feasible pair in the quadrant) against a threshold.
-__device__ __forceinline__ bool g_le(int32_t g, int64_t t) { return g != kInf && (int64_t)g <= t; }
-
 // Warp-aggregated append of one record per lane that wants it.
 __device__ __forceinline__ void emit_point(bool want, const ppipe_point& p, const F2Out& out) {
   const unsigned m = __ballot_sync(0xffffffffu, want);
@@ -176,53 +147,156 @@ __global__ void __launch_bounds__(kF2Threads) f2_g3_kernel(Problem pb, int ml, i
   }
 }
 
-// K = 3 queries: CTA per (segment in chunk, batch b); warp per c_1, lanes over c_2.
-__global__ void __launch_bounds__(kF2Threads) f2_q3_kernel(Problem pb, int ml, int seg_lo, const int32_t* G,
-                                                           F2Out out) {
+// Inverse stage tables (per model; B x B x M per class, u16, c in [1, M-1]):
+//   PF[k][b][b'][c]  = last c' in [1, M-1] with P_{k,b'}[c'] * b <= P_{k,b}[c] * b'  (0 = none)
+//   SF[k][b][b'][c]  = first c' in [1, M-1] with (P_{k,b'}[M] - P_{k,b'}[c']) * b
+//                      <= (P_{k,b}[M] - P_{k,b}[c]) * b'                              (M = none)
+// and the strict (<) versions PFs / SFs. A first stage [0, c) at batch b is matched or
+// beaten at b' exactly by the cuts c' <= PF (C'_1 non-decreasing in c'); a last stage
+// [c, M) by the cuts c' >= SF. K = 3 clamps them to [1, M-2] / [2, M-1].
+__global__ void __launch_bounds__(kF2Threads) f2_inv_kernel(Problem pb, int ml, F2Out out) {
+  const DevModel md = pb.models[ml];
+  const int M = (int)md.M, B = pb.B;
+  const int bq = blockIdx.x % B, bi = (blockIdx.x / B) % B, k = blockIdx.x / (B * B);
+  const int32_t *P = prow(pb, md, k, bi), *Q = prow(pb, md, k, bq);
+  const uint64_t b = pb.batches[bi], bv = pb.batches[bq];
+  const int64_t PM = P[M], QM = Q[M];
+  const size_t row = ((size_t)blockIdx.x) * M;
+  for (int c = 1 + threadIdx.x; c <= M - 1; c += blockDim.x) {
+    const uint64_t r1 = (uint64_t)P[c] * bv, r2 = (uint64_t)(PM - P[c]) * bv;
+    // prefix stage: largest c' with Q[c'] * b <= r1 (resp. < r1)
+    int lo = 1, hi = M;  // first c' failing, in [1, M]
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((uint64_t)Q[mid] * b <= r1) lo = mid + 1;
+      else hi = mid;
+    }
+    const int pf = lo - 1;
+    lo = 1;
+    hi = pf + 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((uint64_t)Q[mid] * b < r1) lo = mid + 1;
+      else hi = mid;
+    }
+    const int pfs = lo - 1;
+    // suffix stage: smallest c' with (QM - Q[c']) * b <= r2 (resp. < r2); non-increasing in c'
+    lo = 1;
+    hi = M;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((uint64_t)(QM - Q[mid]) * b <= r2) hi = mid;
+      else lo = mid + 1;
+    }
+    const int sf = lo;
+    hi = M;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((uint64_t)(QM - Q[mid]) * b < r2) hi = mid;
+      else lo = mid + 1;
+    }
+    out.PF[row + c] = (uint16_t)pf;
+    out.PFs[row + c] = (uint16_t)pfs;
+    out.SF[row + c] = (uint16_t)sf;
+    out.SFs[row + c] = (uint16_t)lo;
+  }
+}
+
+// K = 3 queries. Persistent warps pull rows (segment, b, c_1) from a counter in
+// segment-major order (the rows in flight share one segment's G tables in L2). A
+// warp scans its row 32 c_2 at a time, appends the feasible c_2 to a per-warp list
+// and, whenever 32 are queued, runs one candidate per lane through the batches b'
+// (largest first, exit on the first dominator):
+//   u = PF_{k1}[c_1], l = SF_{k3}[c_2]; G[u][l] * b > C_2 b'  => nothing at b' (the
+//   strict variants read G at (us, l) / (u, ls), which are >= G[u][l]);
+//   G[u][l] * b < C_2 b' => dominated (strict in stage 2); equal => check
+//   G[us][l] * b <= C_2 b' (strict in stage 1) and G[u][ls] * b <= C_2 b' (stage 3).
+constexpr int kQ3Warps = kF2Threads / 32;
+
+__device__ __forceinline__ bool f2_dominated3(const Problem& pb, const F2Out& out, int M, int B, int k1, int k3,
+                                              int bi, int c1, int c2, uint32_t b, int32_t C2, const int32_t* Gseg) {
+  const int n = M - 2;
+  const size_t row1 = ((size_t)k1 * B + bi) * B, row3 = ((size_t)k3 * B + bi) * B;
+  for (int bq = B - 1; bq >= 0; --bq) {
+    const int u = min((int)out.PF[(row1 + bq) * M + c1], M - 2);
+    if (u < 1) continue;
+    const int l = max((int)out.SF[(row3 + bq) * M + c2], 2);
+    if (l > M - 1) continue;
+    const int32_t* Gb = Gseg + (size_t)bq * n * n;
+    const int32_t g = Gb[(size_t)(u - 1) * n + (l - 2)];
+    if (g == kInf) continue;
+    const uint64_t r2 = (uint64_t)C2 * pb.batches[bq], gb = (uint64_t)g * b;
+    if (gb > r2) continue;
+    if (gb < r2) return true;
+    const int us = min((int)out.PFs[(row1 + bq) * M + c1], M - 2);
+    if (us >= 1) {
+      const int32_t g1 = Gb[(size_t)(us - 1) * n + (l - 2)];
+      if (g1 != kInf && (uint64_t)g1 * b <= r2) return true;
+    }
+    const int ls = max((int)out.SFs[(row3 + bq) * M + c2], 2);
+    if (ls <= M - 1) {
+      const int32_t g3 = Gb[(size_t)(u - 1) * n + (ls - 2)];
+      if (g3 != kInf && (uint64_t)g3 * b <= r2) return true;
+    }
+  }
+  return false;
+}
+
+__global__ void __launch_bounds__(kF2Threads) f2_q3_kernel(Problem pb, int ml, int seg_lo, int nseg,
+                                                           const int32_t* G, F2Out out) {
+  __shared__ int32_t list[kQ3Warps][64];
   const DevModel md = pb.models[ml];
   const int M = (int)md.M, n = M - 2, C = pb.C, B = pb.B;
-  const int bi = blockIdx.x % B, segc = blockIdx.x / B, seg = seg_lo + segc;
-  const int k1 = seg / (C * C), k2 = (seg / C) % C, k3 = seg % C;
-  const int32_t *P1 = prow(pb, md, k1, bi), *P2 = prow(pb, md, k2, bi), *P3 = prow(pb, md, k3, bi);
-  const int32_t *Y12 = yrow(pb, md, k1, k2, bi), *Y23 = yrow(pb, md, k2, k3, bi);
-  const int32_t T = md.T, P3M = P3[M];
-  const uint32_t b = pb.batches[bi];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int32_t T = md.T;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t* L = list[warp];
+  const unsigned long long n_units = (unsigned long long)nseg * B * n;
   unsigned long long feas = 0;
-  for (int c1 = 1 + warp; c1 <= M - 2; c1 += nw) {
-    const int32_t C1 = P1[c1], a = C1 - P2[c1] + Y12[c1], p2c1 = P2[c1];
-    for (int base = c1 + 1; base <= M - 1; base += 32) {
-      const int c2 = base + lane;
+  for (;;) {
+    unsigned long long unit = 0;
+    if (lane == 0) unit = atomicAdd(&out.counters[2], 1ull);
+    unit = __shfl_sync(0xffffffffu, unit, 0);
+    if (unit >= n_units) break;
+    const int c1 = 1 + (int)(unit % n);
+    const int bi = (int)((unit / n) % B);
+    const int segc = (int)(unit / ((unsigned long long)n * B));
+    const int seg = seg_lo + segc;
+    const int k1 = seg / (C * C), k2 = (seg / C) % C, k3 = seg % C;
+    const int32_t *P1 = prow(pb, md, k1, bi), *P2 = prow(pb, md, k2, bi), *P3 = prow(pb, md, k3, bi);
+    const int32_t *Y12 = yrow(pb, md, k1, k2, bi), *Y23 = yrow(pb, md, k2, k3, bi);
+    const int32_t P3M = P3[M], C1 = P1[c1], p2c1 = P2[c1], a = C1 - p2c1 + Y12[c1];
+    const uint32_t b = pb.batches[bi];
+    const int32_t* Gseg = G + (size_t)segc * B * n * n;
+    int cnt = 0;
+    for (int base = c1 + 1; base <= M - 1 || cnt > 0; base += 32) {
+      if (base <= M - 1) {
+        const int c2 = base + lane;
+        bool f = false;
+        if (c2 <= M - 1) f = a + P2[c2] + (P3M - P3[c2]) + Y23[c2] <= T;
+        const unsigned m = __ballot_sync(0xffffffffu, f);
+        if (f) L[cnt + __popc(m & ((1u << lane) - 1))] = c2;
+        cnt += __popc(m);
+        feas += f;
+        __syncwarp();
+        if (cnt < 32 && base + 32 <= M - 1) continue;  // keep filling
+      }
+      // process up to 32 queued candidates, one per lane
+      const bool act = lane < cnt;
       bool keep = false;
-      int32_t E = 0, C2 = 0, C3 = 0;
-      if (c2 <= M - 1) {
+      int32_t c2 = 0, E = 0, C2 = 0, C3 = 0;
+      if (act) {
+        c2 = L[lane];
+        C2 = P2[c2] - p2c1;
         C3 = P3M - P3[c2];
         E = a + P2[c2] + C3 + Y23[c2];
-        if (E <= T) {
-          ++feas;
-          C2 = P2[c2] - p2c1;
-          bool dom = false;
-          for (int bq = B - 1; bq >= 0 && !dom; --bq) {
-            const uint32_t bv = pb.batches[bq];
-            const uint64_t r1 = (uint64_t)C1 * bv, r2 = (uint64_t)C2 * bv, r3 = (uint64_t)C3 * bv;
-            const int32_t *Q1 = prow(pb, md, k1, bq), *Q3 = prow(pb, md, k3, bq);
-            const int64_t Q3M = Q3[M];
-            const int u = last_le(Q1, 1, M - 2, thr_le(r1, b));
-            if (u < 1) continue;  // no c'_1 at all: nothing at b' is <= in stage 1
-            const int l = first_ge(Q3, 2, M - 1, Q3M - thr_le(r3, b));
-            if (l > M - 1) continue;
-            const int us = last_le(Q1, 1, u, thr_lt(r1, b));
-            const int ls = first_ge(Q3, l, M - 1, Q3M - thr_lt(r3, b));
-            const int32_t* Gb = G + ((size_t)segc * B + bq) * n * n;
-            const int64_t t2 = thr_le(r2, b), t2s = thr_lt(r2, b);
-            dom = g_le(Gb[(size_t)(u - 1) * n + (l - 2)], t2s) ||
-                  (us >= 1 && g_le(Gb[(size_t)(us - 1) * n + (l - 2)], t2)) ||
-                  (ls <= M - 1 && g_le(Gb[(size_t)(u - 1) * n + (ls - 2)], t2));
-          }
-          keep = !dom;
-        }
+        keep = !f2_dominated3(pb, out, M, B, k1, k3, bi, c1, c2, b, C2, Gseg);
       }
       emit_point(keep, make_point(md, 3, k1, k2, k3, c1, c2, b, E, C1, C2, C3), out);
+      __syncwarp();
+      const int rest = cnt > 32 ? cnt - 32 : 0;
+      if (lane < rest) L[lane] = L[32 + lane];
+      __syncwarp();
+      cnt = rest;
     }
   }
   for (int off = 16; off; off >>= 1) feas += __shfl_down_sync(0xffffffffu, feas, off);
@@ -258,7 +332,8 @@ __global__ void __launch_bounds__(kF2Threads) f2_g2_kernel(Problem pb, int ml, i
   }
 }
 
-// K = 2 queries: CTA per (segment, batch b), thread per c_1.
+// K = 2 queries: CTA per (segment, batch b), thread per c_1. Some feasible c' at b'
+// beats p in stage 1 strictly (others <=) iff one lies in [SF_{k2}, PFs_{k1}], etc.
 __global__ void __launch_bounds__(kF2Threads) f2_q2_kernel(Problem pb, int ml, const int32_t* F, F2Out out) {
   const DevModel md = pb.models[ml];
   const int M = (int)md.M, C = pb.C, B = pb.B;
@@ -267,6 +342,7 @@ __global__ void __launch_bounds__(kF2Threads) f2_q2_kernel(Problem pb, int ml, c
   const int32_t *P1 = prow(pb, md, k1, bi), *P2 = prow(pb, md, k2, bi), *Y12 = yrow(pb, md, k1, k2, bi);
   const int32_t T = md.T, P2M = P2[M];
   const uint32_t b = pb.batches[bi];
+  const size_t row1 = ((size_t)k1 * B + bi) * B, row2 = ((size_t)k2 * B + bi) * B;
   unsigned long long feas = 0;
   for (int c0 = 1; c0 <= M - 1; c0 += blockDim.x) {
     const int c = c0 + threadIdx.x;
@@ -280,17 +356,10 @@ __global__ void __launch_bounds__(kF2Threads) f2_q2_kernel(Problem pb, int ml, c
         ++feas;
         bool dom = false;
         for (int bq = B - 1; bq >= 0 && !dom; --bq) {
-          const uint32_t bv = pb.batches[bq];
-          const uint64_t r1 = (uint64_t)C1 * bv, r2 = (uint64_t)C2 * bv;
-          const int32_t *Q1 = prow(pb, md, k1, bq), *Q2 = prow(pb, md, k2, bq);
-          const int64_t Q2M = Q2[M];
-          const int32_t* Fb = F + ((size_t)seg * B + bq) * M;
-          // stage 1: c' <= u (C'_1 non-decreasing); stage 2: c' >= l (C'_2 = Q2M - Q2[c'] non-increasing)
-          const int u = last_le(Q1, 1, M - 1, thr_le(r1, b));
-          const int l = first_ge(Q2, 1, M - 1, Q2M - thr_le(r2, b));
+          const int u = out.PF[(row1 + bq) * M + c], l = out.SF[(row2 + bq) * M + c];
           if (u < l) continue;
-          const int us = last_le(Q1, 1, u, thr_lt(r1, b));
-          const int ls = first_ge(Q2, l, M - 1, Q2M - thr_lt(r2, b));
+          const int us = out.PFs[(row1 + bq) * M + c], ls = out.SFs[(row2 + bq) * M + c];
+          const int32_t* Fb = F + ((size_t)seg * B + bq) * M;
           dom = (us >= l && Fb[us] - Fb[l - 1] > 0) || (ls <= u && Fb[u] - Fb[ls - 1] > 0);
         }
         keep = !dom;
@@ -346,6 +415,13 @@ cudaError_t launch_g3(const Problem& pb, int ml, int seg_lo, int nseg, int M, in
 
 }  // namespace
 
+int f2_q3_grid(int device) {
+  int sms = 148, per_sm = 4;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f2_q3_kernel, kF2Threads, 0);
+  return sms * std::max(per_sm, 1);
+}
+
 size_t f2_g3_elems_per_segment(int B, uint32_t M) {
   const size_t n = M >= 3 ? M - 2 : 0;
   return (size_t)B * n * n;
@@ -358,6 +434,11 @@ cudaError_t launch_f2_model(const Problem& pb, int ml, uint32_t M, int Kmax, con
   f2_q1_kernel<<<C, 64, 0, s>>>(pb, ml, out);
   ++*n_launches;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (Kmax >= 2 && M >= 2) {
+    f2_inv_kernel<<<C * pb.B * pb.B, kF2Threads, 0, s>>>(pb, ml, out);
+    ++*n_launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
   if (Kmax >= 2 && M >= 2) {
     f2_g2_kernel<<<C * C * pb.B, kF2Threads, 0, s>>>(pb, ml, out.F);
     f2_q2_kernel<<<C * C * pb.B, kF2Threads, 0, s>>>(pb, ml, out.F, out);
@@ -377,7 +458,8 @@ cudaError_t launch_f2_model(const Problem& pb, int ml, uint32_t M, int Kmax, con
       else if (it <= 8) e = launch_g3<8>(pb, ml, lo, ns, (int)M, out.G, s);
       else e = launch_g3<16>(pb, ml, lo, ns, (int)M, out.G, s);
       if (e != cudaSuccess) return e;
-      f2_q3_kernel<<<ns * pb.B, kF2Threads, 0, s>>>(pb, ml, lo, out.G, out);
+      if ((e = cudaMemsetAsync(out.counters + 2, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
+      f2_q3_kernel<<<out.q3_grid, kF2Threads, 0, s>>>(pb, ml, lo, ns, out.G, out);
       *n_launches += 2;
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }

@@ -74,9 +74,12 @@ struct F2Out {
   int32_t* G;                    // K = 3 quadrant-minimum tables, g_cap elements
   size_t g_cap;                  // >= f2_g3_elems_per_segment(B, M) for every model
   int32_t* F;                    // K = 2 prefix counts, >= C * C * B * M elements
+  uint16_t *PF, *PFs, *SF, *SFs;  // inverse stage tables, >= C * B * B * M elements each
+  int q3_grid;                    // persistent K = 3 query CTAs
 };
 constexpr uint32_t kF2MaxLayers = 4096;  // a G row (M - 2 values) is staged in shared memory
 size_t f2_g3_elems_per_segment(int B, uint32_t M);
+int f2_q3_grid(int device);  // persistent grid of the K = 3 query kernel
 cudaError_t launch_f2_model(const Problem& pb, int local_model, uint32_t M, int Kmax, const F2Out& out,
                             cudaStream_t s, int* n_launches);
 
