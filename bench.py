@@ -169,6 +169,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the SLO-sweep (frontier_at) measurement")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-f2", action="store_true", help="skip the F2 (MILP-lossless frontier) measurement")
     ap.add_argument("--models", type=int, default=None, help="config 5 only: first N models (profiling)")
     ap.add_argument("--margin", type=int, default=None, help="override margin_permille (experiments)")
     args = ap.parse_args()
@@ -367,6 +368,30 @@ def main():
         prepart = {"models": len(lat_h), "n_blocks": nblk, "ms": (time.perf_counter() - t0) * 1e3,
                    "ref": "class 1, batch index 0", "timing": "host wall clock around ppipe_prepartition "
                    "(H2D of the layer profiles, two kernels, D2H of bounds and block profiles)"}
+    # ---- F2, the MILP-lossless frontier, on config 4: one blocking
+    # ppipe_pareto_f2 per rep (pack, enumerate, strict-dominance queries, tie runs, sort) ----
+    f2 = None
+    if rank == 0 and not args.no_f2:
+        from workloads import CONFIG_NAMES, config4
+        w4 = config4()
+        c4 = pp.load_workload(w4, device=local_rank)
+        try:
+            pp.pareto_f2(c4, w4.kmax, w4.slo_us, w4.margin_permille, copy_to_host=False)  # warm
+            reps, dev_ms, wall = 3, [], []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                r4 = pp.pareto_f2(c4, w4.kmax, w4.slo_us, w4.margin_permille, copy_to_host=False)
+                wall.append((time.perf_counter() - t0) * 1e3)
+                dev_ms.append(sum(c4.phase_ms()))
+            f2 = {"workload": "config 4: " + CONFIG_NAMES[4], "candidates": r4.n_candidates,
+                  "feasible": r4.n_feasible, "strict_survivors": r4.n_survivors, "points": r4.n_points,
+                  "device_ms": statistics.median(dev_ms), "wall_ms": statistics.median(wall),
+                  "candidates_per_s": r4.n_candidates / (statistics.median(wall) / 1e3),
+                  "launches": c4.launch_count(),
+                  "timing": "median of 3 blocking ppipe_pareto_f2 calls, inputs resident; device_ms = sum of "
+                            "the CUDA-event phases (pack, enumerate+queries, ties+sort), wall_ms = host clock"}
+        finally:
+            pp.free(c4)
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -403,6 +428,7 @@ def main():
         "phase_ms": phase_avg,
         "slo_sweep": sweep,
         "prepartition": prepart,
+        "f2": f2,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

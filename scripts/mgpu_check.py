@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--oracle", action="store_true", help="also compare with the CPU oracle (small configs)")
     ap.add_argument("--vgpu", type=str, default=None, help="comma-separated per-class virtual-GPU counts")
     ap.add_argument("--async-upload", action="store_true", help="load scaled values, then update_profiles_async")
+    ap.add_argument("--f2", action="store_true", help="F2 frontier (ppipe_pareto_f2): owned models + all-gather")
     args = ap.parse_args()
 
     import numpy as np
@@ -63,7 +64,7 @@ def main():
         finally:
             pp.free(ctx)
     else:
-        g = pp.run(w, rank=rank, world=world, device=local, nccl_id=nid, vgpu=vgpu)
+        g = pp.run(w, rank=rank, world=world, device=local, nccl_id=nid, vgpu=vgpu, frontier=2 if args.f2 else 1)
     digest = hashlib.sha256(g.points.tobytes() + g.seg_offsets.tobytes()).hexdigest()
     digests = [None] * world
     dist.all_gather_object(digests, (digest, g.n_candidates, g.n_feasible, g.n_points))
@@ -72,7 +73,7 @@ def main():
         if len(set(digests)) != 1:
             print("ranks disagree:", digests)
             ok = False
-        single = pp.run(w, device=local, vgpu=vgpu)
+        single = pp.run(w, device=local, vgpu=vgpu, frontier=2 if args.f2 else 1)
         if not (np.array_equal(single.points.view(np.uint8), g.points.view(np.uint8))
                 and np.array_equal(single.seg_offsets, g.seg_offsets)
                 and single.n_candidates == g.n_candidates and single.n_feasible == g.n_feasible):
@@ -81,7 +82,7 @@ def main():
             ok = False
         if args.oracle:
             from oracle import run_oracle
-            o = run_oracle(w, vgpu=vgpu)
+            o = run_oracle(w, vgpu=vgpu, frontier=2 if args.f2 else 1)
             if not (np.array_equal(o.points.view(np.uint8), g.points.view(np.uint8))
                     and o.n_candidates == g.n_candidates and o.n_feasible == g.n_feasible):
                 print("multi-GPU result differs from the oracle")
