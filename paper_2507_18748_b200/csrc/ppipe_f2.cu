@@ -45,24 +45,6 @@ __device__ __forceinline__ const int32_t* yrow(const Problem& pb, const DevModel
   return pb.Y + md.y_off + ((size_t)pb.pair_v[k * pb.C + k2] * pb.B + bi) * md.Mp;
 }
 
-// Exclusive suffix minimum over the threads of a block (threads t' > t).
-__device__ __forceinline__ int32_t block_suffix_excl_min(int32_t v, int32_t* sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int32_t inc = v;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int32_t o = __shfl_down_sync(0xffffffffu, inc, off);
-    if (lane + off < 32) inc = min(inc, o);
-  }
-  if (lane == 0) sh[warp] = inc;
-  int32_t excl = __shfl_down_sync(0xffffffffu, inc, 1);
-  if (lane == 31) excl = kInf;
-  __syncthreads();
-  for (int w = warp + 1; w < nw; ++w) excl = min(excl, sh[w]);
-  __syncthreads();
-  return excl;
-}
-
 // Warp-aggregated append of one record per lane that wants it.
 __device__ __forceinline__ void emit_point(bool want, const ppipe_point& p, const F2Out& out) {
   const unsigned m = __ballot_sync(0xffffffffu, want);
@@ -99,106 +81,166 @@ __device__ __forceinline__ ppipe_point make_point(const DevModel& md, int K, int
 
 // ---------------------------------------------------------------------------
 // K = 3: G tables. CTA per (segment in chunk, batch b'). Row u = c'_1 in 1..M-2,
-// column l = c'_2 in 2..M-1 (n = M - 2 of each). Thread t holds columns
-// j = t * IT + i (blocked); G[u][l] = min(G[u-1][l], min_{l' >= l} H[u][l']) with
-// H[u][l] = C'_2 if (u < l and feasible) else +inf.
+// column l = c'_2 in 2..M-1 (n = M - 2 of each; rows padded to g_pitch(n)). Thread t
+// holds columns j = t * IT + i (blocked); G[u][l] = min(G[u-1][l], min_{l' >= l} H[u][l'])
+// with H[u][l] = C'_2 if (u < l and feasible) else +inf, and
 // E' = (P1[u] - P2[u] + Y12[u]) + (P2[l] + P3[M] - P3[l] + Y23[l]) = a(u) + e(l).
+// R rows per step share one barrier (the cross-warp part of R suffix scans, double-
+// buffered); each thread stores its IT columns of a row as IT/4 vector stores.
+__host__ __device__ __forceinline__ int g_pitch(int n) { return (n + 15) & ~15; }
+
 template <int IT>
+__device__ __forceinline__ void store_cols(int32_t* dst, const int32_t (&v)[IT]) {
+  if constexpr (IT == 1) {
+    dst[0] = v[0];
+  } else if constexpr (IT == 2) {
+    *reinterpret_cast<int2*>(dst) = make_int2(v[0], v[1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < IT; i += 4) *reinterpret_cast<int4*>(dst + i) = make_int4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+  }
+}
+
+template <int IT, int R>
 __global__ void __launch_bounds__(kF2Threads) f2_g3_kernel(Problem pb, int ml, int seg_lo, int32_t* G) {
-  extern __shared__ int32_t row_sh[];
-  __shared__ int32_t sh[32];
+  __shared__ int32_t sh[2][R][kF2Threads / 32];
   const DevModel md = pb.models[ml];
-  const int M = (int)md.M, n = M - 2, C = pb.C, B = pb.B;
+  const int M = (int)md.M, n = M - 2, pitch = g_pitch(n), C = pb.C, B = pb.B;
   const int bq = blockIdx.x % B, seg = seg_lo + blockIdx.x / B;
   const int k1 = seg / (C * C), k2 = (seg / C) % C, k3 = seg % C;
   const int32_t *P1 = prow(pb, md, k1, bq), *P2 = prow(pb, md, k2, bq), *P3 = prow(pb, md, k3, bq);
   const int32_t *Y12 = yrow(pb, md, k1, k2, bq), *Y23 = yrow(pb, md, k2, k3, bq);
   const int32_t T = md.T, P3M = P3[M];
-  int32_t* Gs = G + (size_t)blockIdx.x * n * n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kF2Threads / 32;
+  const int j0 = threadIdx.x * IT;
+  const bool writer = j0 < pitch;
+  int32_t* Gs = G + (size_t)blockIdx.x * n * pitch + j0;
   int32_t e[IT], p2l[IT], prev[IT];
 #pragma unroll
   for (int i = 0; i < IT; ++i) {
-    const int j = threadIdx.x * IT + i, l = j + 2;
-    e[i] = j < n ? P2[l] + (P3M - P3[l]) + Y23[l] : kInf;
+    const int j = j0 + i, l = j + 2;
+    e[i] = j < n ? P2[l] + (P3M - P3[l]) + Y23[l] : 0;
     p2l[i] = j < n ? P2[l] : 0;
     prev[i] = kInf;
   }
-  for (int u = 1; u <= M - 2; ++u) {
-    const int32_t a = P1[u] - P2[u] + Y12[u], p2u = P2[u];
-    int32_t h[IT], run = kInf;
+  int par = 0;
+  for (int u0 = 1; u0 <= M - 2; u0 += R, par ^= 1) {
+    int32_t h[R][IT], inc[R];
 #pragma unroll
-    for (int i = IT - 1; i >= 0; --i) {
-      const int j = threadIdx.x * IT + i;
-      const bool ok = j < n && j + 2 > u && e[i] != kInf && a + e[i] <= T;
-      run = min(run, ok ? p2l[i] - p2u : kInf);
-      h[i] = run;
+    for (int r = 0; r < R; ++r) {
+      const int u = u0 + r;
+      const bool rv = u <= M - 2;
+      const int32_t a = rv ? P1[u] - P2[u] + Y12[u] : 0, p2u = rv ? P2[u] : 0;
+      int32_t run = kInf;
+#pragma unroll
+      for (int i = IT - 1; i >= 0; --i) {
+        const int j = j0 + i;
+        const bool ok = rv && j < n && j + 2 > u && a + e[i] <= T;
+        run = min(run, ok ? p2l[i] - p2u : kInf);
+        h[r][i] = run;
+      }
+      inc[r] = run;
     }
-    const int32_t later = block_suffix_excl_min(run, sh);
+    // R warp-level inclusive suffix scans, interleaved
 #pragma unroll
-    for (int i = 0; i < IT; ++i) {
-      const int j = threadIdx.x * IT + i;
-      prev[i] = min(prev[i], min(h[i], later));
-      if (j < n) row_sh[j] = prev[i];
+    for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int32_t o = __shfl_down_sync(0xffffffffu, inc[r], off);
+        if (lane + off < 32) inc[r] = min(inc[r], o);
+      }
+    }
+    int32_t later[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (lane == 0) sh[par][r][warp] = inc[r];
+      later[r] = __shfl_down_sync(0xffffffffu, inc[r], 1);
+      if (lane == 31) later[r] = kInf;
     }
     __syncthreads();
-    int32_t* out = Gs + (size_t)(u - 1) * n;
-    for (int j = threadIdx.x; j < n; j += blockDim.x) out[j] = row_sh[j];
-    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      for (int w = warp + 1; w < nw; ++w) later[r] = min(later[r], sh[par][r][w]);
+      if (u0 + r <= M - 2) {
+#pragma unroll
+        for (int i = 0; i < IT; ++i) prev[i] = min(prev[i], min(h[r][i], later[r]));
+        if (writer) store_cols<IT>(Gs + (size_t)(u0 + r - 1) * pitch, prev);
+      }
+    }
   }
 }
 
-// Inverse stage tables (per model; B x B x M per class, u16, c in [1, M-1]):
-//   PF[k][b][b'][c]  = last c' in [1, M-1] with P_{k,b'}[c'] * b <= P_{k,b}[c] * b'  (0 = none)
-//   SF[k][b][b'][c]  = first c' in [1, M-1] with (P_{k,b'}[M] - P_{k,b'}[c']) * b
+// Inverse stage tables (per model, u16, c in [1, M-1]; layout [k][b][c][b'] with b'
+// padded to Bp = 4 * ceil(B / 4), so the four tables' entries for 4 consecutive b'
+// are one 8-byte load):
+//   PF[k][b][c][b']  = last c' in [1, M-1] with P_{k,b'}[c'] * b <= P_{k,b}[c] * b'  (0 = none)
+//   SF[k][b][c][b']  = first c' in [1, M-1] with (P_{k,b'}[M] - P_{k,b'}[c']) * b
 //                      <= (P_{k,b}[M] - P_{k,b}[c]) * b'                              (M = none)
 // and the strict (<) versions PFs / SFs. A first stage [0, c) at batch b is matched or
 // beaten at b' exactly by the cuts c' <= PF (C'_1 non-decreasing in c'); a last stage
 // [c, M) by the cuts c' >= SF. K = 3 clamps them to [1, M-2] / [2, M-1].
+__host__ __device__ __forceinline__ int b_pad(int B) { return (B + 3) & ~3; }
+
+__device__ __forceinline__ size_t inv_at(int k, int bi, int c, int B, int M) {
+  return (((size_t)k * B + bi) * M + c) * b_pad(B);
+}
+
+constexpr int kInvSplit = 8;  // CTAs per (class, batch)
+
 __global__ void __launch_bounds__(kF2Threads) f2_inv_kernel(Problem pb, int ml, F2Out out) {
   const DevModel md = pb.models[ml];
-  const int M = (int)md.M, B = pb.B;
-  const int bq = blockIdx.x % B, bi = (blockIdx.x / B) % B, k = blockIdx.x / (B * B);
-  const int32_t *P = prow(pb, md, k, bi), *Q = prow(pb, md, k, bq);
-  const uint64_t b = pb.batches[bi], bv = pb.batches[bq];
-  const int64_t PM = P[M], QM = Q[M];
-  const size_t row = ((size_t)blockIdx.x) * M;
-  for (int c = 1 + threadIdx.x; c <= M - 1; c += blockDim.x) {
-    const uint64_t r1 = (uint64_t)P[c] * bv, r2 = (uint64_t)(PM - P[c]) * bv;
-    // prefix stage: largest c' with Q[c'] * b <= r1 (resp. < r1)
-    int lo = 1, hi = M;  // first c' failing, in [1, M]
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if ((uint64_t)Q[mid] * b <= r1) lo = mid + 1;
-      else hi = mid;
+  const int M = (int)md.M, B = pb.B, Bp = b_pad(B);
+  const int part = blockIdx.x % kInvSplit, bi = (blockIdx.x / kInvSplit) % B, k = blockIdx.x / (kInvSplit * B);
+  const int32_t* P = prow(pb, md, k, bi);
+  const uint64_t b = pb.batches[bi];
+  const int64_t PM = P[M];
+  const size_t base = inv_at(k, bi, 0, B, M);
+  for (int t = part * kF2Threads + threadIdx.x; t < (M - 1) * Bp; t += kInvSplit * kF2Threads) {
+    const int c = 1 + t / Bp, bq = t % Bp;
+    int pf = 0, pfs = 0, sf = M, sfs = M;
+    if (bq < B) {
+      const int32_t* Q = prow(pb, md, k, bq);
+      const uint64_t bv = pb.batches[bq];
+      const int64_t QM = Q[M];
+      const uint64_t r1 = (uint64_t)P[c] * bv, r2 = (uint64_t)(PM - P[c]) * bv;
+      // prefix stage: largest c' with Q[c'] * b <= r1 (resp. < r1)
+      int lo = 1, hi = M;  // first c' failing, in [1, M]
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((uint64_t)Q[mid] * b <= r1) lo = mid + 1;
+        else hi = mid;
+      }
+      pf = lo - 1;
+      lo = 1;
+      hi = pf + 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((uint64_t)Q[mid] * b < r1) lo = mid + 1;
+        else hi = mid;
+      }
+      pfs = lo - 1;
+      // suffix stage: smallest c' with (QM - Q[c']) * b <= r2 (resp. < r2); non-increasing in c'
+      lo = 1;
+      hi = M;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((uint64_t)(QM - Q[mid]) * b <= r2) hi = mid;
+        else lo = mid + 1;
+      }
+      sf = lo;
+      hi = M;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((uint64_t)(QM - Q[mid]) * b < r2) hi = mid;
+        else lo = mid + 1;
+      }
+      sfs = lo;
     }
-    const int pf = lo - 1;
-    lo = 1;
-    hi = pf + 1;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if ((uint64_t)Q[mid] * b < r1) lo = mid + 1;
-      else hi = mid;
-    }
-    const int pfs = lo - 1;
-    // suffix stage: smallest c' with (QM - Q[c']) * b <= r2 (resp. < r2); non-increasing in c'
-    lo = 1;
-    hi = M;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if ((uint64_t)(QM - Q[mid]) * b <= r2) hi = mid;
-      else lo = mid + 1;
-    }
-    const int sf = lo;
-    hi = M;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if ((uint64_t)(QM - Q[mid]) * b < r2) hi = mid;
-      else lo = mid + 1;
-    }
-    out.PF[row + c] = (uint16_t)pf;
-    out.PFs[row + c] = (uint16_t)pfs;
-    out.SF[row + c] = (uint16_t)sf;
-    out.SFs[row + c] = (uint16_t)lo;
+    const size_t at = base + (size_t)c * Bp + bq;
+    out.PF[at] = (uint16_t)pf;
+    out.PFs[at] = (uint16_t)pfs;
+    out.SF[at] = (uint16_t)sf;
+    out.SFs[at] = (uint16_t)sfs;
   }
 }
 
@@ -206,43 +248,57 @@ __global__ void __launch_bounds__(kF2Threads) f2_inv_kernel(Problem pb, int ml, 
 // segment-major order (the rows in flight share one segment's G tables in L2). A
 // warp scans its row 32 c_2 at a time, appends the feasible c_2 to a per-warp list
 // and, whenever 32 are queued, runs one candidate per lane through the batches b'
-// (largest first, exit on the first dominator):
+// (largest first, four at a time, exit on the first dominator):
 //   u = PF_{k1}[c_1], l = SF_{k3}[c_2]; G[u][l] * b > C_2 b'  => nothing at b' (the
 //   strict variants read G at (us, l) / (u, ls), which are >= G[u][l]);
 //   G[u][l] * b < C_2 b' => dominated (strict in stage 2); equal => check
 //   G[us][l] * b <= C_2 b' (strict in stage 1) and G[u][ls] * b <= C_2 b' (stage 3).
 constexpr int kQ3Warps = kF2Threads / 32;
 
+__device__ __forceinline__ int u16_at(const uint2& v, int i) {
+  return (int)(((i < 2 ? v.x : v.y) >> (16 * (i & 1))) & 0xFFFFu);
+}
+
 __device__ __forceinline__ bool f2_dominated3(const Problem& pb, const F2Out& out, int M, int B, int k1, int k3,
                                               int bi, int c1, int c2, uint32_t b, int32_t C2, const int32_t* Gseg) {
-  const int n = M - 2;
-  const size_t row1 = ((size_t)k1 * B + bi) * B, row3 = ((size_t)k3 * B + bi) * B;
-  for (int bq = B - 1; bq >= 0; --bq) {
-    const int u = min((int)out.PF[(row1 + bq) * M + c1], M - 2);
-    if (u < 1) continue;
-    const int l = max((int)out.SF[(row3 + bq) * M + c2], 2);
-    if (l > M - 1) continue;
-    const int32_t* Gb = Gseg + (size_t)bq * n * n;
-    const int32_t g = Gb[(size_t)(u - 1) * n + (l - 2)];
-    if (g == kInf) continue;
-    const uint64_t r2 = (uint64_t)C2 * pb.batches[bq], gb = (uint64_t)g * b;
-    if (gb > r2) continue;
-    if (gb < r2) return true;
-    const int us = min((int)out.PFs[(row1 + bq) * M + c1], M - 2);
-    if (us >= 1) {
-      const int32_t g1 = Gb[(size_t)(us - 1) * n + (l - 2)];
-      if (g1 != kInf && (uint64_t)g1 * b <= r2) return true;
+  const int n = M - 2, pitch = g_pitch(n), Bp = b_pad(B);
+  const size_t at1 = inv_at(k1, bi, c1, B, M), at3 = inv_at(k3, bi, c2, B, M);
+  const size_t gstride = (size_t)n * pitch;
+  for (int q = Bp / 4 - 1; q >= 0; --q) {
+    const uint2 pf4 = *reinterpret_cast<const uint2*>(out.PF + at1 + 4 * q);
+    const uint2 sf4 = *reinterpret_cast<const uint2*>(out.SF + at3 + 4 * q);
+    int32_t g[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int bq = 4 * q + i, u = min(u16_at(pf4, i), M - 2), l = max(u16_at(sf4, i), 2);
+      g[i] = (bq < B && u >= 1 && l <= M - 1) ? Gseg[bq * gstride + (size_t)(u - 1) * pitch + (l - 2)] : kInf;
     }
-    const int ls = max((int)out.SFs[(row3 + bq) * M + c2], 2);
-    if (ls <= M - 1) {
-      const int32_t g3 = Gb[(size_t)(u - 1) * n + (ls - 2)];
-      if (g3 != kInf && (uint64_t)g3 * b <= r2) return true;
+#pragma unroll
+    for (int i = 3; i >= 0; --i) {
+      if (g[i] == kInf) continue;
+      const int bq = 4 * q + i;
+      const uint64_t r2 = (uint64_t)C2 * pb.batches[bq], gb = (uint64_t)g[i] * b;
+      if (gb > r2) continue;
+      if (gb < r2) return true;
+      // G[u][l] * b == C_2 b': a pair strictly better in stage 1 or stage 3 decides
+      const int u = min(u16_at(pf4, i), M - 2), l = max(u16_at(sf4, i), 2);
+      const int32_t* Gb = Gseg + bq * gstride;
+      const int us = min((int)out.PFs[at1 + bq], M - 2);
+      if (us >= 1) {
+        const int32_t g1 = Gb[(size_t)(us - 1) * pitch + (l - 2)];
+        if (g1 != kInf && (uint64_t)g1 * b <= r2) return true;
+      }
+      const int ls = max((int)out.SFs[at3 + bq], 2);
+      if (ls <= M - 1) {
+        const int32_t g3 = Gb[(size_t)(u - 1) * pitch + (ls - 2)];
+        if (g3 != kInf && (uint64_t)g3 * b <= r2) return true;
+      }
     }
   }
   return false;
 }
 
-__global__ void __launch_bounds__(kF2Threads) f2_q3_kernel(Problem pb, int ml, int seg_lo, int nseg,
+__global__ void __launch_bounds__(kF2Threads, 4) f2_q3_kernel(Problem pb, int ml, int seg_lo, int nseg,
                                                            const int32_t* G, F2Out out) {
   __shared__ int32_t list[kQ3Warps][64];
   const DevModel md = pb.models[ml];
@@ -266,7 +322,7 @@ __global__ void __launch_bounds__(kF2Threads) f2_q3_kernel(Problem pb, int ml, i
     const int32_t *Y12 = yrow(pb, md, k1, k2, bi), *Y23 = yrow(pb, md, k2, k3, bi);
     const int32_t P3M = P3[M], C1 = P1[c1], p2c1 = P2[c1], a = C1 - p2c1 + Y12[c1];
     const uint32_t b = pb.batches[bi];
-    const int32_t* Gseg = G + (size_t)segc * B * n * n;
+    const int32_t* Gseg = G + (size_t)segc * B * n * g_pitch(n);
     int cnt = 0;
     for (int base = c1 + 1; base <= M - 1 || cnt > 0; base += 32) {
       if (base <= M - 1) {
@@ -342,7 +398,6 @@ __global__ void __launch_bounds__(kF2Threads) f2_q2_kernel(Problem pb, int ml, c
   const int32_t *P1 = prow(pb, md, k1, bi), *P2 = prow(pb, md, k2, bi), *Y12 = yrow(pb, md, k1, k2, bi);
   const int32_t T = md.T, P2M = P2[M];
   const uint32_t b = pb.batches[bi];
-  const size_t row1 = ((size_t)k1 * B + bi) * B, row2 = ((size_t)k2 * B + bi) * B;
   unsigned long long feas = 0;
   for (int c0 = 1; c0 <= M - 1; c0 += blockDim.x) {
     const int c = c0 + threadIdx.x;
@@ -356,9 +411,10 @@ __global__ void __launch_bounds__(kF2Threads) f2_q2_kernel(Problem pb, int ml, c
         ++feas;
         bool dom = false;
         for (int bq = B - 1; bq >= 0 && !dom; --bq) {
-          const int u = out.PF[(row1 + bq) * M + c], l = out.SF[(row2 + bq) * M + c];
+          const size_t a1 = inv_at(k1, bi, c, B, M) + bq, a2 = inv_at(k2, bi, c, B, M) + bq;
+          const int u = out.PF[a1], l = out.SF[a2];
           if (u < l) continue;
-          const int us = out.PFs[(row1 + bq) * M + c], ls = out.SFs[(row2 + bq) * M + c];
+          const int us = out.PFs[a1], ls = out.SFs[a2];
           const int32_t* Fb = F + ((size_t)seg * B + bq) * M;
           dom = (us >= l && Fb[us] - Fb[l - 1] > 0) || (ls <= u && Fb[u] - Fb[ls - 1] > 0);
         }
@@ -402,14 +458,9 @@ __global__ void __launch_bounds__(kF2Threads) f2_q1_kernel(Problem pb, int ml, F
   if ((threadIdx.x & 31) == 0 && feas) atomicAdd(&out.counters[1], feas);
 }
 
-template <int IT>
-cudaError_t launch_g3(const Problem& pb, int ml, int seg_lo, int nseg, int M, int32_t* G, cudaStream_t s) {
-  const size_t smem = sizeof(int32_t) * (size_t)(M - 2);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(f2_g3_kernel<IT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  f2_g3_kernel<IT><<<nseg * pb.B, kF2Threads, smem, s>>>(pb, ml, seg_lo, G);
+template <int IT, int R>
+cudaError_t launch_g3(const Problem& pb, int ml, int seg_lo, int nseg, int32_t* G, cudaStream_t s) {
+  f2_g3_kernel<IT, R><<<nseg * pb.B, kF2Threads, 0, s>>>(pb, ml, seg_lo, G);
   return cudaGetLastError();
 }
 
@@ -424,7 +475,7 @@ int f2_q3_grid(int device) {
 
 size_t f2_g3_elems_per_segment(int B, uint32_t M) {
   const size_t n = M >= 3 ? M - 2 : 0;
-  return (size_t)B * n * n;
+  return (size_t)B * n * g_pitch((int)n);
 }
 
 cudaError_t launch_f2_model(const Problem& pb, int ml, uint32_t M, int Kmax, const F2Out& out, cudaStream_t s,
@@ -435,7 +486,7 @@ cudaError_t launch_f2_model(const Problem& pb, int ml, uint32_t M, int Kmax, con
   ++*n_launches;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (Kmax >= 2 && M >= 2) {
-    f2_inv_kernel<<<C * pb.B * pb.B, kF2Threads, 0, s>>>(pb, ml, out);
+    f2_inv_kernel<<<C * pb.B * kInvSplit, kF2Threads, 0, s>>>(pb, ml, out);
     ++*n_launches;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
@@ -452,11 +503,11 @@ cudaError_t launch_f2_model(const Problem& pb, int ml, uint32_t M, int Kmax, con
     const int n = (int)M - 2, it = (n + kF2Threads - 1) / kF2Threads;
     for (int lo = 0; lo < nseg_all; lo += chunk) {
       const int ns = std::min(chunk, nseg_all - lo);
-      if (it <= 1) e = launch_g3<1>(pb, ml, lo, ns, (int)M, out.G, s);
-      else if (it <= 2) e = launch_g3<2>(pb, ml, lo, ns, (int)M, out.G, s);
-      else if (it <= 4) e = launch_g3<4>(pb, ml, lo, ns, (int)M, out.G, s);
-      else if (it <= 8) e = launch_g3<8>(pb, ml, lo, ns, (int)M, out.G, s);
-      else e = launch_g3<16>(pb, ml, lo, ns, (int)M, out.G, s);
+      if (it <= 1) e = launch_g3<1, 4>(pb, ml, lo, ns, out.G, s);
+      else if (it <= 2) e = launch_g3<2, 4>(pb, ml, lo, ns, out.G, s);
+      else if (it <= 4) e = launch_g3<4, 4>(pb, ml, lo, ns, out.G, s);
+      else if (it <= 8) e = launch_g3<8, 2>(pb, ml, lo, ns, out.G, s);
+      else e = launch_g3<16, 1>(pb, ml, lo, ns, out.G, s);
       if (e != cudaSuccess) return e;
       if ((e = cudaMemsetAsync(out.counters + 2, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
       f2_q3_kernel<<<out.q3_grid, kF2Threads, 0, s>>>(pb, ml, lo, ns, out.G, out);

@@ -74,7 +74,7 @@ struct F2Out {
   int32_t* G;                    // K = 3 quadrant-minimum tables, g_cap elements
   size_t g_cap;                  // >= f2_g3_elems_per_segment(B, M) for every model
   int32_t* F;                    // K = 2 prefix counts, >= C * C * B * M elements
-  uint16_t *PF, *PFs, *SF, *SFs;  // inverse stage tables, >= C * B * B * M elements each
+  uint16_t *PF, *PFs, *SF, *SFs;  // inverse stage tables, >= C * B * 4 ceil(B / 4) * M elements each
   int q3_grid;                    // persistent K = 3 query CTAs
 };
 constexpr uint32_t kF2MaxLayers = 4096;  // a G row (M - 2 values) is staged in shared memory
