@@ -82,28 +82,21 @@ __device__ __forceinline__ ppipe_point make_point(const DevModel& md, int K, int
 // ---------------------------------------------------------------------------
 // K = 3: G tables. CTA per (segment in chunk, batch b'). Row u = c'_1 in 1..M-2,
 // column l = c'_2 in 2..M-1 (n = M - 2 of each; rows padded to g_pitch(n)). Thread t
-// holds columns j = t * IT + i (blocked); G[u][l] = min(G[u-1][l], min_{l' >= l} H[u][l'])
+// holds columns j = 16 t + i (blocked); G[u][l] = min(G[u-1][l], min_{l' >= l} H[u][l'])
 // with H[u][l] = C'_2 if (u < l and feasible) else +inf, and
 // E' = (P1[u] - P2[u] + Y12[u]) + (P2[l] + P3[M] - P3[l] + Y23[l]) = a(u) + e(l).
-// R rows per step share one barrier (the cross-warp part of R suffix scans, double-
-// buffered); each thread stores its IT columns of a row as IT/4 vector stores.
+// Warp w owns columns [512 w, 512 w + 512), 16 per lane: the row's suffix minimum is a
+// thread-local pass, one warp scan and (W > 1 warps) one exchange through shared
+// memory (double-buffered: one barrier per row). Each lane stores its 16 columns of a
+// row as four 16-byte stores into the padded row pitch.
 __host__ __device__ __forceinline__ int g_pitch(int n) { return (n + 15) & ~15; }
 
-template <int IT>
-__device__ __forceinline__ void store_cols(int32_t* dst, const int32_t (&v)[IT]) {
-  if constexpr (IT == 1) {
-    dst[0] = v[0];
-  } else if constexpr (IT == 2) {
-    *reinterpret_cast<int2*>(dst) = make_int2(v[0], v[1]);
-  } else {
-#pragma unroll
-    for (int i = 0; i < IT; i += 4) *reinterpret_cast<int4*>(dst + i) = make_int4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-  }
-}
+constexpr int kG3Cols = 16;  // columns per lane
 
-template <int IT, int R>
-__global__ void __launch_bounds__(kF2Threads) f2_g3_kernel(Problem pb, int ml, int seg_lo, int32_t* G) {
-  __shared__ int32_t sh[2][R][kF2Threads / 32];
+template <int W>
+__global__ void __launch_bounds__(32 * W) f2_g3_kernel(Problem pb, int ml, int seg_lo, int32_t* G) {
+  constexpr int IT = kG3Cols;
+  __shared__ int32_t sh[2][W];
   const DevModel md = pb.models[ml];
   const int M = (int)md.M, n = M - 2, pitch = g_pitch(n), C = pb.C, B = pb.B;
   const int bq = blockIdx.x % B, seg = seg_lo + blockIdx.x / B;
@@ -111,7 +104,7 @@ __global__ void __launch_bounds__(kF2Threads) f2_g3_kernel(Problem pb, int ml, i
   const int32_t *P1 = prow(pb, md, k1, bq), *P2 = prow(pb, md, k2, bq), *P3 = prow(pb, md, k3, bq);
   const int32_t *Y12 = yrow(pb, md, k1, k2, bq), *Y23 = yrow(pb, md, k2, k3, bq);
   const int32_t T = md.T, P3M = P3[M];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kF2Threads / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j0 = threadIdx.x * IT;
   const bool writer = j0 < pitch;
   int32_t* Gs = G + (size_t)blockIdx.x * n * pitch + j0;
@@ -124,48 +117,38 @@ __global__ void __launch_bounds__(kF2Threads) f2_g3_kernel(Problem pb, int ml, i
     prev[i] = kInf;
   }
   int par = 0;
-  for (int u0 = 1; u0 <= M - 2; u0 += R, par ^= 1) {
-    int32_t h[R][IT], inc[R];
+  for (int u = 1; u <= M - 2; ++u, par ^= 1) {
+    const int32_t a = P1[u] - P2[u] + Y12[u], p2u = P2[u];
+    int32_t h[IT], run = kInf;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int u = u0 + r;
-      const bool rv = u <= M - 2;
-      const int32_t a = rv ? P1[u] - P2[u] + Y12[u] : 0, p2u = rv ? P2[u] : 0;
-      int32_t run = kInf;
-#pragma unroll
-      for (int i = IT - 1; i >= 0; --i) {
-        const int j = j0 + i;
-        const bool ok = rv && j < n && j + 2 > u && a + e[i] <= T;
-        run = min(run, ok ? p2l[i] - p2u : kInf);
-        h[r][i] = run;
-      }
-      inc[r] = run;
+    for (int i = IT - 1; i >= 0; --i) {
+      const int j = j0 + i;
+      const bool ok = j < n && j + 2 > u && a + e[i] <= T;
+      run = min(run, ok ? p2l[i] - p2u : kInf);
+      h[i] = run;
     }
-    // R warp-level inclusive suffix scans, interleaved
+    int32_t inc = run;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int32_t o = __shfl_down_sync(0xffffffffu, inc[r], off);
-        if (lane + off < 32) inc[r] = min(inc[r], o);
-      }
+      const int32_t o = __shfl_down_sync(0xffffffffu, inc, off);
+      if (lane + off < 32) inc = min(inc, o);
     }
-    int32_t later[R];
+    int32_t later = __shfl_down_sync(0xffffffffu, inc, 1);
+    if (lane == 31) later = kInf;
+    if constexpr (W > 1) {
+      if (lane == 0) sh[par][warp] = inc;
+      __syncthreads();
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (lane == 0) sh[par][r][warp] = inc[r];
-      later[r] = __shfl_down_sync(0xffffffffu, inc[r], 1);
-      if (lane == 31) later[r] = kInf;
+      for (int w = 1; w < W; ++w)
+        if (w > warp) later = min(later, sh[par][w]);
     }
-    __syncthreads();
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      for (int w = warp + 1; w < nw; ++w) later[r] = min(later[r], sh[par][r][w]);
-      if (u0 + r <= M - 2) {
+    for (int i = 0; i < IT; ++i) prev[i] = min(prev[i], min(h[i], later));
+    if (writer) {
+      int32_t* dst = Gs + (size_t)(u - 1) * pitch;
 #pragma unroll
-        for (int i = 0; i < IT; ++i) prev[i] = min(prev[i], min(h[r][i], later[r]));
-        if (writer) store_cols<IT>(Gs + (size_t)(u0 + r - 1) * pitch, prev);
-      }
+      for (int i = 0; i < IT; i += 4)
+        if (j0 + i < pitch) *reinterpret_cast<int4*>(dst + i) = make_int4(prev[i], prev[i + 1], prev[i + 2], prev[i + 3]);
     }
   }
 }
@@ -458,9 +441,9 @@ __global__ void __launch_bounds__(kF2Threads) f2_q1_kernel(Problem pb, int ml, F
   if ((threadIdx.x & 31) == 0 && feas) atomicAdd(&out.counters[1], feas);
 }
 
-template <int IT, int R>
+template <int W>
 cudaError_t launch_g3(const Problem& pb, int ml, int seg_lo, int nseg, int32_t* G, cudaStream_t s) {
-  f2_g3_kernel<IT, R><<<nseg * pb.B, kF2Threads, 0, s>>>(pb, ml, seg_lo, G);
+  f2_g3_kernel<W><<<nseg * pb.B, 32 * W, 0, s>>>(pb, ml, seg_lo, G);
   return cudaGetLastError();
 }
 
@@ -500,14 +483,13 @@ cudaError_t launch_f2_model(const Problem& pb, int ml, uint32_t M, int Kmax, con
     const size_t per_seg = f2_g3_elems_per_segment(pb.B, M);
     const int nseg_all = C * C * C;
     int chunk = (int)std::min<size_t>((size_t)nseg_all, std::max<size_t>(1, out.g_cap / per_seg));
-    const int n = (int)M - 2, it = (n + kF2Threads - 1) / kF2Threads;
+    const int n = (int)M - 2, warps = (n + 32 * kG3Cols - 1) / (32 * kG3Cols);
     for (int lo = 0; lo < nseg_all; lo += chunk) {
       const int ns = std::min(chunk, nseg_all - lo);
-      if (it <= 1) e = launch_g3<1, 4>(pb, ml, lo, ns, out.G, s);
-      else if (it <= 2) e = launch_g3<2, 4>(pb, ml, lo, ns, out.G, s);
-      else if (it <= 4) e = launch_g3<4, 4>(pb, ml, lo, ns, out.G, s);
-      else if (it <= 8) e = launch_g3<8, 2>(pb, ml, lo, ns, out.G, s);
-      else e = launch_g3<16, 1>(pb, ml, lo, ns, out.G, s);
+      if (warps <= 1) e = launch_g3<1>(pb, ml, lo, ns, out.G, s);
+      else if (warps <= 2) e = launch_g3<2>(pb, ml, lo, ns, out.G, s);
+      else if (warps <= 4) e = launch_g3<4>(pb, ml, lo, ns, out.G, s);
+      else e = launch_g3<8>(pb, ml, lo, ns, out.G, s);
       if (e != cudaSuccess) return e;
       if ((e = cudaMemsetAsync(out.counters + 2, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
       f2_q3_kernel<<<out.q3_grid, kF2Threads, 0, s>>>(pb, ml, lo, ns, out.G, out);
