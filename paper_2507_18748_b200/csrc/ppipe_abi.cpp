@@ -234,7 +234,7 @@ struct ppipe_ctx {
   cudaEvent_t cev[kMaxChunks + 1] = {};
   DevBuf<unsigned long long> d_err;
   // F2 (ppipe_pareto_f2)
-  DevBuf<int32_t> d_G, d_F;
+  DevBuf<int32_t> d_G, d_F, d_E23;
   DevBuf<uint16_t> d_inv;  // F2 inverse stage tables PF, PFs, SF, SFs
   DevBuf<ppipe_point> d_f2surv, d_f2tmp;
   uint64_t f2_cap = 1ull << 20;
@@ -316,6 +316,7 @@ void free_ctx(ppipe_ctx* c) {
   c->d_err.release();
   c->d_G.release();
   c->d_F.release();
+  c->d_E23.release();
   c->d_inv.release();
   c->d_f2surv.release();
   c->d_f2tmp.release();
@@ -1220,6 +1221,7 @@ PPIPE_API int ppipe_pareto_f2(ppipe_ctx* c, const ppipe_enum_params* p, int copy
   for (int i : own) g_cap = std::max(g_cap, f2_g3_elems_per_segment((int)c->B, c->h_models[i].M));
   if (Kmax >= 3) CU(c, c->d_G.reserve(std::max<size_t>(g_cap, 1)));
   if (Kmax >= 2) CU(c, c->d_F.reserve(f_need));
+  if (Kmax >= 3) CU(c, c->d_E23.reserve(f_need));
   const size_t inv_n = f_need / c->C * ((c->B + 3) & ~3u);  // C * B * 4 ceil(B / 4) * max M
   if (Kmax >= 2) CU(c, c->d_inv.reserve(4 * inv_n));
   const int q3_grid = f2_q3_grid(c->device);
@@ -1227,7 +1229,8 @@ PPIPE_API int ppipe_pareto_f2(ppipe_ctx* c, const ppipe_enum_params* p, int copy
   for (int attempt = 0;; ++attempt) {
     CU(c, c->d_f2surv.reserve(c->f2_cap));
     F2Out fo{c->d_f2surv.p, c->d_counters.p, (unsigned long long)c->d_f2surv.n, c->d_G.p, c->d_G.n, c->d_F.p,
-             c->d_inv.p, c->d_inv.p + inv_n, c->d_inv.p + 2 * inv_n, c->d_inv.p + 3 * inv_n, q3_grid};
+             c->d_inv.p, c->d_inv.p + inv_n, c->d_inv.p + 2 * inv_n, c->d_inv.p + 3 * inv_n, c->d_E23.p,
+             q3_grid};
     nl = 0;
     CU(c, cudaEventRecord(c->ev[0], c->stream));
     CU(c, launch_pack(pb, c->stream));

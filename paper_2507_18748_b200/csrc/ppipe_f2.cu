@@ -237,6 +237,7 @@ __global__ void __launch_bounds__(kF2Threads) f2_inv_kernel(Problem pb, int ml, 
 //   G[u][l] * b < C_2 b' => dominated (strict in stage 2); equal => check
 //   G[us][l] * b <= C_2 b' (strict in stage 1) and G[u][ls] * b <= C_2 b' (stage 3).
 constexpr int kQ3Warps = kF2Threads / 32;
+constexpr int kQ3Rows = 4;  // c_1 rows per work unit
 
 __device__ __forceinline__ int u16_at(const uint2& v, int i) {
   return (int)(((i < 2 ? v.x : v.y) >> (16 * (i & 1))) & 0xFFFFu);
@@ -289,29 +290,33 @@ __global__ void __launch_bounds__(kF2Threads, 4) f2_q3_kernel(Problem pb, int ml
   const int32_t T = md.T;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int32_t* L = list[warp];
-  const unsigned long long n_units = (unsigned long long)nseg * B * n;
+  const int nq = (n + kQ3Rows - 1) / kQ3Rows;
+  const unsigned long long n_units = (unsigned long long)nseg * B * nq;
   unsigned long long feas = 0;
   for (;;) {
     unsigned long long unit = 0;
     if (lane == 0) unit = atomicAdd(&out.counters[2], 1ull);
     unit = __shfl_sync(0xffffffffu, unit, 0);
     if (unit >= n_units) break;
-    const int c1 = 1 + (int)(unit % n);
-    const int bi = (int)((unit / n) % B);
-    const int segc = (int)(unit / ((unsigned long long)n * B));
+    const int bi = (int)((unit / nq) % B);
+    const int segc = (int)(unit / ((unsigned long long)nq * B));
     const int seg = seg_lo + segc;
     const int k1 = seg / (C * C), k2 = (seg / C) % C, k3 = seg % C;
     const int32_t *P1 = prow(pb, md, k1, bi), *P2 = prow(pb, md, k2, bi), *P3 = prow(pb, md, k3, bi);
     const int32_t *Y12 = yrow(pb, md, k1, k2, bi), *Y23 = yrow(pb, md, k2, k3, bi);
-    const int32_t P3M = P3[M], C1 = P1[c1], p2c1 = P2[c1], a = C1 - p2c1 + Y12[c1];
+    const int32_t* E23 = out.E23 + ((size_t)(k2 * C + k3) * B + bi) * M;
+    const int32_t P3M = P3[M];
     const uint32_t b = pb.batches[bi];
     const int32_t* Gseg = G + (size_t)segc * B * n * g_pitch(n);
+    const int c1_lo = 1 + kQ3Rows * (int)(unit % nq), c1_hi = min(c1_lo + kQ3Rows - 1, M - 2);
+    for (int c1 = c1_lo; c1 <= c1_hi; ++c1) {
+    const int32_t C1 = P1[c1], p2c1 = P2[c1], a = C1 - p2c1 + Y12[c1];
     int cnt = 0;
     for (int base = c1 + 1; base <= M - 1 || cnt > 0; base += 32) {
       if (base <= M - 1) {
         const int c2 = base + lane;
         bool f = false;
-        if (c2 <= M - 1) f = a + P2[c2] + (P3M - P3[c2]) + Y23[c2] <= T;
+        if (c2 <= M - 1) f = a + E23[c2] <= T;
         const unsigned m = __ballot_sync(0xffffffffu, f);
         if (f) L[cnt + __popc(m & ((1u << lane) - 1))] = c2;
         cnt += __popc(m);
@@ -337,9 +342,22 @@ __global__ void __launch_bounds__(kF2Threads, 4) f2_q3_kernel(Problem pb, int ml
       __syncwarp();
       cnt = rest;
     }
+    }
   }
   for (int off = 16; off; off >>= 1) feas += __shfl_down_sync(0xffffffffu, feas, off);
   if (lane == 0 && feas) atomicAdd(&out.counters[1], feas);
+}
+
+// E23[k2][k3][b][c] = P_{k2,b}[c] + (P_{k3,b}[M] - P_{k3,b}[c]) + Y_{k2->k3,b}[c]: the part of a
+// K = 3 candidate's E that depends on its second cut (per class pair and batch).
+__global__ void __launch_bounds__(kF2Threads) f2_e23_kernel(Problem pb, int ml, int32_t* E23) {
+  const DevModel md = pb.models[ml];
+  const int M = (int)md.M, C = pb.C, B = pb.B;
+  const int bi = blockIdx.x % B, k3 = (blockIdx.x / B) % C, k2 = blockIdx.x / (B * C);
+  const int32_t *P2 = prow(pb, md, k2, bi), *P3 = prow(pb, md, k3, bi), *Y23 = yrow(pb, md, k2, k3, bi);
+  const int32_t P3M = P3[M];
+  int32_t* row = E23 + (size_t)blockIdx.x * M;
+  for (int c = threadIdx.x; c < M; c += blockDim.x) row[c] = P2[c] + (P3M - P3[c]) + Y23[c];
 }
 
 // K = 2: per (segment, b') prefix counts F[c] = #feasible c'_1 in [1, c], c = 0..M-1.
@@ -491,6 +509,10 @@ cudaError_t launch_f2_model(const Problem& pb, int ml, uint32_t M, int Kmax, con
       else if (warps <= 4) e = launch_g3<4>(pb, ml, lo, ns, out.G, s);
       else e = launch_g3<8>(pb, ml, lo, ns, out.G, s);
       if (e != cudaSuccess) return e;
+      if (lo == 0) {
+        f2_e23_kernel<<<C * C * pb.B, kF2Threads, 0, s>>>(pb, ml, out.E23);
+        ++*n_launches;
+      }
       if ((e = cudaMemsetAsync(out.counters + 2, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
       f2_q3_kernel<<<out.q3_grid, kF2Threads, 0, s>>>(pb, ml, lo, ns, out.G, out);
       *n_launches += 2;
