@@ -243,8 +243,12 @@ __device__ __forceinline__ int u16_at(const uint2& v, int i) {
   return (int)(((i < 2 ? v.x : v.y) >> (16 * (i & 1))) & 0xFFFFu);
 }
 
-__device__ __forceinline__ bool f2_dominated3(const Problem& pb, const F2Out& out, int M, int B, int k1, int k3,
-                                              int bi, int c1, int c2, uint32_t b, int32_t C2, const int32_t* Gseg) {
+// 1: some feasible candidate beats p in every stage (strictly in one); 0: none matches
+// it in every stage at another batch; 2: not dominated, but one may match it exactly at
+// another batch (G[u][l] * b == C_2 b'), so f2_finalize resolves it by its vector.
+__device__ __forceinline__ int f2_dominated3(const Problem& pb, const F2Out& out, int M, int B, int k1, int k3,
+                                             int bi, int c1, int c2, uint32_t b, int32_t C2, const int32_t* Gseg) {
+  int res = 0;
   const int n = M - 2, pitch = g_pitch(n), Bp = b_pad(B);
   const size_t at1 = inv_at(k1, bi, c1, B, M), at3 = inv_at(k3, bi, c2, B, M);
   const size_t gstride = (size_t)n * pitch;
@@ -263,23 +267,24 @@ __device__ __forceinline__ bool f2_dominated3(const Problem& pb, const F2Out& ou
       const int bq = 4 * q + i;
       const uint64_t r2 = (uint64_t)C2 * pb.batches[bq], gb = (uint64_t)g[i] * b;
       if (gb > r2) continue;
-      if (gb < r2) return true;
+      if (gb < r2) return 1;
       // G[u][l] * b == C_2 b': a pair strictly better in stage 1 or stage 3 decides
       const int u = min(u16_at(pf4, i), M - 2), l = max(u16_at(sf4, i), 2);
       const int32_t* Gb = Gseg + bq * gstride;
       const int us = min((int)out.PFs[at1 + bq], M - 2);
       if (us >= 1) {
         const int32_t g1 = Gb[(size_t)(us - 1) * pitch + (l - 2)];
-        if (g1 != kInf && (uint64_t)g1 * b <= r2) return true;
+        if (g1 != kInf && (uint64_t)g1 * b <= r2) return 1;
       }
       const int ls = max((int)out.SFs[at3 + bq], 2);
       if (ls <= M - 1) {
         const int32_t g3 = Gb[(size_t)(u - 1) * pitch + (ls - 2)];
-        if (g3 != kInf && (uint64_t)g3 * b <= r2) return true;
+        if (g3 != kInf && (uint64_t)g3 * b <= r2) return 1;
       }
+      if (bq != bi) res = 2;  // at b' = b the pair found is p itself (same-batch twins: caller)
     }
   }
-  return false;
+  return res;
 }
 
 __global__ void __launch_bounds__(kF2Threads, 4) f2_q3_kernel(Problem pb, int ml, int seg_lo, int nseg,
@@ -326,16 +331,23 @@ __global__ void __launch_bounds__(kF2Threads, 4) f2_q3_kernel(Problem pb, int ml
       }
       // process up to 32 queued candidates, one per lane
       const bool act = lane < cnt;
-      bool keep = false;
+      bool keep = false, tie = false;
       int32_t c2 = 0, E = 0, C2 = 0, C3 = 0;
       if (act) {
         c2 = L[lane];
         C2 = P2[c2] - p2c1;
         C3 = P3M - P3[c2];
         E = a + P2[c2] + C3 + Y23[c2];
-        keep = !f2_dominated3(pb, out, M, B, k1, k3, bi, c1, c2, b, C2, Gseg);
+        const int r = f2_dominated3(pb, out, M, B, k1, k3, bi, c1, c2, b, C2, Gseg);
+        keep = r != 1;
+        // a twin at the same batch has equal P1 at its first cut or equal P3 at its second:
+        // a zero-latency layer next to c_1 (class k1) or c_2 (class k3)
+        tie = r == 2 || (c1 > 1 && P1[c1 - 1] == C1) || (c1 < M - 2 && P1[c1 + 1] == C1) ||
+              (c2 > 2 && P3[c2 - 1] == P3[c2]) || (c2 < M - 1 && P3[c2 + 1] == P3[c2]);
       }
-      emit_point(keep, make_point(md, 3, k1, k2, k3, c1, c2, b, E, C1, C2, C3), out);
+      ppipe_point pt = make_point(md, 3, k1, k2, k3, c1, c2, b, E, C1, C2, C3);
+      pt.reserved = tie ? 1 : 0;
+      emit_point(keep, pt, out);
       __syncwarp();
       const int rest = cnt > 32 ? cnt - 32 : 0;
       if (lane < rest) L[lane] = L[32 + lane];
@@ -402,7 +414,7 @@ __global__ void __launch_bounds__(kF2Threads) f2_q2_kernel(Problem pb, int ml, c
   unsigned long long feas = 0;
   for (int c0 = 1; c0 <= M - 1; c0 += blockDim.x) {
     const int c = c0 + threadIdx.x;
-    bool keep = false;
+    bool keep = false, tie = false;
     int32_t E = 0, C1 = 0, C2 = 0;
     if (c <= M - 1) {
       C1 = P1[c];
@@ -418,11 +430,15 @@ __global__ void __launch_bounds__(kF2Threads) f2_q2_kernel(Problem pb, int ml, c
           const int us = out.PFs[a1], ls = out.SFs[a2];
           const int32_t* Fb = F + ((size_t)seg * B + bq) * M;
           dom = (us >= l && Fb[us] - Fb[l - 1] > 0) || (ls <= u && Fb[u] - Fb[ls - 1] > 0);
+          // not strictly beaten: any other feasible c' in [l, u] equals p in both stages
+          tie = tie || Fb[u] - Fb[l - 1] > (bq == bi ? 1 : 0);
         }
         keep = !dom;
       }
     }
-    emit_point(keep, make_point(md, 2, k1, k2, 0, c, 0, b, E, C1, C2, 0), out);
+    ppipe_point pt = make_point(md, 2, k1, k2, 0, c, 0, b, E, C1, C2, 0);
+    pt.reserved = tie ? 1 : 0;
+    emit_point(keep, pt, out);
   }
   for (int off = 16; off; off >>= 1) feas += __shfl_down_sync(0xffffffffu, feas, off);
   if ((threadIdx.x & 31) == 0 && feas) atomicAdd(&out.counters[1], feas);
@@ -437,7 +453,7 @@ __global__ void __launch_bounds__(kF2Threads) f2_q1_kernel(Problem pb, int ml, F
   unsigned long long feas = 0;
   for (int b0 = 0; b0 < B; b0 += blockDim.x) {
     const int bi = b0 + threadIdx.x;
-    bool keep = false;
+    bool keep = false, tie = false;
     int32_t C1 = 0;
     uint32_t b = 0;
     if (bi < B) {
@@ -449,11 +465,14 @@ __global__ void __launch_bounds__(kF2Threads) f2_q1_kernel(Problem pb, int ml, F
         for (int bq = 0; bq < B && !dom; ++bq) {
           const int32_t Cq = prow(pb, md, k, bq)[M];
           dom = Cq <= T && (uint64_t)Cq * b < (uint64_t)C1 * pb.batches[bq];
+          tie = tie || (bq != bi && Cq <= T && (uint64_t)Cq * b == (uint64_t)C1 * pb.batches[bq]);
         }
         keep = !dom;
       }
     }
-    emit_point(keep, make_point(md, 1, k, 0, 0, 0, 0, b, C1, C1, 0, 0), out);
+    ppipe_point pt = make_point(md, 1, k, 0, 0, 0, 0, b, C1, C1, 0, 0);
+    pt.reserved = tie ? 1 : 0;
+    emit_point(keep, pt, out);
   }
   for (int off = 16; off; off >>= 1) feas += __shfl_down_sync(0xffffffffu, feas, off);
   if ((threadIdx.x & 31) == 0 && feas) atomicAdd(&out.counters[1], feas);
@@ -594,6 +613,30 @@ __global__ void gather_pts_kernel(const ppipe_point* in, const uint32_t* idx, ui
     out[i] = in[idx[i]];
 }
 
+// Canonical key in one word: segment << 40 | b << 24 | c_1 << 12 | c_2 (M <= 4096).
+__global__ void f2_out_key64_kernel(const ppipe_point* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t* key,
+                                    uint32_t* idx) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const ppipe_point p = in[i];
+    key[i] = (seg_of(p, seg_base, C) << 40) | ((uint64_t)p.batch << 24) | ((uint64_t)p.cut[0] << 12) | p.cut[1];
+    idx[i] = (uint32_t)i;
+  }
+}
+
+// Output records: gathered into canonical order, the tie flag cleared.
+__global__ void gather_final_kernel(const ppipe_point* in, const uint32_t* idx, uint64_t n, ppipe_point* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    ppipe_point p = in[idx[i]];
+    p.reserved = 0;
+    out[i] = p;
+  }
+}
+
+struct TieFlag {
+  uint16_t want;
+  __device__ __forceinline__ bool operator()(const ppipe_point& p) const { return p.reserved == want; }
+};
+
 // Of two records with the same vector: the smaller (E, b, c_1, c_2).
 struct PickMinE {
   const ppipe_point* r;
@@ -621,19 +664,22 @@ cudaError_t f2_finalize(const ppipe_point* in, uint64_t n, const uint64_t* seg_b
     return segment_offsets(out, 0, seg_base, C, n_seg, seg_offsets, seg_tmp, s, n_launches);
   }
   const int ni = (int)n;
-  // scratch: hi, lo, hi2 (u64 x n), idx, idx2, agg (u32 x n), keys, ukeys (K128 x n), nruns, cub temp
-  size_t b_sort = 0, b_red = 0;
+  // scratch: hi, lo, k2, k3 (u64 x n), idx, idx2, agg (u32 x n), keys, ukeys (K128 x n), counters, cub temp
+  size_t b_sort = 0, b_red = 0, b_sel = 0;
   e = cub::DeviceRadixSort::SortPairs(nullptr, b_sort, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
                                       (uint32_t*)nullptr, ni, 0, 64, s);
   if (e != cudaSuccess) return e;
   e = cub::DeviceReduce::ReduceByKey(nullptr, b_red, (K128*)nullptr, (K128*)nullptr, (uint32_t*)nullptr,
                                      (uint32_t*)nullptr, (uint64_t*)nullptr, PickMinE{nullptr}, ni, s);
   if (e != cudaSuccess) return e;
+  e = cub::DeviceSelect::If(nullptr, b_sel, (const ppipe_point*)nullptr, (ppipe_point*)nullptr, (uint64_t*)nullptr,
+                            ni, TieFlag{0}, s);
+  if (e != cudaSuccess) return e;
   const size_t o_hi = 0, o_lo = o_hi + align_up(8 * n), o_k2 = o_lo + align_up(8 * n), o_k3 = o_k2 + align_up(8 * n),
                o_idx = o_k3 + align_up(8 * n), o_idx2 = o_idx + align_up(4 * n), o_agg = o_idx2 + align_up(4 * n),
                o_keys = o_agg + align_up(4 * n), o_ukeys = o_keys + align_up(16 * n),
-               o_runs = o_ukeys + align_up(16 * n), o_tmp = o_runs + 256,
-               total = o_tmp + align_up(std::max(b_sort, b_red));
+               o_cnt = o_ukeys + align_up(16 * n), o_tmp = o_cnt + 256,
+               total = o_tmp + align_up(std::max(std::max(b_sort, b_red), b_sel));
   if (scratch->bytes < total) {
     if (scratch->buf) cudaFree(scratch->buf);
     scratch->buf = nullptr;
@@ -646,33 +692,55 @@ cudaError_t f2_finalize(const ppipe_point* in, uint64_t n, const uint64_t* seg_b
            *k3 = (uint64_t*)(base + o_k3);
   uint32_t *idx = (uint32_t*)(base + o_idx), *idx2 = (uint32_t*)(base + o_idx2), *agg = (uint32_t*)(base + o_agg);
   K128 *keys = (K128*)(base + o_keys), *ukeys = (K128*)(base + o_ukeys);
-  uint64_t* nruns = (uint64_t*)(base + o_runs);
+  uint64_t* cnt = (uint64_t*)(base + o_cnt);
   void* tmp = base + o_tmp;
-  const int g = grid_for(n);
 
-  // 1) sort by the equal-vector key (lo, then hi: LSD radix sort is stable)
-  f2_tie_keys_kernel<<<g, 256, 0, s>>>(in, n, seg_base, C, hi, lo, idx);
-  if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, lo, k2, idx, idx2, ni, 0, 64, s)) != cudaSuccess) return e;
-  gather_u64_kernel<<<g, 256, 0, s>>>(hi, idx2, n, k3);
-  if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, k3, k2, idx2, idx, ni, 0, 64, s)) != cudaSuccess) return e;
-  // k2 = hi sorted, idx = record index in sorted order
-  make_k128_kernel<<<g, 256, 0, s>>>(k2, lo, idx, n, keys);
-  // 2) best record of each run of equal vectors
-  if ((e = cub::DeviceReduce::ReduceByKey(tmp, b_red, keys, ukeys, idx, agg, nruns, PickMinE{in}, ni, s)) !=
-      cudaSuccess)
-    return e;
-  uint64_t nr = 0;
-  if ((e = cudaMemcpyAsync(&nr, nruns, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+  // 1) survivors no other candidate can equal (flag 0) go straight to tmp_pts[0, nu);
+  //    the few that might have an identical vector (flag 1) to out[0, nf)
+  if ((e = cub::DeviceSelect::If(tmp, b_sel, in, tmp_pts, cnt, ni, TieFlag{0}, s)) != cudaSuccess) return e;
+  if ((e = cub::DeviceSelect::If(tmp, b_sel, in, out, cnt + 1, ni, TieFlag{1}, s)) != cudaSuccess) return e;
+  uint64_t hc[3] = {0, 0, 0};
+  if ((e = cudaMemcpyAsync(hc, cnt, 16, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-  gather_pts_kernel<<<grid_for(nr), 256, 0, s>>>(in, agg, nr, tmp_pts);
-  // 3) canonical order (segment, b, c_1, c_2)
-  const int nri = (int)nr;
-  f2_out_keys_kernel<<<grid_for(nr), 256, 0, s>>>(tmp_pts, nr, seg_base, C, hi, lo, idx);
-  if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, lo, k2, idx, idx2, nri, 0, 64, s)) != cudaSuccess) return e;
-  gather_u64_kernel<<<grid_for(nr), 256, 0, s>>>(hi, idx2, nr, k3);
-  if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, k3, k2, idx2, idx, nri, 0, 64, s)) != cudaSuccess) return e;
-  gather_pts_kernel<<<grid_for(nr), 256, 0, s>>>(tmp_pts, idx, nr, out);
-  *n_launches += 13;
+  const uint64_t nu = hc[0], nf = hc[1];
+  *n_launches += 2;
+  // 2) flagged: sort by the equal-vector key (lo, then hi: LSD radix sort is stable) and
+  //    keep the best record of each run, appended at tmp_pts[nu, nu + nw)
+  uint64_t nw = 0;
+  if (nf) {
+    const int nfi = (int)nf, g = grid_for(nf);
+    f2_tie_keys_kernel<<<g, 256, 0, s>>>(out, nf, seg_base, C, hi, lo, idx);
+    if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, lo, k2, idx, idx2, nfi, 0, 64, s)) != cudaSuccess) return e;
+    gather_u64_kernel<<<g, 256, 0, s>>>(hi, idx2, nf, k3);
+    if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, k3, k2, idx2, idx, nfi, 0, 64, s)) != cudaSuccess) return e;
+    make_k128_kernel<<<g, 256, 0, s>>>(k2, lo, idx, nf, keys);
+    if ((e = cub::DeviceReduce::ReduceByKey(tmp, b_red, keys, ukeys, idx, agg, cnt + 2, PickMinE{out}, nfi, s)) !=
+        cudaSuccess)
+      return e;
+    if ((e = cudaMemcpyAsync(&nw, cnt + 2, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    gather_pts_kernel<<<grid_for(nw), 256, 0, s>>>(out, agg, nw, tmp_pts + nu);
+    *n_launches += 11;
+  }
+  // 3) canonical order (segment, b, c_1, c_2): one radix sort over the key bits in use
+  const uint64_t nr = nu + nw;
+  const int nri = (int)nr, g = grid_for(nr);
+  int seg_bits = 1;
+  while (seg_bits < 64 && (1ull << seg_bits) < n_seg) ++seg_bits;
+  if (seg_bits + 40 <= 64) {
+    f2_out_key64_kernel<<<g, 256, 0, s>>>(tmp_pts, nr, seg_base, C, lo, idx);
+    if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, lo, k2, idx, idx2, nri, 0, 40 + seg_bits, s)) != cudaSuccess)
+      return e;
+    gather_final_kernel<<<g, 256, 0, s>>>(tmp_pts, idx2, nr, out);
+    *n_launches += 3;
+  } else {
+    f2_out_keys_kernel<<<g, 256, 0, s>>>(tmp_pts, nr, seg_base, C, hi, lo, idx);
+    if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, lo, k2, idx, idx2, nri, 0, 64, s)) != cudaSuccess) return e;
+    gather_u64_kernel<<<g, 256, 0, s>>>(hi, idx2, nr, k3);
+    if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, k3, k2, idx2, idx, nri, 0, 64, s)) != cudaSuccess) return e;
+    gather_final_kernel<<<g, 256, 0, s>>>(tmp_pts, idx, nr, out);
+    *n_launches += 5;
+  }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   *n_out_host = nr;
   return segment_offsets(out, nr, seg_base, C, n_seg, seg_offsets, seg_tmp, s, n_launches);
