@@ -6,9 +6,11 @@ package (paper_2507_18748_b200) never imports it and shares no code with it.
 """
 from .oracle import (  # noqa: F401
     POINT_DTYPE,
+    POINT_PB_DTYPE,
     OracleResult,
     build_oracle,
     run_oracle,
+    run_oracle_pb,
     oracle_lib_path,
     prepartition_oracle,
 )

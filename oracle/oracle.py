@@ -24,6 +24,12 @@ POINT_DTYPE = np.dtype([
     ("batch", "<u2"), ("reserved", "<u2"), ("e2e_us", "<u4"), ("stage_us", "<u4", (3,)),
 ])
 assert POINT_DTYPE.itemsize == 32
+# per-stage batch records (oracle_run_pb): batch INDICES per stage instead of one batch value
+POINT_PB_DTYPE = np.dtype([
+    ("model", "<u4"), ("cut", "<u2", (2,)), ("K", "u1"), ("cls", "u1", (3,)), ("bidx", "u1", (3,)),
+    ("reserved", "u1"), ("e2e_us", "<u4"), ("stage_us", "<u4", (3,)),
+])
+assert POINT_PB_DTYPE.itemsize == 32
 
 
 def oracle_lib_path() -> str:
@@ -64,6 +70,12 @@ def _load():
         lib.oracle_set_threads.argtypes = [ct.c_int]
         lib.oracle_set_vgpu.argtypes = [ct.POINTER(ct.c_uint8), ct.c_uint32]
         lib.oracle_set_frontier.argtypes = [ct.c_int]
+        lib.oracle_run_pb.restype = ct.c_int
+        lib.oracle_run_pb.argtypes = [ct.c_uint32, ct.POINTER(_Model), ct.c_uint32, ct.c_uint32,
+                                      ct.POINTER(ct.c_uint32), ct.POINTER(ct.c_uint32), ct.c_uint32,
+                                      ct.POINTER(ct.c_uint32), ct.c_uint32, ct.c_uint32, ct.c_uint32,
+                                      ct.POINTER(ct.POINTER(_Result))]
+        lib.oracle_result_pb_free.argtypes = [ct.POINTER(_Result)]
         lib.oracle_prepartition.restype = ct.c_int
         lib.oracle_prepartition.argtypes = [ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.POINTER(ct.c_uint32),
                                             ct.POINTER(ct.c_uint64), ct.c_uint32, ct.c_uint32, ct.c_uint32,
@@ -138,6 +150,46 @@ def run_oracle(w, model_lo: int = 0, model_hi: Optional[int] = None, only_K: int
     seg = np.ctypeslib.as_array(r.seg_off, shape=(int(r.n_seg) + 1,)).copy()
     res = OracleResult(pts, seg, int(r.n_cand), int(r.n_feas))
     lib.oracle_result_free(out)
+    del keep
+    return res
+
+
+def run_oracle_pb(w, model_lo: int = 0, model_hi: Optional[int] = None, threads: int = 0,
+                  slo_us: Optional[np.ndarray] = None, kmax: Optional[int] = None) -> OracleResult:
+    """Per-stage batch sizes (oracle_run_pb in ppipe_oracle.c): every partition picks its own
+    batch; records are POINT_PB_DTYPE (batch indices per stage)."""
+    lib = _load()
+    lib.oracle_set_threads(int(threads))
+    n = len(w.models)
+    model_hi = n if model_hi is None else model_hi
+    keep = []
+    models = (_Model * max(n, 1))()
+    for i, mp in enumerate(w.models):
+        lat = np.ascontiguousarray(mp.lat_us, dtype=np.uint32)
+        S = np.ascontiguousarray(mp.act_bytes, dtype=np.uint64)
+        keep += [lat, S]
+        models[i].n_layers = lat.shape[1]
+        models[i].lat_us = _u32p(lat)
+        models[i].act_bytes = S.ctypes.data_as(ct.POINTER(ct.c_uint64))
+    batches = np.ascontiguousarray(w.batches, dtype=np.uint32)
+    bw = np.ascontiguousarray(w.bw, dtype=np.uint32).reshape(-1)
+    slo = np.ascontiguousarray(w.slo_us if slo_us is None else slo_us, dtype=np.uint32)
+    out = ct.POINTER(_Result)()
+    rc = lib.oracle_run_pb(n, models, w.n_classes, w.n_batches, _u32p(batches), _u32p(bw),
+                           w.kmax if kmax is None else kmax, _u32p(slo), w.margin_permille, model_lo, model_hi,
+                           ct.byref(out))
+    if rc != 0:
+        raise ValueError(f"oracle_run_pb rejected its input (rc={rc})")
+    r = out.contents
+    npts = int(r.n_pts)
+    if npts:
+        buf = (ct.c_char * (npts * 32)).from_address(r.pts)
+        pts = np.frombuffer(bytes(buf), dtype=POINT_PB_DTYPE).copy()
+    else:
+        pts = np.zeros(0, dtype=POINT_PB_DTYPE)
+    seg = np.ctypeslib.as_array(r.seg_off, shape=(int(r.n_seg) + 1,)).copy()
+    res = OracleResult(pts, seg, int(r.n_cand), int(r.n_feas))
+    lib.oracle_result_pb_free(out)
     del keep
     return res
 

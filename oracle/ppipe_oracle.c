@@ -46,7 +46,10 @@
  * reduction (oracle_set_frontier(2), below) by tests/test_f2_pins.py (an
  * independent Fraction-based literal definition on random tiny inputs, a
  * hand-worked fixture, the K = 1 closed form, the single-batch all-kept case and
- * the MILP-losslessness property).
+ * the MILP-losslessness property); oracle_run_pb (per-stage batch sizes, end of
+ * file) by tests/test_pb_pins.py (the unified oracle at one batch size, a Fraction
+ * literal definition, closed-form counts, a hand-worked mixed-batch plan and the
+ * superset property over the unified frontier).
  */
 #define _GNU_SOURCE
 #include <pthread.h>
@@ -612,5 +615,332 @@ int oracle_prepartition(uint32_t M, uint32_t C, uint32_t B, const uint32_t *lat,
         block_lat[((size_t)k * N + q) * B + b] = sum;
       }
   for (uint32_t q = 0; q < N; ++q) block_S[q] = S[bounds[q + 1] - 1];
+  return 0;
+}
+
+/*
+ * Per-stage batch sizes (DESIGN.md §3 readings PB-1..PB-4).
+ *
+ * The basic MILP of App. A.1 lets every partition pick its own batch size: eq. 1.1
+ * sums p_{ldbij} over (b, i, j) per partition d, so partition d runs
+ * at b_d. Per candidate (cuts, classes, b_1..b_K):
+ *   C_d = sum_{l in [c_{d-1}, c_d)} lat[k_d][l][b_d]                  eq. 1.9 (C_{ldbij} at b_d)
+ *   Y_d = ceil(8 * S[c_d - 1] * b_d / bw[k_d][k_{d+1}])  for d < K    eq. 1.11: n_ld = Y_{bj} of
+ *         partition d's own (b, j), i.e. the sender's batch
+ *   E   = sum_d C_d + sum_d Y_d <= T                                  eq. 1.12
+ *   theta = min_d b_d / C_d  (x_l = min_d x_ld, X = b / C, one GPU per stage)
+ * and per segment (m, K, k_1..k_K) the (E min, theta max) staircase with ties on
+ * identical (E, theta) broken by the smallest (b_1, .., b_K) (lexicographic), then the
+ * smallest (c_1, c_2). With one batch size this is oracle_run's frontier.
+ * Records carry batch INDICES (bidx[d] into the batch list; 0xFF when unused).
+ * Pinned by tests/test_pb_pins.py.
+ */
+typedef struct {
+  uint32_t model;
+  uint16_t cut[2];
+  uint8_t K;
+  uint8_t cls[3];
+  uint8_t bidx[3];
+  uint8_t reserved;
+  uint32_t e2e_us;
+  uint32_t stage_us[3];
+} oracle_point_pb;
+
+typedef struct {
+  int64_t E;
+  int64_t st[3];
+  int32_t c1, c2;
+  int32_t bi[3];
+} cand_pb;
+
+typedef struct {
+  cand_pb *v;
+  size_t n, cap;
+} cvec_pb;
+
+static void cvec_pb_push(cvec_pb *a, const cand_pb *c) {
+  if (a->n == a->cap) {
+    size_t nc = a->cap ? a->cap * 2 : 64;
+    cand_pb *nv = (cand_pb *)realloc(a->v, nc * sizeof(cand_pb));
+    if (!nv) {
+      fprintf(stderr, "oracle: out of memory\n");
+      abort();
+    }
+    a->v = nv;
+    a->cap = nc;
+  }
+  a->v[a->n++] = *c;
+}
+
+static const uint32_t *g_pb_batches; /* qsort context (sorting is single-threaded) */
+static int g_pb_K;
+
+/* theta = min_d b_d / C_d as the fraction (num, den) of the minimising stage (den 0 = +inf) */
+static void theta_pb(const cand_pb *c, int K, int64_t *num, int64_t *den) {
+  *num = g_pb_batches[c->bi[0]];
+  *den = c->st[0];
+  for (int d = 1; d < K; d++) {
+    const int64_t n2 = g_pb_batches[c->bi[d]], d2 = c->st[d];
+    if (theta_gt(*num, *den, n2, d2)) {
+      *num = n2;
+      *den = d2;
+    }
+  }
+}
+
+static int cand_pb_cmp(const void *pa, const void *pb_) {
+  const cand_pb *p = (const cand_pb *)pa, *q = (const cand_pb *)pb_;
+  if (p->E != q->E) return p->E < q->E ? -1 : 1;
+  int64_t np_, dp, nq, dq;
+  theta_pb(p, g_pb_K, &np_, &dp);
+  theta_pb(q, g_pb_K, &nq, &dq);
+  if (theta_gt(np_, dp, nq, dq)) return -1;
+  if (theta_gt(nq, dq, np_, dp)) return 1;
+  for (int d = 0; d < g_pb_K; d++)
+    if (p->bi[d] != q->bi[d]) return p->bi[d] < q->bi[d] ? -1 : 1;
+  if (p->c1 != q->c1) return p->c1 < q->c1 ? -1 : 1;
+  if (p->c2 != q->c2) return p->c2 < q->c2 ? -1 : 1;
+  return 0;
+}
+
+typedef struct {
+  problem *pb;
+  cvec_pb *segs[4];
+  uint64_t n_cand, n_feas;
+} worker_pb;
+
+static void emit_pb(worker_pb *w, int K, const uint32_t *k, const cand_pb *c) {
+  uint32_t idx = 0;
+  for (int d = 0; d < K; d++) idx = idx * w->pb->C + k[d];
+  cvec_pb_push(&w->segs[K][idx], c);
+}
+
+/* One row: K=1 (c1 = -1) or first cut c1 for K=2 / K=3; every class and batch per stage. */
+static void do_row_pb(worker_pb *w, int K, int32_t c1) {
+  problem *pb = w->pb;
+  const uint32_t C = pb->C, B = pb->B, M = pb->M;
+  uint32_t k[3];
+  cand_pb c;
+  memset(&c, 0, sizeof c);
+  if (K == 1) {
+    for (k[0] = 0; k[0] < C; k[0]++)
+      for (uint32_t b1 = 0; b1 < B; b1++) {
+        memset(&c, 0, sizeof c);
+        c.st[0] = pb->pre[((size_t)M * C + k[0]) * B + b1];
+        c.E = c.st[0];
+        c.bi[0] = (int32_t)b1;
+        w->n_cand++;
+        if (c.E > pb->T) continue;
+        w->n_feas++;
+        emit_pb(w, 1, k, &c);
+      }
+    return;
+  }
+  if (K == 2) {
+    for (k[0] = 0; k[0] < C; k[0]++)
+      for (k[1] = 0; k[1] < C; k[1]++)
+        for (uint32_t b1 = 0; b1 < B; b1++)
+          for (uint32_t b2 = 0; b2 < B; b2++) {
+            memset(&c, 0, sizeof c);
+            c.st[0] = pb->pre[((size_t)c1 * C + k[0]) * B + b1];
+            c.st[1] = pb->suf[((size_t)c1 * C + k[1]) * B + b2];
+            c.E = c.st[0] + c.st[1] + pb->Y[(((size_t)c1 * C + k[0]) * C + k[1]) * B + b1]; /* sender's batch */
+            c.c1 = c1;
+            c.bi[0] = (int32_t)b1;
+            c.bi[1] = (int32_t)b2;
+            w->n_cand++;
+            if (c.E > pb->T) continue;
+            w->n_feas++;
+            emit_pb(w, 2, k, &c);
+          }
+    return;
+  }
+  int64_t *mid = (int64_t *)malloc(sizeof(int64_t) * C * B);
+  for (int32_t c2 = c1 + 1; c2 <= (int32_t)M - 1; c2++) {
+    for (uint32_t kk = 0; kk < C; kk++)
+      for (uint32_t bi = 0; bi < B; bi++) mid[kk * B + bi] = direct_sum(pb, kk, (uint32_t)c1, (uint32_t)c2, bi);
+    for (k[0] = 0; k[0] < C; k[0]++)
+      for (k[1] = 0; k[1] < C; k[1]++)
+        for (k[2] = 0; k[2] < C; k[2]++)
+          for (uint32_t b1 = 0; b1 < B; b1++)
+            for (uint32_t b2 = 0; b2 < B; b2++)
+              for (uint32_t b3 = 0; b3 < B; b3++) {
+                c.st[0] = pb->pre[((size_t)c1 * C + k[0]) * B + b1];
+                c.st[1] = mid[k[1] * B + b2];
+                c.st[2] = pb->suf[((size_t)c2 * C + k[2]) * B + b3];
+                c.E = c.st[0] + c.st[1] + c.st[2] + pb->Y[(((size_t)c1 * C + k[0]) * C + k[1]) * B + b1] +
+                      pb->Y[(((size_t)c2 * C + k[1]) * C + k[2]) * B + b2];
+                c.c1 = c1;
+                c.c2 = c2;
+                c.bi[0] = (int32_t)b1;
+                c.bi[1] = (int32_t)b2;
+                c.bi[2] = (int32_t)b3;
+                w->n_cand++;
+                if (c.E > pb->T) continue;
+                w->n_feas++;
+                emit_pb(w, 3, k, &c);
+              }
+  }
+  free(mid);
+}
+
+static void *worker_pb_main(void *arg) {
+  worker_pb *w = (worker_pb *)arg;
+  problem *pb = w->pb;
+  const int32_t M = (int32_t)pb->M;
+  for (;;) {
+    pthread_mutex_lock(&pb->mu);
+    int32_t r = pb->next_row++;
+    pthread_mutex_unlock(&pb->mu);
+    if (r >= M) break;
+    if (r == 0) {
+      do_row_pb(w, 1, -1);
+      continue;
+    }
+    if (pb->Kmax >= 2) do_row_pb(w, 2, r);
+    if (pb->Kmax >= 3 && r <= M - 2) do_row_pb(w, 3, r);
+  }
+  return NULL;
+}
+
+typedef struct {
+  oracle_point_pb *pts;
+  uint64_t n_pts;
+  uint64_t *seg_off;
+  uint64_t n_seg;
+  uint64_t n_cand, n_feas;
+} oracle_result_pb;
+
+void oracle_result_pb_free(oracle_result_pb *r) {
+  if (!r) return;
+  free(r->pts);
+  free(r->seg_off);
+  free(r);
+}
+
+/* Models [model_lo, model_hi), every K <= kmax; batches <= 255 entries. Returns 0 on success. */
+int oracle_run_pb(uint32_t n_models, const oracle_model *models, uint32_t n_classes, uint32_t n_batches,
+                  const uint32_t *batches, const uint32_t *bw, uint32_t kmax, const uint32_t *slo_us,
+                  uint32_t margin_permille, uint32_t model_lo, uint32_t model_hi, oracle_result_pb **out) {
+  if (!out || n_classes == 0 || n_batches == 0 || n_batches > 255 || kmax < 1 || kmax > 3 || margin_permille >= 1000)
+    return -1;
+  if (model_hi > n_models || model_lo > model_hi) return -1;
+  oracle_result_pb *res = (oracle_result_pb *)calloc(1, sizeof *res);
+  size_t cap_pts = 0;
+  const uint32_t C = n_classes, B = n_batches;
+  uint64_t total_seg = 0;
+  for (uint32_t m = model_lo; m < model_hi; m++) {
+    uint64_t p = 1;
+    for (uint32_t K = 1; K <= kmax && K <= models[m].n_layers; K++) {
+      p *= C;
+      total_seg += p;
+    }
+  }
+  res->seg_off = (uint64_t *)calloc(total_seg + 1, sizeof(uint64_t));
+  res->n_seg = total_seg;
+  uint64_t seg_cursor = 0;
+  int nthreads = g_threads > 0 ? g_threads : (int)sysconf(_SC_NPROCESSORS_ONLN);
+  if (nthreads < 1) nthreads = 1;
+  g_pb_batches = batches;
+  for (uint32_t m = model_lo; m < model_hi; m++) {
+    problem pb;
+    memset(&pb, 0, sizeof pb);
+    pb.md = &models[m];
+    pb.C = C;
+    pb.B = B;
+    pb.M = models[m].n_layers;
+    pb.batches = batches;
+    pb.bw = bw;
+    pb.T = (int64_t)slo_us[m] * (int64_t)(1000 - margin_permille) / 1000;
+    pb.Kmax = (int)kmax;
+    const uint32_t M = pb.M;
+    pthread_mutex_init(&pb.mu, NULL);
+    pb.pre = (int64_t *)malloc(sizeof(int64_t) * (M + 1) * C * B);
+    pb.suf = (int64_t *)malloc(sizeof(int64_t) * (M + 1) * C * B);
+    for (uint32_t c = 0; c <= M; c++)
+      for (uint32_t k = 0; k < C; k++)
+        for (uint32_t bi = 0; bi < B; bi++) {
+          pb.pre[((size_t)c * C + k) * B + bi] = direct_sum(&pb, k, 0, c, bi);
+          pb.suf[((size_t)c * C + k) * B + bi] = direct_sum(&pb, k, c, M, bi);
+        }
+    pb.Y = (int64_t *)calloc((size_t)(M + 1) * C * C * B, sizeof(int64_t));
+    for (uint32_t c = 1; c + 1 <= M; c++)
+      for (uint32_t k = 0; k < C; k++)
+        for (uint32_t k2 = 0; k2 < C; k2++)
+          for (uint32_t bi = 0; bi < B; bi++)
+            pb.Y[(((size_t)c * C + k) * C + k2) * B + bi] =
+                ceil_div(8 * (int64_t)models[m].act_bytes[c - 1] * (int64_t)batches[bi], (int64_t)bw[k * C + k2]);
+    for (uint32_t K = 1; K <= 3; K++) {
+      uint32_t p = 1;
+      for (uint32_t d = 0; d < K; d++) p *= C;
+      pb.nseg[K] = p;
+    }
+    worker_pb *ws = (worker_pb *)calloc((size_t)nthreads, sizeof(worker_pb));
+    pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+    for (int t = 0; t < nthreads; t++) {
+      ws[t].pb = &pb;
+      for (int K = 1; K <= 3; K++) ws[t].segs[K] = (cvec_pb *)calloc(pb.nseg[K], sizeof(cvec_pb));
+      pthread_create(&th[t], NULL, worker_pb_main, &ws[t]);
+    }
+    for (int t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
+    for (int t = 0; t < nthreads; t++) {
+      res->n_cand += ws[t].n_cand;
+      res->n_feas += ws[t].n_feas;
+    }
+    for (uint32_t K = 1; K <= kmax && K <= M; K++) {
+      for (uint32_t s = 0; s < pb.nseg[K]; s++) {
+        cvec_pb all = {0};
+        for (int t = 0; t < nthreads; t++)
+          for (size_t i = 0; i < ws[t].segs[K][s].n; i++) cvec_pb_push(&all, &ws[t].segs[K][s].v[i]);
+        g_pb_K = (int)K;
+        if (all.n) qsort(all.v, all.n, sizeof(cand_pb), cand_pb_cmp);
+        int64_t best_n = 0, best_d = 1;
+        for (size_t i = 0; i < all.n; i++) {
+          const cand_pb *p = &all.v[i];
+          int64_t tn, td;
+          theta_pb(p, (int)K, &tn, &td);
+          if (!theta_gt(tn, td, best_n, best_d)) continue;
+          best_n = tn;
+          best_d = td;
+          if (res->n_pts == cap_pts) {
+            cap_pts = cap_pts ? cap_pts * 2 : 1024;
+            res->pts = (oracle_point_pb *)realloc(res->pts, cap_pts * sizeof(oracle_point_pb));
+          }
+          oracle_point_pb *o = &res->pts[res->n_pts++];
+          memset(o, 0, sizeof *o);
+          o->model = m;
+          o->K = (uint8_t)K;
+          o->cut[0] = (uint16_t)(K >= 2 ? p->c1 : 0);
+          o->cut[1] = (uint16_t)(K >= 3 ? p->c2 : 0);
+          uint32_t idx = s;
+          for (int d = (int)K - 1; d >= 0; d--) {
+            o->cls[d] = (uint8_t)(idx % C);
+            idx /= C;
+          }
+          for (int d = 0; d < 3; d++) {
+            if (d >= (int)K) o->cls[d] = 0xFF;
+            o->bidx[d] = d < (int)K ? (uint8_t)p->bi[d] : (uint8_t)0xFF;
+          }
+          o->e2e_us = (uint32_t)p->E;
+          for (int d = 0; d < (int)K; d++) o->stage_us[d] = (uint32_t)p->st[d];
+        }
+        free(all.v);
+        res->seg_off[++seg_cursor] = res->n_pts;
+      }
+    }
+    for (int t = 0; t < nthreads; t++) {
+      for (int K = 1; K <= 3; K++) {
+        for (uint32_t s = 0; s < pb.nseg[K]; s++) free(ws[t].segs[K][s].v);
+        free(ws[t].segs[K]);
+      }
+    }
+    free(ws);
+    free(th);
+    free(pb.pre);
+    free(pb.suf);
+    free(pb.Y);
+    pthread_mutex_destroy(&pb.mu);
+  }
+  *out = res;
   return 0;
 }

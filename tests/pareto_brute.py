@@ -161,3 +161,53 @@ def literal_f2_np(cands, cls, vgpu=None):
             keep.append(cands[i])
     keep.sort(key=lambda c: (c["b"], c["cuts"]))
     return keep
+
+
+# ---------------- per-stage batch sizes (App. A.1) ----------------
+
+def enumerate_candidates_pb(w, m: int):
+    """All per-stage-batch candidates of model m: dict (K, cls) -> list of dicts. Partition d
+    runs at its own batch b_d (eq. 1.1 sums over b per partition); the
+    transfer after partition d uses the sender's batch (Y_{bj}, eq. 1.11)."""
+    mp = w.models[m]
+    lat = mp.lat_us.astype(object)
+    S = [int(x) for x in mp.act_bytes]
+    C, M, B = mp.lat_us.shape
+    T = t_eff(w.slo_us[m], w.margin_permille)
+    out, n_cand = {}, 0
+    for K in range(1, min(w.kmax, M) + 1):
+        for cuts in itertools.combinations(range(1, M), K - 1):
+            bounds = (0,) + cuts + (M,)
+            for cls in itertools.product(range(C), repeat=K):
+                for bis in itertools.product(range(B), repeat=K):
+                    bs = [int(w.batches[bi]) for bi in bis]
+                    stages = [sum(int(lat[cls[d], l, bis[d]]) for l in range(bounds[d], bounds[d + 1]))
+                              for d in range(K)]
+                    trans = [-(-8 * S[bounds[d + 1] - 1] * bs[d] // int(w.bw[cls[d], cls[d + 1]])) for d in range(K - 1)]
+                    E = sum(stages) + sum(trans)
+                    n_cand += 1
+                    if E > T:
+                        continue
+                    theta = min(Fraction(bs[d], stages[d]) if stages[d] > 0 else math.inf for d in range(K))
+                    out.setdefault((K, cls), []).append(dict(E=E, theta=theta, bidx=tuple(bis), stages=stages,
+                                                             cuts=tuple(cuts) + (0,) * (2 - len(cuts))))
+    return out, n_cand
+
+
+def literal_frontier_pb(cands):
+    """Keep p iff no q has E_q <= E_p and theta_q >= theta_p with one strict, or both equal and
+    (b_1..b_K, cuts)_q < (b_1..b_K, cuts)_p. Output in E order."""
+    keep = []
+    for p in cands:
+        dominated = False
+        for q in cands:
+            if q is p:
+                continue
+            if q["E"] <= p["E"] and q["theta"] >= p["theta"]:
+                if q["E"] < p["E"] or q["theta"] > p["theta"] or (q["bidx"], q["cuts"]) < (p["bidx"], p["cuts"]):
+                    dominated = True
+                    break
+        if not dominated:
+            keep.append(p)
+    keep.sort(key=lambda c: c["E"])
+    return keep
