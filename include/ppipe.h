@@ -195,6 +195,50 @@ int ppipe_pareto(ppipe_ctx *ctx, int copy_to_host, ppipe_frontier *out);
  * PPIPE_ENOMEM, PPIPE_ECUDA, PPIPE_ENCCL. */
 int ppipe_pareto_f2(ppipe_ctx *ctx, const ppipe_enum_params *params, int copy_to_host, ppipe_frontier *out);
 
+/* Per-stage batch sizes (DESIGN.md §3 PB-1..PB-4). App. A.1's
+ * basic MILP lets each partition run its own batch: eq. 1.1 sums p_{ldbij} over
+ * (b, i, j) per partition d. A candidate is (cuts, classes, b_1..b_K):
+ *   C_d = sum_{l in partition d} lat_us[k_d][l][b_d]                     eq. 1.9
+ *   Y_d = ceil(8 * act_bytes[c_d - 1] * b_d / bw[k_d][k_{d+1}]), d < K   eq. 1.11 (the sender's batch)
+ *   E   = sum C_d + sum Y_d <= T_eff                                     eq. 1.12
+ *   theta = min_d b_d / C_d (exact rational; C_d = 0 reads as +inf)
+ * and the frontier per segment (model, K, k_1..k_K) is the (E min, theta max)
+ * staircase; among identical (E, theta) the smallest (b_1, .., b_K) (lexicographic),
+ * then the smallest (c_1, c_2) stays. With one batch size this is ppipe_pareto's frontier.
+ * B^K times the unified candidates: meant for block-level profiles.
+ * Records carry batch INDICES per stage (bidx[d] into the batch list, 0xFF unused). */
+typedef struct {
+  uint32_t model;       /* model index */
+  uint16_t cut[2];      /* c_1, c_2; 0 when unused */
+  uint8_t K;            /* 1..3 */
+  uint8_t cls[3];       /* k_d for d < K; 0xFF when unused */
+  uint8_t bidx[3];      /* batch index of stage d for d < K; 0xFF when unused */
+  uint8_t reserved;     /* 0 */
+  uint32_t e2e_us;      /* E */
+  uint32_t stage_us[3]; /* C_1..C_K */
+} ppipe_point_pb;
+
+typedef struct {
+  uint64_t n_candidates;  /* all ranks: sum_m sum_K C(M-1, K-1) * C^K * B^K */
+  uint64_t n_feasible;
+  uint64_t n_points;
+  uint64_t n_segments;
+  const ppipe_point_pb *points;   /* host (page-locked, ctx-owned) if copy_to_host, else NULL; per segment E-ascending */
+  const uint64_t *seg_offsets;    /* host [n_segments + 1] if copy_to_host */
+  const ppipe_point_pb *d_points; /* device */
+  const uint64_t *d_seg_offsets;  /* device */
+  uint64_t n_survivors;           /* this rank's survivors of the in-CTA E-bucket fold */
+} ppipe_frontier_pb;
+
+/* One blocking call: pack, enumerate every per-stage-batch candidate, reduce, and
+ * (world > 1 with NCCL) all-gather the per-rank frontiers; like ppipe_pareto_f2, each
+ * model is computed whole by the rank holding its K = 1 row. The result shares the
+ * context's result buffers (invalidates the last ppipe_enumerate / ppipe_pareto /
+ * ppipe_pareto_f2 result) and is valid until the next such call or ppipe_free.
+ * Errors: as ppipe_enumerate; PPIPE_ERANGE if n_batches > 255; PPIPE_ESTATE after
+ * ppipe_update_profiles_async; PPIPE_ENOMEM, PPIPE_ECUDA, PPIPE_ENCCL. */
+int ppipe_pareto_pb(ppipe_ctx *ctx, const ppipe_enum_params *params, int copy_to_host, ppipe_frontier_pb *out);
+
 /* Virtual GPUs (§5.1; App. A.2 L_{kvbi}): declare
  * class k a pseudo-class that runs on 1/vgpu[k] of a physical GPU (MPS), vgpu[k] in
  * 1..4 (NULL = all 1, the default). Its profile is the caller's lat_us for that

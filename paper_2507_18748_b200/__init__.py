@@ -6,6 +6,7 @@ Pareto frontier -- as hand-written sm_100a CUDA kernels behind a C ABI
 """
 from ._binding import (  # noqa: F401
     POINT_DTYPE,
+    POINT_PB_DTYPE,
     Context,
     Frontier,
     PPipeError,
@@ -17,6 +18,7 @@ from ._binding import (  # noqa: F401
     nccl_unique_id,
     pareto,
     pareto_f2,
+    pareto_pb,
     partition_rows,
     prepartition,
     run,

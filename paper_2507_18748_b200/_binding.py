@@ -27,6 +27,12 @@ POINT_DTYPE = np.dtype([
     ("batch", "<u2"), ("reserved", "<u2"), ("e2e_us", "<u4"), ("stage_us", "<u4", (3,)),
 ])
 assert POINT_DTYPE.itemsize == 32
+# ppipe_point_pb, 32 bytes: per-stage batch INDICES instead of one batch value
+POINT_PB_DTYPE = np.dtype([
+    ("model", "<u4"), ("cut", "<u2", (2,)), ("K", "u1"), ("cls", "u1", (3,)), ("bidx", "u1", (3,)),
+    ("reserved", "u1"), ("e2e_us", "<u4"), ("stage_us", "<u4", (3,)),
+])
+assert POINT_PB_DTYPE.itemsize == 32
 
 
 class PPipeError(RuntimeError):
@@ -54,6 +60,12 @@ class _Frontier(ct.Structure):
                 ("n_segments", ct.c_uint64), ("points", ct.c_void_p), ("seg_offsets", ct.POINTER(ct.c_uint64)),
                 ("d_points", ct.c_void_p), ("d_seg_offsets", ct.c_void_p), ("n_survivors", ct.c_uint64),
                 ("n_candidates_local", ct.c_uint64), ("n_feasible_local", ct.c_uint64)]
+
+
+class _FrontierPB(ct.Structure):
+    _fields_ = [("n_candidates", ct.c_uint64), ("n_feasible", ct.c_uint64), ("n_points", ct.c_uint64),
+                ("n_segments", ct.c_uint64), ("points", ct.c_void_p), ("seg_offsets", ct.POINTER(ct.c_uint64)),
+                ("d_points", ct.c_void_p), ("d_seg_offsets", ct.c_void_p), ("n_survivors", ct.c_uint64)]
 
 
 _lib = None
@@ -84,6 +96,8 @@ def lib():
         L.ppipe_update_profiles_async.argtypes = [ct.c_void_p, ct.c_uint32, ct.POINTER(_Model)]
         L.ppipe_set_vgpu.restype = ct.c_int
         L.ppipe_set_vgpu.argtypes = [ct.c_void_p, ct.POINTER(ct.c_uint8)]
+        L.ppipe_pareto_pb.restype = ct.c_int
+        L.ppipe_pareto_pb.argtypes = [ct.c_void_p, ct.POINTER(_EnumParams), ct.c_int, ct.POINTER(_FrontierPB)]
         L.ppipe_pareto_f2.restype = ct.c_int
         L.ppipe_pareto_f2.argtypes = [ct.c_void_p, ct.POINTER(_EnumParams), ct.c_int, ct.POINTER(_Frontier)]
         L.ppipe_frontier_at.restype = ct.c_int
@@ -222,23 +236,23 @@ class Frontier:
     n_feasible_local: int = 0
 
 
-def _frontier_from(f, copy_to_host: bool, zero_copy: bool) -> Frontier:
+def _frontier_from(f, copy_to_host: bool, zero_copy: bool, dtype=POINT_DTYPE) -> Frontier:
     pts = seg = None
     if copy_to_host:
         n = int(f.n_points)
         if n:
             buf = (ct.c_char * (32 * n)).from_address(f.points)
-            pts = np.frombuffer(buf, dtype=POINT_DTYPE)
+            pts = np.frombuffer(buf, dtype=dtype)
             if not zero_copy:
                 pts = pts.copy()
         else:
-            pts = np.zeros(0, dtype=POINT_DTYPE)
+            pts = np.zeros(0, dtype=dtype)
         seg = np.ctypeslib.as_array(f.seg_offsets, shape=(int(f.n_segments) + 1,))
         if not zero_copy:
             seg = seg.copy()
     return Frontier(int(f.n_candidates), int(f.n_feasible), int(f.n_points), int(f.n_segments),
                     int(f.n_survivors), pts, seg, int(f.d_points or 0), int(f.d_seg_offsets or 0),
-                    int(f.n_candidates_local), int(f.n_feasible_local))
+                    int(getattr(f, "n_candidates_local", 0)), int(getattr(f, "n_feasible_local", 0)))
 
 
 def pareto(ctx: Context, copy_to_host: bool = True, zero_copy: bool = False) -> Frontier:
@@ -262,6 +276,19 @@ def pareto_f2(ctx: Context, max_partitions: int, slo_us: np.ndarray, margin_perm
     f = _Frontier()
     _check(lib().ppipe_pareto_f2(ctx.handle, ct.byref(p), 1 if copy_to_host else 0, ct.byref(f)), ctx.handle)
     return _frontier_from(f, copy_to_host, zero_copy)
+
+
+def pareto_pb(ctx: Context, max_partitions: int, slo_us: np.ndarray, margin_permille: int,
+              copy_to_host: bool = True, zero_copy: bool = False) -> Frontier:
+    """Per-stage batch sizes (include/ppipe.h ppipe_pareto_pb): every partition at its own
+    batch; points are POINT_PB_DTYPE (batch indices per stage), per segment E-ascending."""
+    slo = np.ascontiguousarray(slo_us, dtype=np.uint32)
+    if slo.shape[0] != ctx.n_models:
+        raise PPipeError(PPIPE_EINVAL, f"slo_us has {slo.shape[0]} entries for {ctx.n_models} models")
+    p = _EnumParams(max_partitions, _u32p(slo), margin_permille)
+    f = _FrontierPB()
+    _check(lib().ppipe_pareto_pb(ctx.handle, ct.byref(p), 1 if copy_to_host else 0, ct.byref(f)), ctx.handle)
+    return _frontier_from(f, copy_to_host, zero_copy, POINT_PB_DTYPE)
 
 
 def frontier_at(ctx: Context, slo_us: np.ndarray, margin_permille: int, copy_to_host: bool = True,
@@ -324,13 +351,16 @@ def partition_rows(n_layers: Sequence[int], n_classes: int, n_batches: int, max_
 
 def run(w, rank: int = 0, world: int = 1, device: int = -1, nccl_id: Optional[bytes] = None,
         copy_to_host: bool = True, vgpu: Optional[Sequence[int]] = None, frontier: int = 1) -> Frontier:
-    """One full pass: load, (set_vgpu), enumerate, pareto, free. frontier=2: F2 (pareto_f2)."""
+    """One full pass: load, (set_vgpu), enumerate, pareto, free. frontier=2: F2 (pareto_f2);
+    frontier=3: per-stage batch sizes (pareto_pb)."""
     ctx = load_workload(w, rank, world, device, nccl_id)
     try:
         if vgpu is not None:
             set_vgpu(ctx, vgpu)
         if frontier == 2:
             return pareto_f2(ctx, w.kmax, w.slo_us, w.margin_permille, copy_to_host)
+        if frontier == 3:
+            return pareto_pb(ctx, w.kmax, w.slo_us, w.margin_permille, copy_to_host)
         enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
         return pareto(ctx, copy_to_host)
     finally:

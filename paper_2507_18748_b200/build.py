@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libppipe_b200.so")
-SOURCES = [os.path.join(CSRC, "ppipe_kernels.cu"), os.path.join(CSRC, "ppipe_f2.cu"), os.path.join(CSRC, "ppipe_abi.cpp")]
+SOURCES = [os.path.join(CSRC, "ppipe_kernels.cu"), os.path.join(CSRC, "ppipe_f2.cu"), os.path.join(CSRC, "ppipe_pb.cu"), os.path.join(CSRC, "ppipe_abi.cpp")]
 HEADERS = [os.path.join(CSRC, "ppipe_internal.h"), os.path.join(ROOT, "include", "ppipe.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -1174,47 +1174,161 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
 // scored whole by the rank that holds its row 0 (its K = 1 row), so each rank's
 // frontier is final for its models and the global one is the rank-ordered
 // concatenation.
-PPIPE_API int ppipe_pareto_f2(ppipe_ctx* c, const ppipe_enum_params* p, int copy_to_host, ppipe_frontier* out) {
-  if (!c) return fail(nullptr, PPIPE_EINVAL, "ppipe_pareto_f2: NULL ctx");
-  if (!out) return fail(c, PPIPE_EINVAL, "ppipe_pareto_f2: NULL output");
-  int rc = check_params(c, p, "ppipe_pareto_f2");
+static_assert(sizeof(ppipe_point_pb) == sizeof(ppipe_point) && offsetof(ppipe_point_pb, K) == offsetof(ppipe_point, K) &&
+                  offsetof(ppipe_point_pb, cls) == offsetof(ppipe_point, cls),
+              "per-stage-batch records share the point buffers and the segment-offset kernels");
+
+// Models owned by this rank for the whole-model paths (F2, per-stage batch): the rank
+// holding a model's row 0 (its K = 1 row) scores all of it.
+static int owned_models(ppipe_ctx* c, std::vector<int>* own, const char* who) {
+  own->clear();
+  for (size_t i = 0; i < c->local.size(); ++i)
+    if (c->h_models[i].row_lo == 0 && c->h_models[i].row_hi > 0) own->push_back((int)i);
+  (void)who;
+  return PPIPE_OK;
+}
+
+// Candidate count of the owned models: sum_K C(M-1, K-1) * C^K * B^(K if per_stage else 1).
+static uint64_t owned_candidates(ppipe_ctx* c, const std::vector<int>& own, int Kmax, bool per_stage) {
+  uint64_t n = 0;
+  for (int i : own) {
+    const uint32_t M = c->h_models[i].M;
+    uint64_t pw = 1, bw = 1, comb = 1;
+    for (uint32_t K = 1; K <= (uint32_t)Kmax && K <= M; ++K) {
+      pw *= c->C;
+      bw = per_stage ? bw * c->B : c->B;
+      n += comb * pw * bw;
+      comb = comb * (M - K) / K;
+    }
+  }
+  return n;
+}
+
+// Whole-model paths under NCCL: every rank's points (32-byte records in canonical
+// order, owned models only) are final, so the global result is their rank-ordered
+// concatenation (counts all-gather + one padded all-gather), then the CSR.
+static int concat_owned(ppipe_ctx* c, uint64_t* n_pts, uint64_t n_cand, uint64_t n_feas_local, uint64_t* n_cand_all,
+                        uint64_t* n_feas_all, const ppipe_point** d_pts, const uint64_t** d_off, int* nl) {
+  *d_pts = c->d_local.p;
+  *d_off = c->d_segoff_local.p;
+  *n_cand_all = n_cand;
+  *n_feas_all = n_feas_local;
+  if (!(c->world > 1 && c->comm)) return PPIPE_OK;
+  constexpr int kCnt = 3;
+  CU(c, c->d_cnt_send.reserve(kCnt));
+  CU(c, c->d_cnt_recv.reserve(kCnt * (size_t)c->world));
+  uint64_t hs[kCnt] = {*n_pts, n_cand, n_feas_local};
+  CU(c, cudaMemcpyAsync(c->d_cnt_send.p, hs, sizeof hs, cudaMemcpyHostToDevice, c->stream));
+  NC_(c, g_nccl.AllGather(c->d_cnt_send.p, c->d_cnt_recv.p, kCnt, ncclUint64, c->comm, c->stream));
+  std::vector<uint64_t> cnts(kCnt * (size_t)c->world);
+  CU(c, cudaMemcpyAsync(cnts.data(), c->d_cnt_recv.p, 8 * cnts.size(), cudaMemcpyDeviceToHost, c->stream));
+  CU(c, cudaStreamSynchronize(c->stream));
+  uint64_t maxc = 1, tot = 0;
+  *n_cand_all = *n_feas_all = 0;
+  for (int r = 0; r < c->world; ++r) {
+    maxc = std::max(maxc, cnts[kCnt * r]);
+    tot += cnts[kCnt * r];
+    *n_cand_all += cnts[kCnt * r + 1];
+    *n_feas_all += cnts[kCnt * r + 2];
+  }
+  if (c->d_local.n < maxc) {
+    DevBuf<ppipe_point> tmp;
+    CU(c, tmp.reserve(maxc));
+    if (*n_pts)
+      CU(c, cudaMemcpyAsync(tmp.p, c->d_local.p, sizeof(ppipe_point) * *n_pts, cudaMemcpyDeviceToDevice, c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
+    c->d_local.release();
+    c->d_local = tmp;
+  }
+  CU(c, c->d_gather.reserve(maxc * c->world));
+  NC_(c, g_nccl.AllGather(c->d_local.p, c->d_gather.p, maxc * sizeof(ppipe_point), ncclUint8, c->comm, c->stream));
+  CU(c, c->d_final.reserve(std::max<uint64_t>(tot, 1)));
+  uint64_t w = 0;
+  for (int r = 0; r < c->world; ++r) {
+    const uint64_t n = cnts[kCnt * r];
+    if (n)
+      CU(c, cudaMemcpyAsync(c->d_final.p + w, c->d_gather.p + (uint64_t)r * maxc, sizeof(ppipe_point) * n,
+                            cudaMemcpyDeviceToDevice, c->stream));
+    w += n;
+  }
+  *n_pts = w;
+  CU(c, c->d_segoff_final.reserve(c->n_seg_total + 1));
+  CU(c, c->d_segtmp.reserve(std::max<uint64_t>(w, 1)));
+  CU(c, segment_offsets(c->d_final.p, w, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_segoff_final.p,
+                        c->d_segtmp.p, c->stream, nl));
+  *nl += 2;
+  *d_pts = c->d_final.p;
+  *d_off = c->d_segoff_final.p;
+  return PPIPE_OK;
+}
+
+// Phase times, launch count and the optional host copy (into the page-locked buffers)
+// of a whole-model path's result.
+static int publish_owned(ppipe_ctx* c, int nl, const ppipe_point* d_pts, const uint64_t* d_off, uint64_t n_pts,
+                         int copy_to_host, const ppipe_point** h_pts, const uint64_t** h_off) {
+  CU(c, cudaEventRecord(c->ev[4], c->stream));
+  CU(c, cudaEventSynchronize(c->ev[4]));
+  cudaEventElapsedTime(&c->phase_ms[0], c->ev[0], c->ev[1]);
+  cudaEventElapsedTime(&c->phase_ms[1], c->ev[1], c->ev[2]);
+  cudaEventElapsedTime(&c->phase_ms[2], c->ev[2], c->ev[3]);
+  cudaEventElapsedTime(&c->phase_ms[3], c->ev[3], c->ev[4]);
+  c->launches = (uint64_t)nl;
+  *h_pts = nullptr;
+  *h_off = nullptr;
+  if (copy_to_host) {
+    CU(c, c->h_points.reserve(n_pts));
+    CU(c, c->h_segoff.reserve(c->n_seg_total + 1));
+    if (n_pts)
+      CU(c, cudaMemcpyAsync(c->h_points.p, d_pts, sizeof(ppipe_point) * n_pts, cudaMemcpyDeviceToHost, c->stream));
+    CU(c, cudaMemcpyAsync(c->h_segoff.p, d_off, 8 * (c->n_seg_total + 1), cudaMemcpyDeviceToHost, c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
+    *h_pts = c->h_points.p;
+    *h_off = c->h_segoff.p;
+  }
+  return PPIPE_OK;
+}
+
+// Shared prologue of the whole-model paths: parameter checks, owned models, problem setup.
+static int whole_model_setup(ppipe_ctx* c, const ppipe_enum_params* p, const char* who, std::vector<int>* own,
+                             Problem* pb) {
+  int rc = check_params(c, p, who);
   if (rc != PPIPE_OK) return rc;
   if (c->pending_upload)
-    return fail(c, PPIPE_ESTATE, "ppipe_pareto_f2: profiles from ppipe_update_profiles_async are uploaded by "
-                                 "ppipe_enumerate only; use ppipe_update_profiles");
-  std::vector<int> own;  // local indices of the models this rank scores
-  for (size_t i = 0; i < c->local.size(); ++i)
-    if (c->h_models[i].row_lo == 0 && c->h_models[i].row_hi > 0) own.push_back((int)i);
-  for (int i : own)
-    if (c->h_models[i].M > kF2MaxLayers)
-      return fail(c, PPIPE_ERANGE, "model %d: %u layers; F2 supports at most %u", c->local[i], c->h_models[i].M,
-                  kF2MaxLayers);
+    return fail(c, PPIPE_ESTATE, "%s: profiles from ppipe_update_profiles_async are uploaded by ppipe_enumerate only; "
+                                 "use ppipe_update_profiles", who);
+  owned_models(c, own, who);
   CU(c, cudaSetDevice(c->device));
   c->have_result = false;
   c->enumerated = false;
   c->last_params = *p;
   c->last_slo.assign(p->slo_us, p->slo_us + c->n_models);
   c->last_params.slo_us = c->last_slo.data();
+  return setup_problem(c, pb);
+}
+
+PPIPE_API int ppipe_pareto_f2(ppipe_ctx* c, const ppipe_enum_params* p, int copy_to_host, ppipe_frontier* out) {
+  if (!c) return fail(nullptr, PPIPE_EINVAL, "ppipe_pareto_f2: NULL ctx");
+  if (!out) return fail(c, PPIPE_EINVAL, "ppipe_pareto_f2: NULL output");
+  std::vector<int> own;
+  if (p)
+    for (size_t i = 0; i < c->local.size(); ++i)
+      if (c->h_models[i].row_lo == 0 && c->h_models[i].M > kF2MaxLayers)
+        return fail(c, PPIPE_ERANGE, "model %d: %u layers; F2 supports at most %u", c->local[i], c->h_models[i].M,
+                    kF2MaxLayers);
   Problem pb{};
-  rc = setup_problem(c, &pb);
+  int rc = whole_model_setup(c, p, "ppipe_pareto_f2", &own, &pb);
   if (rc != PPIPE_OK) return rc;
   if (c->n_seg_total >= (1ull << 28)) return fail(c, PPIPE_ERANGE, "F2: %llu segments >= 2^28",
                                                   (unsigned long long)c->n_seg_total);
   const int Kmax = (int)p->max_partitions;
   // G: all C^3 segments of the largest model, capped at PPIPE_F2_G_BYTES (default 8 GiB), at least one segment
   size_t g_need = 0, f_need = 1;
-  uint64_t n_cand = 0;
   for (int i : own) {
     const uint32_t M = c->h_models[i].M;
     g_need = std::max(g_need, f2_g3_elems_per_segment((int)c->B, M) * c->C * c->C * c->C);
     f_need = std::max<size_t>(f_need, (size_t)c->C * c->C * c->B * M);
-    uint64_t pw = 1, comb = 1;  // C(M-1, K-1) * C^K * B
-    for (uint32_t K = 1; K <= (uint32_t)Kmax && K <= M; ++K) {
-      pw *= c->C;
-      n_cand += comb * pw * c->B;
-      comb = comb * (M - K) / K;
-    }
   }
+  const uint64_t n_cand = owned_candidates(c, own, Kmax, false);
   size_t g_budget = 8ull << 30;
   if (const char* gb = getenv("PPIPE_F2_G_BYTES")) g_budget = (size_t)strtoull(gb, nullptr, 10);
   size_t g_cap = std::min(g_need, g_budget / sizeof(int32_t));
@@ -1254,64 +1368,14 @@ PPIPE_API int ppipe_pareto_f2(ppipe_ctx* c, const ppipe_enum_params* p, int copy
   CU(c, f2_finalize(c->d_f2surv.p, n_surv, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_local.p, c->d_f2tmp.p,
                     c->d_segoff_local.p, c->d_segtmp.p, &n_pts, &c->scratch, c->stream, &nl));
   CU(c, cudaEventRecord(c->ev[3], c->stream));
-  const ppipe_point* d_pts = c->d_local.p;
-  const uint64_t* d_off = c->d_segoff_local.p;
-  uint64_t n_cand_all = n_cand, n_feas_all = n_feas_local;
-  if (c->world > 1 && c->comm) {
-    constexpr int kCnt = 3;
-    CU(c, c->d_cnt_send.reserve(kCnt));
-    CU(c, c->d_cnt_recv.reserve(kCnt * (size_t)c->world));
-    uint64_t hs[kCnt] = {n_pts, n_cand, n_feas_local};
-    CU(c, cudaMemcpyAsync(c->d_cnt_send.p, hs, sizeof hs, cudaMemcpyHostToDevice, c->stream));
-    NC_(c, g_nccl.AllGather(c->d_cnt_send.p, c->d_cnt_recv.p, kCnt, ncclUint64, c->comm, c->stream));
-    std::vector<uint64_t> cnts(kCnt * (size_t)c->world);
-    CU(c, cudaMemcpyAsync(cnts.data(), c->d_cnt_recv.p, 8 * cnts.size(), cudaMemcpyDeviceToHost, c->stream));
-    CU(c, cudaStreamSynchronize(c->stream));
-    uint64_t maxc = 1, tot = 0;
-    n_cand_all = n_feas_all = 0;
-    for (int r = 0; r < c->world; ++r) {
-      maxc = std::max(maxc, cnts[kCnt * r]);
-      tot += cnts[kCnt * r];
-      n_cand_all += cnts[kCnt * r + 1];
-      n_feas_all += cnts[kCnt * r + 2];
-    }
-    if (c->d_local.n < maxc) {
-      DevBuf<ppipe_point> tmp;
-      CU(c, tmp.reserve(maxc));
-      if (n_pts)
-        CU(c, cudaMemcpyAsync(tmp.p, c->d_local.p, sizeof(ppipe_point) * n_pts, cudaMemcpyDeviceToDevice, c->stream));
-      CU(c, cudaStreamSynchronize(c->stream));
-      c->d_local.release();
-      c->d_local = tmp;
-    }
-    CU(c, c->d_gather.reserve(maxc * c->world));
-    NC_(c, g_nccl.AllGather(c->d_local.p, c->d_gather.p, maxc * sizeof(ppipe_point), ncclUint8, c->comm, c->stream));
-    CU(c, c->d_final.reserve(std::max<uint64_t>(tot, 1)));
-    uint64_t w = 0;
-    for (int r = 0; r < c->world; ++r) {
-      const uint64_t n = cnts[kCnt * r];
-      if (n)
-        CU(c, cudaMemcpyAsync(c->d_final.p + w, c->d_gather.p + (uint64_t)r * maxc, sizeof(ppipe_point) * n,
-                              cudaMemcpyDeviceToDevice, c->stream));
-      w += n;
-    }
-    n_pts = w;
-    CU(c, c->d_segoff_final.reserve(c->n_seg_total + 1));
-    CU(c, c->d_segtmp.reserve(std::max<uint64_t>(n_pts, 1)));
-    CU(c, segment_offsets(c->d_final.p, n_pts, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_segoff_final.p,
-                          c->d_segtmp.p, c->stream, &nl));
-    nl += 2;
-    d_pts = c->d_final.p;
-    d_off = c->d_segoff_final.p;
-  }
-  CU(c, cudaEventRecord(c->ev[4], c->stream));
-  CU(c, cudaEventSynchronize(c->ev[4]));
-  cudaEventElapsedTime(&c->phase_ms[0], c->ev[0], c->ev[1]);
-  cudaEventElapsedTime(&c->phase_ms[1], c->ev[1], c->ev[2]);
-  cudaEventElapsedTime(&c->phase_ms[2], c->ev[2], c->ev[3]);
-  cudaEventElapsedTime(&c->phase_ms[3], c->ev[3], c->ev[4]);
-  c->launches = (uint64_t)nl;
+  const ppipe_point* d_pts = nullptr;
+  const uint64_t* d_off = nullptr;
+  uint64_t n_cand_all = 0, n_feas_all = 0;
+  if ((rc = concat_owned(c, &n_pts, n_cand, n_feas_local, &n_cand_all, &n_feas_all, &d_pts, &d_off, &nl)) != PPIPE_OK)
+    return rc;
   std::memset(out, 0, sizeof *out);
+  if ((rc = publish_owned(c, nl, d_pts, d_off, n_pts, copy_to_host, &out->points, &out->seg_offsets)) != PPIPE_OK)
+    return rc;
   out->n_candidates = n_cand_all;
   out->n_feasible = n_feas_all;
   out->n_points = n_pts;
@@ -1321,16 +1385,62 @@ PPIPE_API int ppipe_pareto_f2(ppipe_ctx* c, const ppipe_enum_params* p, int copy
   out->n_survivors = n_surv;
   out->n_candidates_local = n_cand;
   out->n_feasible_local = n_feas_local;
-  if (copy_to_host) {
-    CU(c, c->h_points.reserve(n_pts));
-    CU(c, c->h_segoff.reserve(c->n_seg_total + 1));
-    if (n_pts)
-      CU(c, cudaMemcpyAsync(c->h_points.p, d_pts, sizeof(ppipe_point) * n_pts, cudaMemcpyDeviceToHost, c->stream));
-    CU(c, cudaMemcpyAsync(c->h_segoff.p, d_off, 8 * (c->n_seg_total + 1), cudaMemcpyDeviceToHost, c->stream));
+  return PPIPE_OK;
+}
+
+PPIPE_API int ppipe_pareto_pb(ppipe_ctx* c, const ppipe_enum_params* p, int copy_to_host, ppipe_frontier_pb* out) {
+  if (!c) return fail(nullptr, PPIPE_EINVAL, "ppipe_pareto_pb: NULL ctx");
+  if (!out) return fail(c, PPIPE_EINVAL, "ppipe_pareto_pb: NULL output");
+  if (c->B > 255) return fail(c, PPIPE_ERANGE, "ppipe_pareto_pb: %u batch sizes; at most 255", c->B);
+  std::vector<int> own;
+  Problem pb{};
+  int rc = whole_model_setup(c, p, "ppipe_pareto_pb", &own, &pb);
+  if (rc != PPIPE_OK) return rc;
+  const int Kmax = (int)p->max_partitions;
+  const uint64_t n_cand = owned_candidates(c, own, Kmax, true);
+  int nl = 0;
+  for (;;) {
+    CU(c, c->d_f2surv.reserve(c->f2_cap));
+    PbOut po{reinterpret_cast<ppipe_point_pb*>(c->d_f2surv.p), c->d_counters.p, (unsigned long long)c->d_f2surv.n};
+    nl = 0;
+    CU(c, cudaEventRecord(c->ev[0], c->stream));
+    CU(c, launch_pack(pb, c->stream));
+    nl += pb.n_local ? 2 : 0;
+    CU(c, cudaEventRecord(c->ev[1], c->stream));
+    CU(c, cudaMemsetAsync(c->d_counters.p, 0, 16 * sizeof(unsigned long long), c->stream));
+    for (int i : own) CU(c, launch_pb_model(pb, i, c->h_models[i].M, Kmax, po, c->stream, &nl));
+    CU(c, cudaEventRecord(c->ev[2], c->stream));
+    CU(c, cudaMemcpyAsync(c->h_counters, c->d_counters.p, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          c->stream));
     CU(c, cudaStreamSynchronize(c->stream));
-    out->points = c->h_points.p;
-    out->seg_offsets = c->h_segoff.p;
+    if (c->h_counters[0] <= c->d_f2surv.n) break;
+    c->f2_cap = c->h_counters[0] + c->h_counters[0] / 4 + 1024;  // deterministic: re-run with room
   }
+  const uint64_t n_surv = c->h_counters[0], n_feas_local = c->h_counters[1];
+  CU(c, c->d_local.reserve(std::max<uint64_t>(n_surv, 1)));
+  CU(c, c->d_segoff_local.reserve(c->n_seg_total + 1));
+  uint64_t n_pts = 0;
+  CU(c, pb_frontier_pass(reinterpret_cast<const ppipe_point_pb*>(c->d_f2surv.p), n_surv, c->d_segbase.p, (int)c->C,
+                         c->n_seg_total, c->d_batches.p, (int)c->B, reinterpret_cast<ppipe_point_pb*>(c->d_local.p),
+                         c->d_segoff_local.p, &n_pts, &c->scratch, c->stream, &nl));
+  CU(c, cudaEventRecord(c->ev[3], c->stream));
+  const ppipe_point* d_pts = nullptr;
+  const uint64_t* d_off = nullptr;
+  uint64_t n_cand_all = 0, n_feas_all = 0;
+  if ((rc = concat_owned(c, &n_pts, n_cand, n_feas_local, &n_cand_all, &n_feas_all, &d_pts, &d_off, &nl)) != PPIPE_OK)
+    return rc;
+  std::memset(out, 0, sizeof *out);
+  const ppipe_point* h_pts = nullptr;
+  if ((rc = publish_owned(c, nl, d_pts, d_off, n_pts, copy_to_host, &h_pts, &out->seg_offsets)) != PPIPE_OK)
+    return rc;
+  out->points = reinterpret_cast<const ppipe_point_pb*>(h_pts);
+  out->n_candidates = n_cand_all;
+  out->n_feasible = n_feas_all;
+  out->n_points = n_pts;
+  out->n_segments = c->n_seg_total;
+  out->d_points = reinterpret_cast<const ppipe_point_pb*>(d_pts);
+  out->d_seg_offsets = d_off;
+  out->n_survivors = n_surv;
   return PPIPE_OK;
 }
 

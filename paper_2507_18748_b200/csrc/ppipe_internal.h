@@ -116,6 +116,18 @@ cudaError_t truncate_frontier(const ppipe_point* in, const uint64_t* seg_offsets
                               const uint32_t* T_new, ppipe_point* out, uint64_t* seg_offsets_out,
                               uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches);
 
+// Per-stage batch sizes (ppipe_pb.cu).
+struct PbOut {
+  ppipe_point_pb* surv;
+  unsigned long long* counters;  // [0] survivors appended, [1] feasible
+  unsigned long long cap;
+};
+cudaError_t launch_pb_model(const Problem& pb, int local_model, uint32_t M, int Kmax, const PbOut& out,
+                            cudaStream_t s, int* n_launches);
+cudaError_t pb_frontier_pass(const ppipe_point_pb* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t n_seg,
+                             const uint16_t* batches, int B, ppipe_point_pb* out, uint64_t* seg_offsets,
+                             uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches);
+
 // F2 tail: resolve equal vectors (keep the smallest (E, b, c_1, c_2) of each run),
 // sort into (segment, b, c_1, c_2) order and build the CSR. tmp_pts holds n records.
 cudaError_t f2_finalize(const ppipe_point* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t n_seg,

@@ -1,0 +1,389 @@
+// ppipe_pb.cu -- per-stage batch sizes (App. A.1).
+//
+// The basic MILP of App. A.1 lets every partition run its own batch size: eq. 1.1
+// sums p_{ldbij} over (b, i, j) per partition d. A candidate is
+// (cuts, classes, b_1..b_K) with
+//   C_d = sum of lat[k_d][l][b_d] over partition d              (eq. 1.9)
+//   Y_d = ceil(8 S[c_d - 1] b_d / bw[k_d][k_{d+1}]), d < K       (eq. 1.11: the sender's batch)
+//   E = sum C_d + sum Y_d <= T_eff                               (eq. 1.12)
+//   theta = min_d b_d / C_d                                      (x_l = min_d x_ld)
+// reduced per segment to the (E min, theta max) staircase; ties on identical
+// (E, theta) keep the smallest (b_1..b_K) (lexicographic batch indices), then the
+// smallest (c_1, c_2) (PB-1..PB-4). B^K times the unified candidates.
+//
+// pb_score_kernel<K>: one CTA per unit (K = 3: segment, c_1, b_2; K = 2: segment, b_1;
+// K = 1: segment) enumerates the unit's candidates twice. Pass 1 folds each feasible
+// candidate's theta into its E-bucket (atomicMax on an order-preserving 64-bit key,
+// see theta_key); an exclusive prefix maximum over the buckets then gives, per bucket,
+// the best theta of every smaller E. Pass 2 emits only the candidates above it -- a
+// candidate at or below it is beaten by a feasible candidate with strictly smaller E,
+// so the drop is exact and the survivors' frontier is the unit's. pb_frontier_pass
+// reduces all survivors: sort by (segment, E), best per (segment, E), strict
+// staircase over theta, CSR.
+#include <cub/cub.cuh>
+#include <climits>
+
+#include "ppipe_internal.h"
+
+namespace ppipe {
+
+namespace {
+
+constexpr int kPbThreads = 256;
+constexpr int kPbBuckets = 1024;  // E-buckets per unit (4 per thread in the prefix scan)
+
+__device__ __forceinline__ const int32_t* prow_pb(const Problem& pb, const DevModel& md, int k, int bi) {
+  return pb.P + md.p_off + ((size_t)k * pb.B + bi) * md.Mp;
+}
+__device__ __forceinline__ const int32_t* yrow_pb(const Problem& pb, const DevModel& md, int k, int k2, int bi) {
+  return pb.Y + md.y_off + ((size_t)pb.pair_v[k * pb.C + k2] * pb.B + bi) * md.Mp;
+}
+
+// theta = b / C as a double is exact-order-preserving for b < 2^16, C < 2^28: two distinct
+// fractions differ by a relative 1 / (b s) >= 2^-44, far above the 2^-53 rounding of each,
+// and equal fractions round alike. Positive doubles (and +inf for C = 0) order as their
+// bit patterns, so theta compares as one 64-bit integer.
+__device__ __forceinline__ double stage_theta(uint32_t b, int32_t Cd) {
+  return Cd > 0 ? (double)b / (double)Cd : __longlong_as_double(0x7FF0000000000000ll);
+}
+__device__ __forceinline__ unsigned long long theta_key(double th) {
+  return (unsigned long long)__double_as_longlong(th);
+}
+
+struct PbCand {
+  int32_t E, C1, C2, C3;
+  int c1, c2, b1, b2, b3;  // cuts and batch indices
+};
+
+// Candidate t of unit `unit` (see pb_score_kernel); returns false past the unit's end.
+template <int K>
+__device__ __forceinline__ void pb_candidate(const Problem& pb, const DevModel& md, int M, int k1, int k2, int k3,
+                                             int c1u, int b2u, int b1u, int t, PbCand& c) {
+  const int B = pb.B;
+  if constexpr (K == 3) {
+    c.b3 = t % B;
+    c.b1 = (t / B) % B;
+    c.b2 = b2u;
+    c.c1 = c1u;
+    c.c2 = c1u + 1 + t / (B * B);
+    const int32_t *P1 = prow_pb(pb, md, k1, c.b1), *P2 = prow_pb(pb, md, k2, c.b2), *P3 = prow_pb(pb, md, k3, c.b3);
+    c.C1 = P1[c.c1];
+    c.C2 = P2[c.c2] - P2[c.c1];
+    c.C3 = P3[M] - P3[c.c2];
+    c.E = c.C1 + c.C2 + c.C3 + yrow_pb(pb, md, k1, k2, c.b1)[c.c1] + yrow_pb(pb, md, k2, k3, c.b2)[c.c2];
+  } else if constexpr (K == 2) {
+    c.b2 = t % B;
+    c.b1 = b1u;
+    c.b3 = 0xFF;
+    c.c1 = 1 + t / B;
+    c.c2 = 0;
+    const int32_t *P1 = prow_pb(pb, md, k1, c.b1), *P2 = prow_pb(pb, md, k2, c.b2);
+    c.C1 = P1[c.c1];
+    c.C2 = P2[M] - P2[c.c1];
+    c.C3 = 0;
+    c.E = c.C1 + c.C2 + yrow_pb(pb, md, k1, k2, c.b1)[c.c1];
+  } else {
+    c.b1 = t;
+    c.b2 = c.b3 = 0xFF;
+    c.c1 = c.c2 = 0;
+    c.C1 = prow_pb(pb, md, k1, c.b1)[M];
+    c.C2 = c.C3 = 0;
+    c.E = c.C1;
+  }
+}
+
+template <int K>
+__device__ __forceinline__ unsigned long long pb_key(const Problem& pb, const PbCand& c) {
+  double th = stage_theta(pb.batches[c.b1], c.C1);
+  if constexpr (K >= 2) th = fmin(th, stage_theta(pb.batches[c.b2], c.C2));
+  if constexpr (K >= 3) th = fmin(th, stage_theta(pb.batches[c.b3], c.C3));
+  return theta_key(th);
+}
+
+template <int K>
+__global__ void __launch_bounds__(kPbThreads) pb_score_kernel(Problem pb, int ml, PbOut out) {
+  using Scan = cub::BlockScan<unsigned long long, kPbThreads>;
+  __shared__ unsigned long long tab[kPbBuckets];
+  __shared__ typename Scan::TempStorage scan_tmp;
+  const DevModel md = pb.models[ml];
+  const int M = (int)md.M, C = pb.C, B = pb.B;
+  const int32_t T = md.T;
+  int seg, c1u = 0, b2u = 0, b1u = 0, n;
+  if constexpr (K == 3) {
+    b2u = blockIdx.x % B;
+    c1u = 1 + (blockIdx.x / B) % (M - 2);
+    seg = blockIdx.x / (B * (M - 2));
+    n = (M - 1 - c1u) * B * B;
+  } else if constexpr (K == 2) {
+    b1u = blockIdx.x % B;
+    seg = blockIdx.x / B;
+    n = (M - 1) * B;
+  } else {
+    seg = blockIdx.x;
+    n = B;
+  }
+  int k1, k2 = 0, k3 = 0;
+  if constexpr (K == 3) {
+    k1 = seg / (C * C);
+    k2 = (seg / C) % C;
+    k3 = seg % C;
+  } else if constexpr (K == 2) {
+    k1 = seg / C;
+    k2 = seg % C;
+  } else {
+    k1 = seg;
+  }
+  for (int i = threadIdx.x; i < kPbBuckets; i += blockDim.x) tab[i] = 0;
+  __syncthreads();
+  const uint64_t span = (uint64_t)T + 1;
+  unsigned long long feas = 0;
+  // pass 1: best theta per E-bucket
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    PbCand c;
+    pb_candidate<K>(pb, md, M, k1, k2, k3, c1u, b2u, b1u, t, c);
+    if (c.E <= T) {
+      ++feas;
+      atomicMax(&tab[(uint64_t)c.E * kPbBuckets / span], pb_key<K>(pb, c));
+    }
+  }
+  __syncthreads();
+  // exclusive prefix maximum: the best theta at any strictly smaller bucket
+  {
+    unsigned long long v[kPbBuckets / kPbThreads];
+#pragma unroll
+    for (int i = 0; i < kPbBuckets / kPbThreads; ++i) v[i] = tab[threadIdx.x * (kPbBuckets / kPbThreads) + i];
+    Scan(scan_tmp).ExclusiveScan(v, v, 0ull, cub::Max());
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kPbBuckets / kPbThreads; ++i) tab[threadIdx.x * (kPbBuckets / kPbThreads) + i] = v[i];
+  }
+  __syncthreads();
+  // pass 2: emit what no smaller-E bucket beats (warp-uniform trip count for the ballot)
+  const int lane = threadIdx.x & 31;
+  for (int t0 = 0; t0 < n; t0 += blockDim.x) {
+    const int t = t0 + threadIdx.x;
+    bool want = false;
+    PbCand c;
+    if (t < n) {
+      pb_candidate<K>(pb, md, M, k1, k2, k3, c1u, b2u, b1u, t, c);
+      want = c.E <= T && pb_key<K>(pb, c) > tab[(uint64_t)c.E * kPbBuckets / span];
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, want);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(&out.counters[0], (unsigned long long)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (want) {
+        const unsigned long long i = base + __popc(m & ((1u << lane) - 1));
+        if (i < out.cap) {
+          ppipe_point_pb p;
+          p.model = md.model;
+          p.cut[0] = (uint16_t)c.c1;
+          p.cut[1] = (uint16_t)c.c2;
+          p.K = (uint8_t)K;
+          p.cls[0] = (uint8_t)k1;
+          p.cls[1] = K >= 2 ? (uint8_t)k2 : (uint8_t)0xFF;
+          p.cls[2] = K >= 3 ? (uint8_t)k3 : (uint8_t)0xFF;
+          p.bidx[0] = (uint8_t)c.b1;
+          p.bidx[1] = K >= 2 ? (uint8_t)c.b2 : (uint8_t)0xFF;
+          p.bidx[2] = K >= 3 ? (uint8_t)c.b3 : (uint8_t)0xFF;
+          p.reserved = 0;
+          p.e2e_us = (uint32_t)c.E;
+          p.stage_us[0] = (uint32_t)c.C1;
+          p.stage_us[1] = (uint32_t)c.C2;
+          p.stage_us[2] = (uint32_t)c.C3;
+          out.surv[i] = p;
+        }
+      }
+    }
+  }
+  for (int off = 16; off; off >>= 1) feas += __shfl_down_sync(0xffffffffu, feas, off);
+  if (lane == 0 && feas) atomicAdd(&out.counters[1], feas);
+}
+
+// ---------------------------------------------------------------------------
+// frontier pass over per-stage-batch survivors
+// ---------------------------------------------------------------------------
+constexpr int kEBitsPb = 28;
+
+__device__ __forceinline__ uint64_t seg_of_pb(const ppipe_point_pb& p, const uint64_t* seg_base, int C) {
+  uint64_t off = 0, pw = 1;
+  for (int k = 1; k < p.K; ++k) {
+    pw *= (uint64_t)C;
+    off += pw;
+  }
+  uint64_t idx = 0;
+  for (int d = 0; d < p.K; ++d) idx = idx * C + p.cls[d];
+  return seg_base[p.model] + off + idx;
+}
+
+// theta key of a record. CUB's reduce-by-key may also apply its operator to the unused
+// slots of a partial tile, so K and the batch indices are clamped: garbage in, no fault.
+__device__ __forceinline__ unsigned long long rec_key(const ppipe_point_pb& p, const uint16_t* batches, int B) {
+  const int K = min((int)p.K, 3);
+  double th = stage_theta(batches[min((int)p.bidx[0], B - 1)], (int32_t)p.stage_us[0]);
+  for (int d = 1; d < K; ++d) th = fmin(th, stage_theta(batches[min((int)p.bidx[d], B - 1)], (int32_t)p.stage_us[d]));
+  return theta_key(th);
+}
+
+__global__ void pb_keys_kernel(const ppipe_point_pb* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t* keys,
+                               uint32_t* vals) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    keys[i] = (seg_of_pb(in[i], seg_base, C) << kEBitsPb) | (uint64_t)in[i].e2e_us;
+    vals[i] = (uint32_t)i;
+  }
+}
+
+__global__ void pb_gather_kernel(const ppipe_point_pb* in, const uint32_t* idx, uint64_t n, ppipe_point_pb* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = in[idx[i]];
+}
+
+// Among records with the same (segment, E): theta desc, then batch indices asc, then cuts asc.
+struct PickBetterPb {
+  const uint16_t* batches;
+  int B;
+  __device__ __forceinline__ ppipe_point_pb operator()(const ppipe_point_pb& a, const ppipe_point_pb& b) const {
+    const unsigned long long ka = rec_key(a, batches, B), kb = rec_key(b, batches, B);
+    if (ka != kb) return ka > kb ? a : b;
+    for (int d = 0; d < min((int)a.K, 3); ++d)
+      if (a.bidx[d] != b.bidx[d]) return a.bidx[d] < b.bidx[d] ? a : b;
+    if (a.cut[0] != b.cut[0]) return a.cut[0] < b.cut[0] ? a : b;
+    return a.cut[1] <= b.cut[1] ? a : b;
+  }
+};
+
+__global__ void pb_group_kernel(const uint64_t* gkeys, const ppipe_point_pb* best, uint64_t ng,
+                                const uint16_t* batches, int B, uint64_t* segk, unsigned long long* th) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ng; i += (uint64_t)gridDim.x * blockDim.x) {
+    segk[i] = gkeys[i] >> kEBitsPb;
+    th[i] = rec_key(best[i], batches, B);
+  }
+}
+
+__global__ void pb_keep_kernel(const unsigned long long* th, const unsigned long long* prefix, uint64_t ng,
+                               uint8_t* keep) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ng; i += (uint64_t)gridDim.x * blockDim.x)
+    keep[i] = th[i] > prefix[i] ? 1 : 0;  // strictly above every smaller E of the segment
+}
+
+__global__ void pb_seg_start_kernel(const uint64_t* segs, uint64_t n, uint64_t n_seg, uint64_t* start) {
+  const uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (s > n_seg) return;
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (segs[mid] < s) lo = mid + 1;
+    else hi = mid;
+  }
+  start[s] = lo;
+}
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+}  // namespace
+
+cudaError_t launch_pb_model(const Problem& pb, int ml, uint32_t M, int Kmax, const PbOut& out, cudaStream_t s,
+                            int* n_launches) {
+  const int C = pb.C, B = pb.B;
+  pb_score_kernel<1><<<C, kPbThreads, 0, s>>>(pb, ml, out);
+  ++*n_launches;
+  if (Kmax >= 2 && M >= 2) {
+    pb_score_kernel<2><<<C * C * B, kPbThreads, 0, s>>>(pb, ml, out);
+    ++*n_launches;
+  }
+  if (Kmax >= 3 && M >= 3) {
+    pb_score_kernel<3><<<C * C * C * (int)(M - 2) * B, kPbThreads, 0, s>>>(pb, ml, out);
+    ++*n_launches;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t pb_frontier_pass(const ppipe_point_pb* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t n_seg,
+                             const uint16_t* batches, int B, ppipe_point_pb* out, uint64_t* seg_offsets,
+                             uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches) {
+  int seg_bits = 1;
+  while ((1ull << seg_bits) <= n_seg) ++seg_bits;
+  const int end_bit = kEBitsPb + seg_bits;
+  const int64_t ni = (int64_t)n;
+  size_t b_sort = 0, b_red = 0, b_scan = 0, b_sel = 0, b_sel2 = 0;
+  cudaError_t e;
+  if ((e = cub::DeviceRadixSort::SortPairs(nullptr, b_sort, (uint64_t*)nullptr, (uint64_t*)nullptr,
+                                           (uint32_t*)nullptr, (uint32_t*)nullptr, ni, 0, end_bit, s)) != cudaSuccess)
+    return e;
+  if ((e = cub::DeviceReduce::ReduceByKey(nullptr, b_red, (uint64_t*)nullptr, (uint64_t*)nullptr,
+                                          (ppipe_point_pb*)nullptr, (ppipe_point_pb*)nullptr, (int64_t*)nullptr,
+                                          PickBetterPb{nullptr, 1}, ni, s)) != cudaSuccess)
+    return e;
+  if ((e = cub::DeviceScan::ExclusiveScanByKey(nullptr, b_scan, (uint64_t*)nullptr, (unsigned long long*)nullptr,
+                                               (unsigned long long*)nullptr, cub::Max(), 0ull, ni, cub::Equality(),
+                                               s)) != cudaSuccess)
+    return e;
+  if ((e = cub::DeviceSelect::Flagged(nullptr, b_sel, (ppipe_point_pb*)nullptr, (uint8_t*)nullptr,
+                                      (ppipe_point_pb*)nullptr, (int64_t*)nullptr, ni, s)) != cudaSuccess)
+    return e;
+  if ((e = cub::DeviceSelect::Flagged(nullptr, b_sel2, (uint64_t*)nullptr, (uint8_t*)nullptr, (uint64_t*)nullptr,
+                                      (int64_t*)nullptr, ni, s)) != cudaSuccess)
+    return e;
+  const size_t tmpb = std::max(std::max(b_sort, b_red), std::max(b_scan, std::max(b_sel, b_sel2)));
+  const size_t nn = n > 0 ? n : 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align256(off + bytes);
+    return o;
+  };
+  const size_t o_k1 = take(nn * 8), o_k2 = take(nn * 8), o_v1 = take(nn * 4), o_v2 = take(nn * 4);
+  const size_t o_rec = take(nn * 32), o_best = take(nn * 32), o_gk = take(nn * 8), o_sk = take(nn * 8);
+  const size_t o_th = take(nn * 8), o_pre = take(nn * 8), o_keep = take(nn), o_num = take(16);
+  const size_t o_tmp = take(tmpb);
+  if (scratch->bytes < off) {
+    if (scratch->buf) cudaFree(scratch->buf);
+    scratch->buf = nullptr;
+    scratch->bytes = 0;
+    if ((e = cudaMalloc(&scratch->buf, off)) != cudaSuccess) return e;
+    scratch->bytes = off;
+  }
+  char* base = (char*)scratch->buf;
+  uint64_t *keys = (uint64_t*)(base + o_k1), *keys2 = (uint64_t*)(base + o_k2);
+  uint32_t *vals = (uint32_t*)(base + o_v1), *vals2 = (uint32_t*)(base + o_v2);
+  ppipe_point_pb *rec = (ppipe_point_pb*)(base + o_rec), *best = (ppipe_point_pb*)(base + o_best);
+  uint64_t *gkeys = (uint64_t*)(base + o_gk), *segk = (uint64_t*)(base + o_sk);
+  unsigned long long *th = (unsigned long long*)(base + o_th), *pre = (unsigned long long*)(base + o_pre);
+  uint8_t* keep = (uint8_t*)(base + o_keep);
+  int64_t* d_num = (int64_t*)(base + o_num);
+  void* tmp = base + o_tmp;
+  int64_t ng = 0, nk = 0;
+  if (n > 0) {
+    const int blocks = (int)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+    pb_keys_kernel<<<blocks, 256, 0, s>>>(in, n, seg_base, C, keys, vals);
+    if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, keys, keys2, vals, vals2, ni, 0, end_bit, s)) !=
+        cudaSuccess)
+      return e;
+    pb_gather_kernel<<<blocks, 256, 0, s>>>(in, vals2, n, rec);
+    if ((e = cub::DeviceReduce::ReduceByKey(tmp, b_red, keys2, gkeys, rec, best, d_num, PickBetterPb{batches, B}, ni,
+                                            s)) != cudaSuccess)
+      return e;
+    if ((e = cudaMemcpyAsync(&ng, d_num, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    const int gb = (int)std::min<int64_t>((ng + 255) / 256, 148 * 16);
+    pb_group_kernel<<<gb, 256, 0, s>>>(gkeys, best, (uint64_t)ng, batches, B, segk, th);
+    if ((e = cub::DeviceScan::ExclusiveScanByKey(tmp, b_scan, segk, th, pre, cub::Max(), 0ull, ng, cub::Equality(),
+                                                 s)) != cudaSuccess)
+      return e;
+    pb_keep_kernel<<<gb, 256, 0, s>>>(th, pre, (uint64_t)ng, keep);
+    if ((e = cub::DeviceSelect::Flagged(tmp, b_sel, best, keep, out, d_num, ng, s)) != cudaSuccess) return e;
+    if ((e = cub::DeviceSelect::Flagged(tmp, b_sel2, segk, keep, keys, d_num + 1, ng, s)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(&nk, d_num, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    *n_launches += 10;
+  }
+  pb_seg_start_kernel<<<(unsigned)((n_seg + 1 + 255) / 256), 256, 0, s>>>(keys, (uint64_t)nk, n_seg, seg_offsets);
+  ++*n_launches;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  *n_out_host = (uint64_t)nk;
+  return cudaSuccess;
+}
+
+}  // namespace ppipe
