@@ -202,6 +202,118 @@ __global__ void __launch_bounds__(kPbThreads) pb_score_kernel(Problem pb, int ml
   if (lane == 0 && feas) atomicAdd(&out.counters[1], feas);
 }
 
+// K = 3, separable form. In a unit (segment, c_1, b_2) a candidate (c_2, b_1, b_3) has
+//   E = A1[b_1] + A2[c_2] + C3[c_2][b_3],   A1 = C_1 + Y_1 (depends on b_1 only),
+//   A2 = C_2 + Y_2 (c_2 only), theta = min(th1[b_1], th2[c_2], th3[c_2][b_3]),
+// so the CTA stages A1 / th1 for every b_1 sorted by A1 and, per (c_2, b_3) pair, visits
+// only the prefix of b_1 with A1 <= T - A2 - C3 (the feasible ones): the work is
+// O(pairs + feasible candidates) instead of O(candidates), with no division or global
+// load per candidate.
+__global__ void __launch_bounds__(kPbThreads) pb_score3_kernel(Problem pb, int ml, PbOut out) {
+  using Scan = cub::BlockScan<unsigned long long, kPbThreads>;
+  __shared__ unsigned long long tab[kPbBuckets];
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ int32_t sA1[256];
+  __shared__ unsigned long long sTh1[256];
+  __shared__ uint8_t sIdx1[256];
+  const DevModel md = pb.models[ml];
+  const int M = (int)md.M, C = pb.C, B = pb.B;
+  const int32_t T = md.T;
+  const int b2 = blockIdx.x % B;
+  const int c1 = 1 + (blockIdx.x / B) % (M - 2);
+  const int seg = blockIdx.x / (B * (M - 2));
+  const int k1 = seg / (C * C), k2 = (seg / C) % C, k3 = seg % C;
+  const int n_pairs = (M - 1 - c1) * B;
+  // stage A1 / th1 per b_1, then sort them by (A1, b_1) through ranks
+  __shared__ int32_t uA1[256];
+  __shared__ int32_t uC1[256];
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    uC1[b] = prow_pb(pb, md, k1, b)[c1];
+    uA1[b] = uC1[b] + yrow_pb(pb, md, k1, k2, b)[c1];
+  }
+  for (int i = threadIdx.x; i < kPbBuckets; i += blockDim.x) tab[i] = 0;
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    const int32_t a = uA1[b];
+    int rank = 0;
+    for (int q = 0; q < B; ++q) rank += (uA1[q] < a || (uA1[q] == a && q < b)) ? 1 : 0;
+    sA1[rank] = a;
+    sTh1[rank] = theta_key(stage_theta(pb.batches[b], uC1[b]));
+    sIdx1[rank] = (uint8_t)b;
+  }
+  __syncthreads();
+  const int32_t *P2 = prow_pb(pb, md, k2, b2), *Y23 = yrow_pb(pb, md, k2, k3, b2);
+  const int32_t p2c1 = P2[c1];
+  const uint32_t bv2 = pb.batches[b2];
+  const uint64_t span = (uint64_t)T + 1;
+  unsigned long long feas = 0;
+  // pass 1: best theta per E-bucket
+  for (int t = threadIdx.x; t < n_pairs; t += blockDim.x) {
+    const int b3 = t % B, c2 = c1 + 1 + t / B;
+    const int32_t C2 = P2[c2] - p2c1, A2 = C2 + Y23[c2];
+    const int32_t* P3 = prow_pb(pb, md, k3, b3);
+    const int32_t C3 = P3[M] - P3[c2];
+    const int32_t rem = T - A2 - C3;
+    if (rem < sA1[0]) continue;
+    const unsigned long long th23 =
+        min(theta_key(stage_theta(bv2, C2)), theta_key(stage_theta(pb.batches[b3], C3)));
+    for (int j = 0; j < B && sA1[j] <= rem; ++j) {
+      const int32_t E = sA1[j] + A2 + C3;
+      ++feas;
+      atomicMax(&tab[(uint64_t)E * kPbBuckets / span], min(sTh1[j], th23));
+    }
+  }
+  __syncthreads();
+  {
+    unsigned long long v[kPbBuckets / kPbThreads];
+#pragma unroll
+    for (int i = 0; i < kPbBuckets / kPbThreads; ++i) v[i] = tab[threadIdx.x * (kPbBuckets / kPbThreads) + i];
+    Scan(scan_tmp).ExclusiveScan(v, v, 0ull, cub::Max());
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kPbBuckets / kPbThreads; ++i) tab[threadIdx.x * (kPbBuckets / kPbThreads) + i] = v[i];
+  }
+  __syncthreads();
+  // pass 2: emit the candidates no smaller-E bucket beats (rare: a plain atomic per record)
+  for (int t = threadIdx.x; t < n_pairs; t += blockDim.x) {
+    const int b3 = t % B, c2 = c1 + 1 + t / B;
+    const int32_t C2 = P2[c2] - p2c1, A2 = C2 + Y23[c2];
+    const int32_t* P3 = prow_pb(pb, md, k3, b3);
+    const int32_t C3 = P3[M] - P3[c2];
+    const int32_t rem = T - A2 - C3;
+    if (rem < sA1[0]) continue;
+    const unsigned long long th23 =
+        min(theta_key(stage_theta(bv2, C2)), theta_key(stage_theta(pb.batches[b3], C3)));
+    for (int j = 0; j < B && sA1[j] <= rem; ++j) {
+      const int32_t E = sA1[j] + A2 + C3;
+      if (min(sTh1[j], th23) <= tab[(uint64_t)E * kPbBuckets / span]) continue;
+      const unsigned long long i = atomicAdd(&out.counters[0], 1ull);
+      if (i < out.cap) {
+        const int b1 = sIdx1[j];
+        ppipe_point_pb p;
+        p.model = md.model;
+        p.cut[0] = (uint16_t)c1;
+        p.cut[1] = (uint16_t)c2;
+        p.K = 3;
+        p.cls[0] = (uint8_t)k1;
+        p.cls[1] = (uint8_t)k2;
+        p.cls[2] = (uint8_t)k3;
+        p.bidx[0] = (uint8_t)b1;
+        p.bidx[1] = (uint8_t)b2;
+        p.bidx[2] = (uint8_t)b3;
+        p.reserved = 0;
+        p.e2e_us = (uint32_t)E;
+        p.stage_us[0] = (uint32_t)uC1[b1];
+        p.stage_us[1] = (uint32_t)C2;
+        p.stage_us[2] = (uint32_t)C3;
+        out.surv[i] = p;
+      }
+    }
+  }
+  for (int off = 16; off; off >>= 1) feas += __shfl_down_sync(0xffffffffu, feas, off);
+  if ((threadIdx.x & 31) == 0 && feas) atomicAdd(&out.counters[1], feas);
+}
+
 // ---------------------------------------------------------------------------
 // frontier pass over per-stage-batch survivors
 // ---------------------------------------------------------------------------
@@ -294,7 +406,7 @@ cudaError_t launch_pb_model(const Problem& pb, int ml, uint32_t M, int Kmax, con
     ++*n_launches;
   }
   if (Kmax >= 3 && M >= 3) {
-    pb_score_kernel<3><<<C * C * C * (int)(M - 2) * B, kPbThreads, 0, s>>>(pb, ml, out);
+    pb_score3_kernel<<<C * C * C * (int)(M - 2) * B, kPbThreads, 0, s>>>(pb, ml, out);
     ++*n_launches;
   }
   return cudaGetLastError();
