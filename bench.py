@@ -154,11 +154,26 @@ def run_reference(args):
                                             "sample": sample},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit_line(line)
     return 0
 
 
+_JSON_OUT = None
+
+
+def emit_line(line: dict) -> None:
+    """The one JSON line on stdout (rank 0). Everything else that reaches fd 1 -- NCCL's
+    version banner, library prints -- was redirected to stderr by main()."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -170,6 +185,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true", help="skip the SLO-sweep (frontier_at) measurement")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-f2", action="store_true", help="skip the F2 (MILP-lossless frontier) measurement")
+    ap.add_argument("--no-pb", action="store_true", help="skip the per-stage batch (App. A.1) measurement")
     ap.add_argument("--models", type=int, default=None, help="config 5 only: first N models (profiling)")
     ap.add_argument("--margin", type=int, default=None, help="override margin_permille (experiments)")
     args = ap.parse_args()
@@ -370,9 +386,9 @@ def main():
                    "(H2D of the layer profiles, two kernels, D2H of bounds and block profiles)"}
     # ---- F2, the MILP-lossless frontier, on config 4: one blocking
     # ppipe_pareto_f2 per rep (pack, enumerate, strict-dominance queries, tie runs, sort) ----
+    from workloads import CONFIG_NAMES, config4
     f2 = None
     if rank == 0 and not args.no_f2:
-        from workloads import CONFIG_NAMES, config4
         w4 = config4()
         c4 = pp.load_workload(w4, device=local_rank)
         try:
@@ -392,6 +408,31 @@ def main():
                             "the CUDA-event phases (pack, enumerate+queries, ties+sort), wall_ms = host clock"}
         finally:
             pp.free(c4)
+    # ---- per-stage batch sizes (App. A.1): every partition at its own
+    # batch, B^K times the candidates; on the block-level 18-CNN suite (config 3) and config 4 ----
+    pbm = None
+    if rank == 0 and not args.no_pb:
+        from workloads import config3
+        pbm = {}
+        for name, wk, reps in (("config 3", config3(), 5), ("config 4", config4(), 2)):
+            cx = pp.load_workload(wk, device=local_rank)
+            try:
+                pp.pareto_pb(cx, wk.kmax, wk.slo_us, wk.margin_permille, copy_to_host=False)  # warm
+                dev_ms, wall = [], []
+                for _ in range(reps):
+                    t0 = time.perf_counter()
+                    rp = pp.pareto_pb(cx, wk.kmax, wk.slo_us, wk.margin_permille, copy_to_host=False)
+                    wall.append((time.perf_counter() - t0) * 1e3)
+                    dev_ms.append(sum(cx.phase_ms()))
+                pbm[name] = {"candidates": rp.n_candidates, "feasible": rp.n_feasible, "survivors": rp.n_survivors,
+                             "points": rp.n_points, "device_ms": statistics.median(dev_ms),
+                             "wall_ms": statistics.median(wall),
+                             "candidates_per_s": rp.n_candidates / (statistics.median(wall) / 1e3),
+                             "launches": cx.launch_count()}
+            finally:
+                pp.free(cx)
+        pbm["timing"] = ("median of blocking ppipe_pareto_pb calls, inputs resident; candidates = sum_m sum_K "
+                         "C(M-1,K-1) C^K B^K, decided per (c2, b3) pair by a sorted feasible-b1 prefix")
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -429,8 +470,9 @@ def main():
         "slo_sweep": sweep,
         "prepartition": prepart,
         "f2": f2,
+        "per_stage_batch": pbm,
     }
-    print(json.dumps(line), flush=True)
+    emit_line(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -206,7 +206,8 @@ int ppipe_pareto_f2(ppipe_ctx *ctx, const ppipe_enum_params *params, int copy_to
  * staircase; among identical (E, theta) the smallest (b_1, .., b_K) (lexicographic),
  * then the smallest (c_1, c_2) stays. With one batch size this is ppipe_pareto's frontier.
  * B^K times the unified candidates: meant for block-level profiles.
- * Records carry batch INDICES per stage (bidx[d] into the batch list, 0xFF unused). */
+ * Records carry batch INDICES per stage (bidx[d] into the batch list, 0xFF unused).
+ * Virtual-GPU weights (ppipe_set_vgpu, an A.2 feature) do not apply: theta uses v = 1. */
 typedef struct {
   uint32_t model;       /* model index */
   uint16_t cut[2];      /* c_1, c_2; 0 when unused */

@@ -28,7 +28,9 @@ def main():
     ap.add_argument("--vgpu", type=str, default=None, help="comma-separated per-class virtual-GPU counts")
     ap.add_argument("--async-upload", action="store_true", help="load scaled values, then update_profiles_async")
     ap.add_argument("--f2", action="store_true", help="F2 frontier (ppipe_pareto_f2): owned models + all-gather")
+    ap.add_argument("--pb", action="store_true", help="per-stage batch sizes (ppipe_pareto_pb): owned models")
     args = ap.parse_args()
+    kind = 2 if args.f2 else (3 if args.pb else 1)
 
     import numpy as np
     import torch
@@ -64,7 +66,7 @@ def main():
         finally:
             pp.free(ctx)
     else:
-        g = pp.run(w, rank=rank, world=world, device=local, nccl_id=nid, vgpu=vgpu, frontier=2 if args.f2 else 1)
+        g = pp.run(w, rank=rank, world=world, device=local, nccl_id=nid, vgpu=vgpu, frontier=kind)
     digest = hashlib.sha256(g.points.tobytes() + g.seg_offsets.tobytes()).hexdigest()
     digests = [None] * world
     dist.all_gather_object(digests, (digest, g.n_candidates, g.n_feasible, g.n_points))
@@ -73,7 +75,7 @@ def main():
         if len(set(digests)) != 1:
             print("ranks disagree:", digests)
             ok = False
-        single = pp.run(w, device=local, vgpu=vgpu, frontier=2 if args.f2 else 1)
+        single = pp.run(w, device=local, vgpu=vgpu, frontier=kind)
         if not (np.array_equal(single.points.view(np.uint8), g.points.view(np.uint8))
                 and np.array_equal(single.seg_offsets, g.seg_offsets)
                 and single.n_candidates == g.n_candidates and single.n_feasible == g.n_feasible):
@@ -81,8 +83,8 @@ def main():
                   f"({g.n_points} vs {single.n_points} points)")
             ok = False
         if args.oracle:
-            from oracle import run_oracle
-            o = run_oracle(w, vgpu=vgpu, frontier=2 if args.f2 else 1)
+            from oracle import run_oracle, run_oracle_pb
+            o = run_oracle_pb(w) if kind == 3 else run_oracle(w, vgpu=vgpu, frontier=kind)
             if not (np.array_equal(o.points.view(np.uint8), g.points.view(np.uint8))
                     and o.n_candidates == g.n_candidates and o.n_feasible == g.n_feasible):
                 print("multi-GPU result differs from the oracle")

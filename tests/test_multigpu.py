@@ -135,7 +135,8 @@ def test_gloo_two_rank_f2_owned_models(oracle_built, cfg):
                                        (1, ["--oracle"]),  # tiny: some ranks hold no rows
                                        (3, ["--oracle", "--vgpu", "1,2,4,3", "--async-upload"]),
                                        (3, ["--oracle", "--f2"]),  # F2: owned models + all-gather
-                                       (5, ["--models", "6", "--f2"])])
+                                       (5, ["--models", "6", "--f2"]),
+                                       (3, ["--oracle", "--pb"])])  # per-stage batch sizes
 def test_nccl_two_rank_merge(cfg, extra):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
