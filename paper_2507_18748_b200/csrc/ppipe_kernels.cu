@@ -590,6 +590,18 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
     for (int c2 = c2_start + lane; c2 < c2_end; c2 += 32) bmin = min(bmin, Bs[c2]);
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) bmin = min(bmin, __shfl_xor_sync(FULL_MASK, bmin, d));
+    // Tile skip: when no slot's threshold reaches the smallest B(c2) of the range, no
+    // candidate of the tile is feasible (in pass 2: can survive) and nothing below runs.
+    // Most tiles of a deep model end here (far from the SLO); candidates were counted above.
+    int tmax = INT_MIN;
+#pragma unroll
+    for (int j = 0; j < kJ1; ++j) {
+#pragma unroll
+      for (int k1 = 0; k1 < NC; ++k1) tmax = max(tmax, thr[j][k1]);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) tmax = max(tmax, __shfl_xor_sync(FULL_MASK, tmax, d));
+    if (tmax < bmin) return;
     const long long L = (long long)bmin + 16383;
     // entries past c2_end hold n' = 0 (never pass) so that the unrolled, prefetching
     // scan below may read up to 16 values ahead
