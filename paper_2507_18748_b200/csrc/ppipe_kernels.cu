@@ -586,13 +586,10 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
   unsigned thr16[kPairs];
   unsigned long long thr64[kQ64 > 0 ? kQ64 : 1];
   {
-    int bmin = INT_MAX;
-    for (int c2 = c2_start + lane; c2 < c2_end; c2 += 32) bmin = min(bmin, Bs[c2]);
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) bmin = min(bmin, __shfl_xor_sync(FULL_MASK, bmin, d));
-    // Tile skip: when no slot's threshold reaches the smallest B(c2) of the range, no
-    // candidate of the tile is feasible (in pass 2: can survive) and nothing below runs.
-    // Most tiles of a deep model end here (far from the SLO); candidates were counted above.
+    // Tile skip and range trim: a c2 with B(c2) above every slot's threshold holds no
+    // feasible candidate (in pass 2: no survivor). If no c2 of the range is reachable the
+    // tile ends here (most tiles of a deep model: far from the SLO; candidates were
+    // counted above); otherwise the scan runs from the first to the last reachable c2.
     int tmax = INT_MIN;
 #pragma unroll
     for (int j = 0; j < kJ1; ++j) {
@@ -601,7 +598,24 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) tmax = max(tmax, __shfl_xor_sync(FULL_MASK, tmax, d));
-    if (tmax < bmin) return;
+    int bmin = INT_MAX, rlo = INT_MAX, rhi = -1;
+    for (int c2 = c2_start + lane; c2 < c2_end; c2 += 32) {
+      const int bv = Bs[c2];
+      bmin = min(bmin, bv);
+      if (bv <= tmax) {
+        rlo = min(rlo, c2);
+        rhi = c2;
+      }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      bmin = min(bmin, __shfl_xor_sync(FULL_MASK, bmin, d));
+      rlo = min(rlo, __shfl_xor_sync(FULL_MASK, rlo, d));
+      rhi = max(rhi, __shfl_xor_sync(FULL_MASK, rhi, d));
+    }
+    if (rhi < 0) return;
+    c2_start += (rlo - c2_start) & ~3;  // keep the groups aligned (c2_start = c1_base + 1 mod 4)
+    c2_end = rhi + 1;
     const long long L = (long long)bmin + 16383;
     // entries past c2_end hold n' = 0 (never pass) so that the unrolled, prefetching
     // scan below may read up to 16 values ahead
