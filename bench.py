@@ -458,7 +458,9 @@ def main():
                      "kernel": "score_kernel", "kernel_ms": kern_max,
                      "ops_per_launch": "SURVEY.md §8(d) W: 4 int32 ops per K=2,3 candidate, 2 per K=1 candidate "
                                        "(DESIGN.md §5); the prefilter decides two candidates per 32-bit lane-op "
-                                       "(16-bit fields), so frac can exceed the one-candidate-per-op model",
+                                       "(16-bit fields) and the tile skip decides whole tiles with one compare, so frac can "
+                                       "exceed the one-candidate-per-op model (issue-active from ncu: "
+                                       "profiles/r1_ncu_summary_v2.md)",
                      "frac_one_cmp_plus_3_per_feasible": min_achieved / peak_ops,
                      "peak_basis": f"{SM_COUNT} SMs x {ISSUE_LANES_PER_CLK_PER_SM} int lane-ops/clk (issue) x "
                                    f"{f_clk / 1e6:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"},
