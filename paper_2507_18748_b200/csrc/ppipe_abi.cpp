@@ -234,7 +234,7 @@ struct ppipe_ctx {
   cudaEvent_t cev[kMaxChunks + 1] = {};
   DevBuf<unsigned long long> d_err;
   // F2 (ppipe_pareto_f2)
-  DevBuf<int32_t> d_G, d_F, d_E23;
+  DevBuf<int32_t> d_G, d_F, d_E23, d_pbsd;
   DevBuf<uint16_t> d_inv;  // F2 inverse stage tables PF, PFs, SF, SFs
   DevBuf<ppipe_point> d_f2surv, d_f2tmp;
   uint64_t f2_cap = 1ull << 20;
@@ -317,6 +317,7 @@ void free_ctx(ppipe_ctx* c) {
   c->d_G.release();
   c->d_F.release();
   c->d_E23.release();
+  c->d_pbsd.release();
   c->d_inv.release();
   c->d_f2surv.release();
   c->d_f2tmp.release();
@@ -1398,10 +1399,19 @@ PPIPE_API int ppipe_pareto_pb(ppipe_ctx* c, const ppipe_enum_params* p, int copy
   if (rc != PPIPE_OK) return rc;
   const int Kmax = (int)p->max_partitions;
   const uint64_t n_cand = owned_candidates(c, own, Kmax, true);
+  // suffix-minimum rows for the K = 3 unit bound, when they fit in 2 GiB
+  uint32_t maxM = 0;
+  for (int i : own) maxM = std::max(maxM, c->h_models[i].M);
+  const size_t sd_n = (size_t)c->C * c->C * c->B * c->B * maxM;
+  int32_t* sd = nullptr;
+  if (Kmax >= 3 && sd_n > 0 && sd_n * sizeof(int32_t) <= (2ull << 30)) {
+    CU(c, c->d_pbsd.reserve(sd_n));
+    sd = c->d_pbsd.p;
+  }
   int nl = 0;
   for (;;) {
     CU(c, c->d_f2surv.reserve(c->f2_cap));
-    PbOut po{reinterpret_cast<ppipe_point_pb*>(c->d_f2surv.p), c->d_counters.p, (unsigned long long)c->d_f2surv.n};
+    PbOut po{reinterpret_cast<ppipe_point_pb*>(c->d_f2surv.p), c->d_counters.p, (unsigned long long)c->d_f2surv.n, sd};
     nl = 0;
     CU(c, cudaEventRecord(c->ev[0], c->stream));
     CU(c, launch_pack(pb, c->stream));

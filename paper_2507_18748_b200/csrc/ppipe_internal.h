@@ -121,6 +121,7 @@ struct PbOut {
   ppipe_point_pb* surv;
   unsigned long long* counters;  // [0] survivors appended, [1] feasible
   unsigned long long cap;
+  int32_t* SD;                   // K = 3 suffix-minimum rows, C * C * B * B * M (nullptr: no unit bound)
 };
 cudaError_t launch_pb_model(const Problem& pb, int local_model, uint32_t M, int Kmax, const PbOut& out,
                             cudaStream_t s, int* n_launches);

@@ -223,7 +223,8 @@ __global__ void __launch_bounds__(kPbThreads) pb_score3_kernel(Problem pb, int m
   const int c1 = 1 + (blockIdx.x / B) % (M - 2);
   const int seg = blockIdx.x / (B * (M - 2));
   const int k1 = seg / (C * C), k2 = (seg / C) % C, k3 = seg % C;
-  const int n_pairs = (M - 1 - c1) * B;
+  __shared__ uint8_t sB3[256];  // batches b_3 some pair of this unit can make feasible
+  __shared__ int nB3;
   // stage A1 / th1 per b_1, then sort them by (A1, b_1) through ranks
   __shared__ int32_t uA1[256];
   __shared__ int32_t uC1[256];
@@ -241,15 +242,32 @@ __global__ void __launch_bounds__(kPbThreads) pb_score3_kernel(Problem pb, int m
     sTh1[rank] = theta_key(stage_theta(pb.batches[b], uC1[b]));
     sIdx1[rank] = (uint8_t)b;
   }
+  if (threadIdx.x == 0) nB3 = 0;
   __syncthreads();
   const int32_t *P2 = prow_pb(pb, md, k2, b2), *Y23 = yrow_pb(pb, md, k2, k3, b2);
   const int32_t p2c1 = P2[c1];
+  // Unit bound: E >= min A1 - P2[c1] + P3_{b3}[M] + min_{c2 > c1} (P2[c2] + Y23[c2] - P3_{b3}[c2]),
+  // the last term from the suffix-minimum rows SD (when the context built them). A b_3
+  // whose bound exceeds T_eff has no feasible pair; most units of a deep model have none.
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    bool keep = true;
+    if (out.SD) {
+      const int32_t* P3 = prow_pb(pb, md, k3, b);
+      const int64_t bound = (int64_t)sA1[0] - p2c1 + P3[M] +
+                            out.SD[((((size_t)k2 * C + k3) * B + b2) * B + b) * M + c1 + 1];
+      keep = bound <= T;
+    }
+    if (keep) sB3[atomicAdd(&nB3, 1)] = (uint8_t)b;
+  }
+  __syncthreads();
+  const int nb3 = nB3;
+  const int n_pairs = (M - 1 - c1) * nb3;
   const uint32_t bv2 = pb.batches[b2];
   const uint64_t span = (uint64_t)T + 1;
   unsigned long long feas = 0;
   // pass 1: best theta per E-bucket
   for (int t = threadIdx.x; t < n_pairs; t += blockDim.x) {
-    const int b3 = t % B, c2 = c1 + 1 + t / B;
+    const int b3 = sB3[t % nb3], c2 = c1 + 1 + t / nb3;
     const int32_t C2 = P2[c2] - p2c1, A2 = C2 + Y23[c2];
     const int32_t* P3 = prow_pb(pb, md, k3, b3);
     const int32_t C3 = P3[M] - P3[c2];
@@ -276,7 +294,7 @@ __global__ void __launch_bounds__(kPbThreads) pb_score3_kernel(Problem pb, int m
   __syncthreads();
   // pass 2: emit the candidates no smaller-E bucket beats (rare: a plain atomic per record)
   for (int t = threadIdx.x; t < n_pairs; t += blockDim.x) {
-    const int b3 = t % B, c2 = c1 + 1 + t / B;
+    const int b3 = sB3[t % nb3], c2 = c1 + 1 + t / nb3;
     const int32_t C2 = P2[c2] - p2c1, A2 = C2 + Y23[c2];
     const int32_t* P3 = prow_pb(pb, md, k3, b3);
     const int32_t C3 = P3[M] - P3[c2];
@@ -396,6 +414,24 @@ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 }  // namespace
 
+// SD[k2][k3][b2][b3][c] = min_{c <= c' <= M - 1} (P_{k2,b2}[c'] + Y_{k2->k3,b2}[c'] - P_{k3,b3}[c'])
+// for c in [1, M - 1]: one thread per (class pair, batch pair) row, a reverse running minimum.
+__global__ void __launch_bounds__(kPbThreads) pb_sd_kernel(Problem pb, int ml, int32_t* SD) {
+  const DevModel md = pb.models[ml];
+  const int M = (int)md.M, C = pb.C, B = pb.B;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= C * C * B * B) return;
+  const int b3 = r % B, b2 = (r / B) % B, k3 = (r / (B * B)) % C, k2 = r / (B * B * C);
+  const int32_t *P2 = prow_pb(pb, md, k2, b2), *Y23 = yrow_pb(pb, md, k2, k3, b2), *P3 = prow_pb(pb, md, k3, b3);
+  int32_t* row = SD + (size_t)r * M;
+  int32_t m = INT32_MAX;
+  for (int c = M - 1; c >= 1; --c) {
+    m = min(m, P2[c] + Y23[c] - P3[c]);
+    row[c] = m;
+  }
+  row[0] = m;
+}
+
 cudaError_t launch_pb_model(const Problem& pb, int ml, uint32_t M, int Kmax, const PbOut& out, cudaStream_t s,
                             int* n_launches) {
   const int C = pb.C, B = pb.B;
@@ -406,6 +442,10 @@ cudaError_t launch_pb_model(const Problem& pb, int ml, uint32_t M, int Kmax, con
     ++*n_launches;
   }
   if (Kmax >= 3 && M >= 3) {
+    if (out.SD) {
+      pb_sd_kernel<<<(C * C * B * B + kPbThreads - 1) / kPbThreads, kPbThreads, 0, s>>>(pb, ml, out.SD);
+      ++*n_launches;
+    }
     pb_score3_kernel<<<C * C * C * (int)(M - 2) * B, kPbThreads, 0, s>>>(pb, ml, out);
     ++*n_launches;
   }
