@@ -1336,7 +1336,7 @@ PPIPE_API int ppipe_pareto_f2(ppipe_ctx* c, const ppipe_enum_params* p, int copy
   for (int i : own) g_cap = std::max(g_cap, f2_g3_elems_per_segment((int)c->B, c->h_models[i].M));
   if (Kmax >= 3) CU(c, c->d_G.reserve(std::max<size_t>(g_cap, 1)));
   if (Kmax >= 2) CU(c, c->d_F.reserve(f_need));
-  if (Kmax >= 3) CU(c, c->d_E23.reserve(f_need));
+  if (Kmax >= 3) CU(c, c->d_E23.reserve(2 * f_need));
   const size_t inv_n = f_need / c->C * ((c->B + 3) & ~3u);  // C * B * 4 ceil(B / 4) * max M
   if (Kmax >= 2) CU(c, c->d_inv.reserve(4 * inv_n));
   const int q3_grid = f2_q3_grid(c->device);

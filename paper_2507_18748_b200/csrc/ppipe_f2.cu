@@ -310,12 +310,14 @@ __global__ void __launch_bounds__(kF2Threads, 4) f2_q3_kernel(Problem pb, int ml
     const int32_t *P1 = prow(pb, md, k1, bi), *P2 = prow(pb, md, k2, bi), *P3 = prow(pb, md, k3, bi);
     const int32_t *Y12 = yrow(pb, md, k1, k2, bi), *Y23 = yrow(pb, md, k2, k3, bi);
     const int32_t* E23 = out.E23 + ((size_t)(k2 * C + k3) * B + bi) * M;
+    const int32_t* E23min = E23 + (size_t)C * C * B * M;
     const int32_t P3M = P3[M];
     const uint32_t b = pb.batches[bi];
     const int32_t* Gseg = G + (size_t)segc * B * n * g_pitch(n);
     const int c1_lo = 1 + kQ3Rows * (int)(unit % nq), c1_hi = min(c1_lo + kQ3Rows - 1, M - 2);
     for (int c1 = c1_lo; c1 <= c1_hi; ++c1) {
     const int32_t C1 = P1[c1], p2c1 = P2[c1], a = C1 - p2c1 + Y12[c1];
+    if (a + E23min[c1 + 1] > T) continue;  // no feasible c_2 in this row (warp-uniform)
     int cnt = 0;
     for (int base = c1 + 1; base <= M - 1 || cnt > 0; base += 32) {
       if (base <= M - 1) {
@@ -370,6 +372,17 @@ __global__ void __launch_bounds__(kF2Threads) f2_e23_kernel(Problem pb, int ml, 
   const int32_t P3M = P3[M];
   int32_t* row = E23 + (size_t)blockIdx.x * M;
   for (int c = threadIdx.x; c < M; c += blockDim.x) row[c] = P2[c] + (P3M - P3[c]) + Y23[c];
+  __syncthreads();
+  // suffix minimum over c_2 in [c, M - 1] (E23min, at E23 + C*C*B*M): a row (c_1) with
+  // a(c_1) + E23min[c_1 + 1] > T_eff has no feasible c_2 and is skipped whole
+  if (threadIdx.x == 0) {
+    int32_t* mrow = E23 + (size_t)C * C * B * M + (size_t)blockIdx.x * M;
+    int32_t m = INT32_MAX;
+    for (int c = M - 1; c >= 0; --c) {
+      m = min(m, row[c]);
+      mrow[c] = m;
+    }
+  }
 }
 
 // K = 2: per (segment, b') prefix counts F[c] = #feasible c'_1 in [1, c], c = 0..M-1.

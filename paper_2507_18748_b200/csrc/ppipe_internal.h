@@ -75,7 +75,7 @@ struct F2Out {
   size_t g_cap;                  // >= f2_g3_elems_per_segment(B, M) for every model
   int32_t* F;                    // K = 2 prefix counts, >= C * C * B * M elements
   uint16_t *PF, *PFs, *SF, *SFs;  // inverse stage tables, >= C * B * 4 ceil(B / 4) * M elements each
-  int32_t* E23;                   // K = 3 second-cut part of E, >= C * C * B * M elements
+  int32_t* E23;                   // K = 3 second-cut part of E and its suffix minimum, 2 * C * C * B * M
   int q3_grid;                    // persistent K = 3 query CTAs
 };
 constexpr uint32_t kF2MaxLayers = 4096;  // a G row (M - 2 values) is staged in shared memory
