@@ -33,7 +33,7 @@ def test_async_upload_replaces_the_loaded_values(oracle_built):
 
 
 def test_async_upload_chunks_config5_slice():
-    w = config5(n_models=24)  # 8 chunks of 3 models
+    w = config5(n_models=24)  # 4 chunks of 6 models
     ref = pp.run(w)
     ctx = pp.load_profiles(_scaled(w, 3), [m.act_bytes for m in w.models], w.n_classes, w.batches, w.bw)
     try:
