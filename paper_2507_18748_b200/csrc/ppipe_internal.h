@@ -58,7 +58,7 @@ struct ScoreOut {
   ppipe_point* surv;
   unsigned long long* counters;  // [0] survivors, [1] feasible, [2] candidates, [3] hot units, [4] pass-2 progress
   unsigned long long cap;
-  uint4* hot;                    // [hot_cap] (local model, k2, k3, batch index) of units with feasible candidates
+  uint4* hot;                    // [hot_cap] (local model, k2 | k3 << 4 | b << 8, tile mask lo, hi) of hot units
   uint64_t* hot_tab;             // [hot_cap][table words] their finalized fold tables
   unsigned long long hot_cap;
 };

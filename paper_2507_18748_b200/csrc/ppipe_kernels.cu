@@ -1040,6 +1040,7 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ int s_tile;
   __shared__ unsigned long long s_slot;
+  __shared__ unsigned long long s_tmask;  // tiles (t < 64) of this unit with a feasible candidate
   const int nb = 1 << nb_log2;
   const ScoreSmem sm = carve_smem<NC>(smem_raw, nb, row_len);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1059,7 +1060,10 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
 #pragma unroll 1
     for (int k3 = 0; k3 < NC; ++k3) {
       stage_rows(cx, sm, k3, r.c2_from, r.c2_to, k3 == 0);
-      if (tid == 0) s_tile = 0;
+      if (tid == 0) {
+        s_tile = 0;
+        s_tmask = r.ntiles > 64 ? ~0ull : 0ull;  // more tiles than mask bits: pass 2 visits all
+      }
       __syncthreads();
       const unsigned long long feas0 = feas;
 #pragma unroll 1
@@ -1068,13 +1072,19 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
         if (lane == 0) t = atomicAdd(&s_tile, 1);
         t = __shfl_sync(FULL_MASK, t, 0);
         if (t >= r.ntiles) break;
+        const unsigned long long ft = feas;
         k3_tile<NC, 1, W>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin,
                        SlotData{}, sm.nb16 + warp * row_len, out, em, feas, cand);
+        if (__any_sync(FULL_MASK, feas != ft) && lane == 0 && t < 64) atomicOr(&s_tmask, 1ull << t);
       }
       if (__syncthreads_or(feas != feas0) && !(pb.debug_flags & 2)) {
         if (tid == 0) {
           s_slot = atomicAdd(&out.counters[3], 1ull);
-          if (s_slot < out.hot_cap) out.hot[s_slot] = make_uint4(ml, k2, k3, bi);
+          // (local model, k2 | k3 << 4 | b << 8, tile mask): pass 2 skips the tiles without a
+          // feasible candidate (it only emits feasible ones)
+          if (s_slot < out.hot_cap)
+            out.hot[s_slot] = make_uint4(ml, (unsigned)k2 | ((unsigned)k3 << 4) | ((unsigned)bi << 8),
+                                         (unsigned)s_tmask, (unsigned)(s_tmask >> 32));
         }
         __syncthreads();
         if (s_slot < out.hot_cap)  // finalized tables straight to the unit's global slot
@@ -1112,7 +1122,8 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
     const unsigned long long u = s_unit;
     if (u >= n_hot) break;
     const uint4 hu = out.hot[u];
-    const int ml = (int)hu.x, k2 = (int)hu.y, k3 = (int)hu.z, bi = (int)hu.w;
+    const int ml = (int)hu.x, k2 = (int)(hu.y & 15u), k3 = (int)((hu.y >> 4) & 15u), bi = (int)(hu.y >> 8);
+    const unsigned long long tmask = ((unsigned long long)hu.w << 32) | hu.z;
     const DevModel md = pb.models[ml];
     CtaCtx<NC> cx;
     make_ctx<NC, W>(cx, pb, md, k2, bi, nb);
@@ -1133,6 +1144,7 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
       if (lane == 0) t = atomicAdd(&s_tile, 1);
       t = __shfl_sync(FULL_MASK, t, 0);
       if (t >= r.ntiles) break;
+      if (t < 64 && !((tmask >> t) & 1ull)) continue;  // no feasible candidate in pass 1
       k3_tile<NC, 2, W>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin,
                      carve_slot<NC>(sm.slot + warp * slot_bytes<NC>()), sm.nb16 + warp * row_len, out, em, feas, cand, Bmin);
     }
