@@ -237,7 +237,7 @@ struct ppipe_ctx {
   cudaEvent_t cev[kMaxChunks + 1] = {};
   DevBuf<unsigned long long> d_err;
   // F2 (ppipe_pareto_f2)
-  DevBuf<int32_t> d_G, d_F, d_E23, d_pbsd;
+  DevBuf<int32_t> d_G, d_F, d_E23, d_pbsd, d_minA;
   DevBuf<uint16_t> d_inv;  // F2 inverse stage tables PF, PFs, SF, SFs
   DevBuf<ppipe_point> d_f2surv, d_f2tmp;
   uint64_t f2_cap = 1ull << 20;
@@ -321,6 +321,7 @@ void free_ctx(ppipe_ctx* c) {
   c->d_F.release();
   c->d_E23.release();
   c->d_pbsd.release();
+  c->d_minA.release();
   c->d_inv.release();
   c->d_f2surv.release();
   c->d_f2tmp.release();
@@ -839,9 +840,17 @@ static int setup_problem(ppipe_ctx* c, Problem* out) {
   }
   pb.model_base = 0;
   pb.n_chunk = pb.n_local;
+  // per-tile minimum of A for the K = 3 early tile skip (ppipe_kernels.cu tile_mina_kernel)
+  pb.max_tiles = (int)((c->max_M + 32 * kJ1 - 1) / (32 * kJ1)) + 1;
+  const size_t mina_n = (size_t)std::max<size_t>(c->local.size(), 1) * c->C * c->B * pb.max_tiles;
+  CU(c, c->d_minA.reserve(mina_n));
+  pb.minA = c->d_minA.p;
   *out = pb;
   return PPIPE_OK;
 }
+
+// kernels launch_pack issues (pack_p, pack_y, and tile_mina for K = 3)
+static int pack_launches(const Problem& pb) { return pb.n_chunk ? (pb.Kmax >= 3 && pb.minA ? 3 : 2) : 0; }
 
 static int run_enumerate(ppipe_ctx* c) {
   CU(c, cudaSetDevice(c->device));
@@ -895,7 +904,7 @@ static int run_enumerate(ppipe_ctx* c) {
                             (uint64_t)INT64_MAX / (8 * bmax), c->d_err.p, c->stream));
       CU(c, launch_pack(pb, c->stream));
       CU(c, launch_score_part(pb, so, c->stream, &c->launches_i, 1));
-      c->launches_i += 3;
+      c->launches_i += 1 + pack_launches(pb);
     }
     CU(c, cudaEventRecord(c->ev[1], c->stream));  // phase 0 = upload + pack + score3a, interleaved
     pb.model_base = 0;
@@ -908,7 +917,7 @@ static int run_enumerate(ppipe_ctx* c) {
   }
   CU(c, cudaEventRecord(c->ev[0], c->stream));
   CU(c, launch_pack(pb, c->stream));
-  c->launches_i += pb.n_local ? 2 : 0;
+  c->launches_i += pack_launches(pb);
   CU(c, cudaEventRecord(c->ev[1], c->stream));
   CU(c, cudaMemsetAsync(c->d_counters.p, 0, 16 * sizeof(unsigned long long), c->stream));
   CU(c, launch_score(pb, so, c->stream, &c->launches_i));
@@ -1352,7 +1361,7 @@ PPIPE_API int ppipe_pareto_f2(ppipe_ctx* c, const ppipe_enum_params* p, int copy
     nl = 0;
     CU(c, cudaEventRecord(c->ev[0], c->stream));
     CU(c, launch_pack(pb, c->stream));
-    nl += pb.n_local ? 2 : 0;
+    nl += pack_launches(pb);
     CU(c, cudaEventRecord(c->ev[1], c->stream));
     CU(c, cudaMemsetAsync(c->d_counters.p, 0, 16 * sizeof(unsigned long long), c->stream));
     for (int i : own) CU(c, launch_f2_model(pb, i, c->h_models[i].M, Kmax, fo, c->stream, &nl));
@@ -1418,7 +1427,7 @@ PPIPE_API int ppipe_pareto_pb(ppipe_ctx* c, const ppipe_enum_params* p, int copy
     nl = 0;
     CU(c, cudaEventRecord(c->ev[0], c->stream));
     CU(c, launch_pack(pb, c->stream));
-    nl += pb.n_local ? 2 : 0;
+    nl += pack_launches(pb);
     CU(c, cudaEventRecord(c->ev[1], c->stream));
     CU(c, cudaMemsetAsync(c->d_counters.p, 0, 16 * sizeof(unsigned long long), c->stream));
     for (int i : own) CU(c, launch_pb_model(pb, i, c->h_models[i].M, Kmax, po, c->stream, &nl));

@@ -52,6 +52,10 @@ struct Problem {
   uint32_t wpack;
   int w_bits;                 // bits of max_k w_k (widens the fold keys' Cmax)
   int debug_flags;            // timing experiments only (PPIPE_DEBUG_FLAGS); 0 in production
+  // per (local model, k2, batch, K = 3 tile): min over the tile's first cuts and k1 of
+  // A = C_1 + Y_1 - P[k2][c_1] (written by the pack launch; nullptr = not kept)
+  int32_t* minA;
+  int max_tiles;
 };
 
 struct ScoreOut {

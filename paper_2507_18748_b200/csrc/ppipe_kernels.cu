@@ -125,6 +125,13 @@ __global__ void __launch_bounds__(256) pack_y_kernel(Problem pb) {
   }
 }
 
+__device__ __forceinline__ void tile_mina_body(const Problem& pb);
+
+// CTA per (local model, batch), all k2 at once: for every K = 3 tile of 32 * kJ1 first
+// cuts, the minimum over its valid c_1 and every k_1 of A(c_1, k_1) = C_1 + Y_1 - P[k2][c_1]. Then
+// T_eff - minA is the loosest threshold of the tile, known before any slot is loaded.
+__global__ void __launch_bounds__(128) tile_mina_kernel(Problem pb) { tile_mina_body(pb); }
+
 cudaError_t launch_pack(const Problem& pb, cudaStream_t s) {
   if (pb.n_chunk == 0) return cudaSuccess;
   const int n_btiles = (pb.B + kPackBT - 1) / kPackBT;
@@ -132,6 +139,11 @@ cudaError_t launch_pack(const Problem& pb, cudaStream_t s) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   pack_y_kernel<<<pb.n_chunk * pb.V * pb.B, 256, 0, s>>>(pb);
+  if (pb.minA && pb.Kmax >= 3) {
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    tile_mina_kernel<<<pb.n_chunk * pb.B, 32 * kJ1, 0, s>>>(pb);
+  }
   return cudaGetLastError();
 }
 
@@ -477,9 +489,27 @@ template <int NC, int pass, bool W>
 __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, int c1_hi,
                         const int32_t* Bs, const int32_t* Qs, const int32_t* Rs, uint32_t* raw, const uint2* fin,
                         const SlotData& sd, uint32_t* nb16, const ScoreOut& out, Emitter& em,
-                        unsigned long long& feas, unsigned long long& cand, int Bmin = 0) {
+                        unsigned long long& feas, unsigned long long& cand, int Bmin = 0,
+                        int tmax_hint = INT_MAX) {
   const int lane = threadIdx.x & 31;
   const int nb = cx.nb;
+  if (pass == 1 && tmax_hint != INT_MAX) {
+    // Early tile skip: T_eff - minA (the loosest threshold of the tile, from the pack
+    // launch) below every B(c2) of the range => no feasible candidate; count and leave
+    // before loading any slot.
+    int bmin = INT_MAX;
+    for (int c2 = c1_base + 1 + lane; c2 < cx.M; c2 += 32) bmin = min(bmin, Bs[c2]);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) bmin = min(bmin, __shfl_xor_sync(FULL_MASK, bmin, d));
+    if (tmax_hint < bmin) {
+#pragma unroll
+      for (int j = 0; j < kJ1; ++j) {
+        const int c1 = c1_base + 32 * j + lane;
+        if (c1 >= c1_lo && c1 <= c1_hi) cand += (unsigned long long)(cx.M - 1 - c1) * NC;
+      }
+      return;
+    }
+  }
   // virtual-GPU weights: compile-time 1 unless the context set some (W)
   const uint32_t wp = W ? cx.wpack : 0x11111111u;
   const int w2 = W ? cx.w2 : 1;
@@ -918,6 +948,45 @@ __device__ __forceinline__ K3Range k3_range(const DevModel& md) {
   return r;
 }
 
+__device__ __forceinline__ void tile_mina_body(const Problem& pb) {
+  const int bi = blockIdx.x % pb.B;
+  const int ml = pb.model_base + blockIdx.x / pb.B;
+  const DevModel md = pb.models[ml];
+  const K3Range r = k3_range(md);
+  if (r.empty) return;
+  const int C = pb.C;
+  __shared__ int wmin[4][kMaxClasses];
+  const int32_t* Pm = pb.P + md.p_off;
+  const int32_t* Ym = pb.Y + md.y_off;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = 0; t < r.ntiles; ++t) {
+    const int c1 = r.c1_base0 + t * 32 * kJ1 + (int)threadIdx.x;
+    const bool valid = c1 >= r.c1lo && c1 <= r.c1hi;
+    int P[kMaxClasses];
+#pragma unroll
+    for (int k = 0; k < kMaxClasses; ++k) P[k] = (k < C && valid) ? Pm[((size_t)k * pb.B + bi) * md.Mp + c1] : 0;
+#pragma unroll
+    for (int k2 = 0; k2 < kMaxClasses; ++k2) {
+      if (k2 >= C) break;
+      int m = INT_MAX;
+      if (valid)
+        for (int k1 = 0; k1 < C; ++k1) {
+          const int y = Ym[((size_t)pb.pair_v[k1 * C + k2] * pb.B + bi) * md.Mp + c1];
+          m = min(m, P[k1] + y - P[k2]);
+        }
+      for (int d = 16; d > 0; d >>= 1) m = min(m, __shfl_xor_sync(FULL_MASK, m, d));
+      if (lane == 0) wmin[warp][k2] = m;
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < C) {
+      const int k2 = threadIdx.x;
+      pb.minA[((size_t)(ml * C + k2) * pb.B + bi) * pb.max_tiles + t] =
+          min(min(wmin[0][k2], wmin[1][k2]), min(wmin[2][k2], wmin[3][k2]));
+    }
+    __syncthreads();
+  }
+}
+
 __device__ __forceinline__ void flush_counters(const ScoreOut& out, unsigned long long feas, unsigned long long cand) {
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {
@@ -1073,8 +1142,10 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
         t = __shfl_sync(FULL_MASK, t, 0);
         if (t >= r.ntiles) break;
         const unsigned long long ft = feas;
+        const int hint = pb.minA ? cx.T - __ldg(pb.minA + ((size_t)(ml * NC + k2) * pb.B + bi) * pb.max_tiles + t)
+                                 : INT_MAX;
         k3_tile<NC, 1, W>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin,
-                       SlotData{}, sm.nb16 + warp * row_len, out, em, feas, cand);
+                       SlotData{}, sm.nb16 + warp * row_len, out, em, feas, cand, 0, hint);
         if (__any_sync(FULL_MASK, feas != ft) && lane == 0 && t < 64) atomicOr(&s_tmask, 1ull << t);
       }
       if (__syncthreads_or(feas != feas0) && !(pb.debug_flags & 2)) {
