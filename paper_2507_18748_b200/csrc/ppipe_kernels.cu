@@ -1387,6 +1387,20 @@ struct PickBetter {  // associative and commutative: "the better of two" under a
   }
 };
 
+// The same choice over record indices: ReduceByKey moves 4-byte indices instead of
+// 32-byte records (CUB may also apply the operator to the unused slots of a partial
+// tile, so an index is clamped to the array).
+struct PickBetterIdx {
+  const ppipe_point* r;
+  uint32_t n;
+  uint32_t wpack;
+  __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const {
+    a = min(a, n - 1);
+    b = min(b, n - 1);
+    return better(r[b], r[a], wpack) ? b : a;
+  }
+};
+
 struct Theta {
   uint32_t b, c;  // theta = b / c
 };
@@ -1433,8 +1447,8 @@ cudaError_t frontier_pass(const ppipe_point* in, uint64_t n, const uint64_t* seg
   e = cub::DeviceRadixSort::SortPairs(nullptr, b_sort, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
                                       (uint32_t*)nullptr, ni, 0, end_bit, s);
   if (e != cudaSuccess) return e;
-  e = cub::DeviceReduce::ReduceByKey(nullptr, b_red, (uint64_t*)nullptr, (uint64_t*)nullptr, (ppipe_point*)nullptr,
-                                     (ppipe_point*)nullptr, (int64_t*)nullptr, PickBetter{wpack}, ni, s);
+  e = cub::DeviceReduce::ReduceByKey(nullptr, b_red, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
+                                     (uint32_t*)nullptr, (int64_t*)nullptr, PickBetterIdx{nullptr, 1, wpack}, ni, s);
   if (e != cudaSuccess) return e;
   e = cub::DeviceScan::ExclusiveScanByKey(nullptr, b_scan, (uint64_t*)nullptr, (Theta*)nullptr, (Theta*)nullptr,
                                           MaxTheta(), Theta{0, 1}, ni, cub::Equality(), s);
@@ -1455,7 +1469,7 @@ cudaError_t frontier_pass(const ppipe_point* in, uint64_t n, const uint64_t* seg
     return o;
   };
   const size_t o_k1 = take(nn * 8), o_k2 = take(nn * 8), o_v1 = take(nn * 4), o_v2 = take(nn * 4);
-  const size_t o_rec = take(nn * 32), o_best = take(nn * 32), o_gk = take(nn * 8), o_sk = take(nn * 8);
+  const size_t o_best = take(nn * 32), o_gk = take(nn * 8), o_sk = take(nn * 8);
   const size_t o_th = take(nn * 8), o_pre = take(nn * 8), o_keep = take(nn), o_num = take(16);
   const size_t o_tmp = take(tmpb);
   if (scratch->bytes < off) {
@@ -1471,7 +1485,6 @@ cudaError_t frontier_pass(const ppipe_point* in, uint64_t n, const uint64_t* seg
   uint64_t* keys2 = (uint64_t*)(base + o_k2);
   uint32_t* vals = (uint32_t*)(base + o_v1);
   uint32_t* vals2 = (uint32_t*)(base + o_v2);
-  ppipe_point* rec = (ppipe_point*)(base + o_rec);
   ppipe_point* best = (ppipe_point*)(base + o_best);
   uint64_t* gkeys = (uint64_t*)(base + o_gk);
   uint64_t* segk = (uint64_t*)(base + o_sk);
@@ -1487,14 +1500,16 @@ cudaError_t frontier_pass(const ppipe_point* in, uint64_t n, const uint64_t* seg
     make_keys_kernel<<<blocks, 256, 0, s>>>(in, n, seg_base_by_model, C, keys, vals);
     e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, keys, keys2, vals, vals2, ni, 0, end_bit, s);
     if (e != cudaSuccess) return e;
-    gather_kernel<<<blocks, 256, 0, s>>>(in, vals2, n, rec);
-    e = cub::DeviceReduce::ReduceByKey(tmp, b_red, keys2, gkeys, rec, best, d_num, PickBetter{wpack}, ni, s);
+    // best record per (segment, E): reduce the sorted record indices, then gather the winners
+    e = cub::DeviceReduce::ReduceByKey(tmp, b_red, keys2, gkeys, vals2, vals, d_num,
+                                       PickBetterIdx{in, (uint32_t)n, wpack}, ni, s);
     if (e != cudaSuccess) return e;
     e = cudaMemcpyAsync(&ng, d_num, 8, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return e;
     e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return e;
     const int gb = (int)std::min<int64_t>((ng + 255) / 256, 148 * 16);
+    gather_kernel<<<gb, 256, 0, s>>>(in, vals, (uint64_t)ng, best);
     group_theta_kernel<<<gb, 256, 0, s>>>(gkeys, best, (uint64_t)ng, segk, th, wpack);
     e = cub::DeviceScan::ExclusiveScanByKey(tmp, b_scan, segk, th, pre, MaxTheta(), Theta{0, 1}, ng,
                                             cub::Equality(), s);
