@@ -460,11 +460,11 @@ def main():
                                        "(DESIGN.md §5); the prefilter decides two candidates per 32-bit lane-op "
                                        "(16-bit fields) and the tile skip decides whole tiles with one compare, so frac can "
                                        "exceed the one-candidate-per-op model (issue-active from ncu: "
-                                       "profiles/r1_ncu_summary_v3.md)",
+                                       "profiles/r1_ncu_summary_v4.md)",
                      "frac_one_cmp_plus_3_per_feasible": min_achieved / peak_ops,
                      "issue_active_ncu": {"score3a": 0.534, "score3b": 0.374, "score12": 0.606,
                                           "source": "smsp__issue_active from ncu --set full of this build "
-                                                    "(profiles/r1_ncu_summary_v3.md); the measured issue side "
+                                                    "(profiles/r1_ncu_summary_v4.md); the measured issue side "
                                                     "of the integer-issue roofline"},
                      "peak_basis": f"{SM_COUNT} SMs x {ISSUE_LANES_PER_CLK_PER_SM} int lane-ops/clk (issue) x "
                                    f"{f_clk / 1e6:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"},
