@@ -1229,6 +1229,33 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
 // rounded down to a power of two (128..2048 buckets).
 constexpr size_t kSmemBudget = 32 * 1024;  // sized for the pass-2 kernel (7 CTAs per SM)
 
+#ifndef PPIPE_CONCURRENT_12
+#define PPIPE_CONCURRENT_12 0
+#endif
+#if PPIPE_CONCURRENT_12
+// One non-blocking side stream (and its fork/join events) per device, created on
+// first use and kept for the process lifetime.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static SideStream& side_stream() {
+  static SideStream per_dev[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SideStream& ss = per_dev[dev & 63];
+  if (ss.s == nullptr) {
+    if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
+      ss.s = nullptr;
+      cudaGetLastError();
+    }
+  }
+  return ss;
+}
+#endif
+
 template <int NC, bool W>
 static cudaError_t launch_score_w(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches,
                                   int part) {
@@ -1261,6 +1288,22 @@ static cudaError_t launch_score_w(const Problem& pb, const ScoreOut& out, cudaSt
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     const int ctas = std::max(1, std::min(k3bCtasPerSm, smem_sm / (int)(smem + 1024)));  // persistent: fill the SMs
+#if PPIPE_CONCURRENT_12
+    // score12 does not read what score3b writes (both only append survivors through
+    // atomics), so it runs on a side stream and fills the SMs score3b's persistent
+    // CTAs release at its tail; the join keeps the stream order for the frontier pass.
+    SideStream& ss = side_stream();
+    if (ss.s != nullptr) {
+      cudaEventRecord(ss.fork, s);
+      cudaStreamWaitEvent(ss.s, ss.fork, 0);
+      score3b_kernel<NC, W><<<n_sm * ctas, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
+      score12_kernel<NC, W><<<(unsigned)pb.n_local * NC * pb.B, 32 * kWarps, smem12, ss.s>>>(pb, out, nb12_log2);
+      cudaEventRecord(ss.join, ss.s);
+      cudaStreamWaitEvent(s, ss.join, 0);
+      *n_launches += 2;
+      return cudaGetLastError();
+    }
+#endif
     score3b_kernel<NC, W><<<n_sm * ctas, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
     ++*n_launches;
   }
