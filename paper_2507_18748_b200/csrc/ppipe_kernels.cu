@@ -1232,14 +1232,13 @@ constexpr size_t kSmemBudget = 32 * 1024;  // sized for the pass-2 kernel (7 CTA
 #ifndef PPIPE_CONCURRENT_12
 #define PPIPE_CONCURRENT_12 0
 #endif
-#if PPIPE_CONCURRENT_12
 // One non-blocking side stream (and its fork/join events) per device, created on
 // first use and kept for the process lifetime.
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
 };
-static SideStream& side_stream() {
+[[maybe_unused]] static SideStream& side_stream() {
   static SideStream per_dev[64];
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1254,7 +1253,6 @@ static SideStream& side_stream() {
   }
   return ss;
 }
-#endif
 
 template <int NC, bool W>
 static cudaError_t launch_score_w(const Problem& pb, const ScoreOut& out, cudaStream_t s, int* n_launches,
@@ -1277,38 +1275,54 @@ static cudaError_t launch_score_w(const Problem& pb, const ScoreOut& out, cudaSt
   e = cudaFuncSetAttribute(score3b_kernel<NC, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   // part 0: everything; 1: score3a over the chunk; 2: score3b + score12 over all local models
-  if (pb.Kmax >= 3 && part != 2 && pb.n_chunk > 0) {
+  const bool k3a = pb.Kmax >= 3 && part != 2 && pb.n_chunk > 0;
+  // score12 reads none of what score3a / score3b write (all three only append
+  // survivors and counts through atomics), so with PPIPE_CONCURRENT_12 it runs on a
+  // side stream: mode 1 forks after score3a (score12 fills the SMs score3b's
+  // persistent CTAs release at its tail), mode 2 before it (score12's latency-bound
+  // CTAs share the SMs with score3a's ALU-bound ones). The join restores the stream
+  // order for the frontier pass.
+  SideStream* ss = nullptr;
+#if PPIPE_CONCURRENT_12
+  if (part != 1) {
+    ss = &side_stream();
+    if (ss->s == nullptr) ss = nullptr;
+  }
+#endif
+  const bool early = ss != nullptr && PPIPE_CONCURRENT_12 == 2;
+  const cudaStream_t s12 = ss != nullptr ? ss->s : s;
+  if (early) {
+    cudaEventRecord(ss->fork, s);
+    cudaStreamWaitEvent(s12, ss->fork, 0);
+    score12_kernel<NC, W><<<(unsigned)pb.n_local * NC * pb.B, 32 * kWarps, smem12, s12>>>(pb, out, nb12_log2);
+    ++*n_launches;
+  }
+  if (k3a) {
     score3a_kernel<NC, W><<<grid, 32 * kWarps, smem_a, s>>>(pb, out, nb_log2, row_len);
     ++*n_launches;
   }
   if (part == 1) return cudaGetLastError();
+  if (ss != nullptr && !early) {
+    cudaEventRecord(ss->fork, s);
+    cudaStreamWaitEvent(s12, ss->fork, 0);
+  }
   if (pb.Kmax >= 3) {
     int dev = 0, n_sm = 148, smem_sm = 227 * 1024;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     const int ctas = std::max(1, std::min(k3bCtasPerSm, smem_sm / (int)(smem + 1024)));  // persistent: fill the SMs
-#if PPIPE_CONCURRENT_12
-    // score12 does not read what score3b writes (both only append survivors through
-    // atomics), so it runs on a side stream and fills the SMs score3b's persistent
-    // CTAs release at its tail; the join keeps the stream order for the frontier pass.
-    SideStream& ss = side_stream();
-    if (ss.s != nullptr) {
-      cudaEventRecord(ss.fork, s);
-      cudaStreamWaitEvent(ss.s, ss.fork, 0);
-      score3b_kernel<NC, W><<<n_sm * ctas, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
-      score12_kernel<NC, W><<<(unsigned)pb.n_local * NC * pb.B, 32 * kWarps, smem12, ss.s>>>(pb, out, nb12_log2);
-      cudaEventRecord(ss.join, ss.s);
-      cudaStreamWaitEvent(s, ss.join, 0);
-      *n_launches += 2;
-      return cudaGetLastError();
-    }
-#endif
     score3b_kernel<NC, W><<<n_sm * ctas, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
     ++*n_launches;
   }
-  score12_kernel<NC, W><<<(unsigned)pb.n_local * NC * pb.B, 32 * kWarps, smem12, s>>>(pb, out, nb12_log2);
-  ++*n_launches;
+  if (!early) {
+    score12_kernel<NC, W><<<(unsigned)pb.n_local * NC * pb.B, 32 * kWarps, smem12, s12>>>(pb, out, nb12_log2);
+    ++*n_launches;
+  }
+  if (ss != nullptr) {
+    cudaEventRecord(ss->join, s12);
+    cudaStreamWaitEvent(s, ss->join, 0);
+  }
   return cudaGetLastError();
 }
 
