@@ -135,9 +135,11 @@ def _u32p(a):
 class Context:
     """Owns a ppipe_ctx* plus the host arrays it was built from."""
 
-    def __init__(self, handle, n_models):
+    def __init__(self, handle, n_models, n_classes=None, n_batches=None):
         self.handle = handle
         self.n_models = n_models
+        self.n_classes = n_classes
+        self.n_batches = n_batches
 
     @property
     def stream(self) -> int:
@@ -177,7 +179,7 @@ def _models_array(lat_us, act_bytes, n_classes=None, n_batches=None):
 
 
 def update_profiles(ctx: Context, lat_us: Sequence[np.ndarray], act_bytes: Sequence[np.ndarray]) -> None:
-    models, keep = _models_array(lat_us, act_bytes)
+    models, keep = _models_array(lat_us, act_bytes, ctx.n_classes, ctx.n_batches)
     _check(lib().ppipe_update_profiles(ctx.handle, len(lat_us), models), ctx.handle)
     del keep
 
@@ -186,7 +188,7 @@ def update_profiles_async(ctx: Context, lat_us: Sequence[np.ndarray], act_bytes:
     """include/ppipe.h ppipe_update_profiles_async: the next enumerate() uploads the
     values in chunks overlapped with scoring. The arrays must stay alive and unchanged
     until the next pareto() returns (the context keeps references until then)."""
-    models, keep = _models_array(lat_us, act_bytes)
+    models, keep = _models_array(lat_us, act_bytes, ctx.n_classes, ctx.n_batches)
     _check(lib().ppipe_update_profiles_async(ctx.handle, len(lat_us), models), ctx.handle)
     ctx._pending = keep  # keep the buffers alive for the deferred copy
 
@@ -204,7 +206,7 @@ def load_profiles(lat_us: Sequence[np.ndarray], act_bytes: Sequence[np.ndarray],
     rc = lib().ppipe_load_profiles(ct.byref(h), n, models, n_classes, len(b), _u32p(b), _u32p(bw), ct.byref(dist))
     _check(rc, None)
     del keep
-    return Context(h, n)
+    return Context(h, n, int(n_classes), len(b))
 
 
 def load_workload(w, rank: int = 0, world: int = 1, device: int = -1, nccl_id: Optional[bytes] = None) -> Context:

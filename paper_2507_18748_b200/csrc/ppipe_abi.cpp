@@ -870,7 +870,14 @@ static int run_enumerate(ppipe_ctx* c) {
   c->launches_i = 0;
   pb.model_base = 0;
   pb.n_chunk = pb.n_local;
-  if (c->pending_upload && pb.n_local == 0) c->pending_upload = false;  // nothing of it lives on this rank
+  if (c->pending_upload && pb.n_local == 0) {
+    // nothing of it lives on this rank; still take part in ppipe_pareto's error all-gather
+    // (every rank issues the same collectives)
+    c->pending_upload = false;
+    CU(c, c->d_err.reserve(1));
+    CU(c, cudaMemsetAsync(c->d_err.p, 0xff, 8, c->stream));
+    c->check_err = true;
+  }
   if (c->pending_upload) {
     // Chunked pipeline: the copy stream uploads chunk i + 1 while the compute stream
     // validates, packs and scores (score3a) chunk i; score3b / score12 follow once.

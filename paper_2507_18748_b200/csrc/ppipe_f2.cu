@@ -26,9 +26,9 @@
 //
 // Bound: the G tables are written once and read by the queries (HBM / L2); the
 // enumeration itself is the same integer work as score3a. DESIGN.md §5.
-#include <cub/cub.cuh>
 #include <climits>
 
+#include "ppipe_block.cuh"
 #include "ppipe_internal.h"
 
 namespace ppipe {
@@ -387,8 +387,7 @@ __global__ void __launch_bounds__(kF2Threads) f2_e23_kernel(Problem pb, int ml, 
 
 // K = 2: per (segment, b') prefix counts F[c] = #feasible c'_1 in [1, c], c = 0..M-1.
 __global__ void __launch_bounds__(kF2Threads) f2_g2_kernel(Problem pb, int ml, int32_t* F) {
-  using Scan = cub::BlockScan<int32_t, kF2Threads>;
-  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int32_t scan_sh[kF2Threads / 32];
   __shared__ int32_t carry;
   const DevModel md = pb.models[ml];
   const int M = (int)md.M, C = pb.C, B = pb.B;
@@ -406,7 +405,7 @@ __global__ void __launch_bounds__(kF2Threads) f2_g2_kernel(Problem pb, int ml, i
     const int c = c0 + threadIdx.x;
     const int32_t f = (c <= M - 1 && P1[c] + (P2M - P2[c]) + Y12[c] <= T) ? 1 : 0;
     int32_t inc, tot;
-    Scan(tmp).InclusiveSum(f, inc, tot);
+    inc = block_inclusive_scan<kF2Threads>(f, 0, OpSum(), &tot, scan_sh);
     if (c <= M - 1) Fs[c] = carry + inc;
     __syncthreads();
     if (threadIdx.x == 0) carry += tot;
@@ -557,206 +556,4 @@ cudaError_t launch_f2_model(const Problem& pb, int ml, uint32_t M, int Kmax, con
 // ---------------------------------------------------------------------------
 // finalize: equal-vector runs, canonical order, CSR
 // ---------------------------------------------------------------------------
-namespace {
-
-struct K128 {
-  uint64_t hi, lo;
-  __host__ __device__ bool operator==(const K128& o) const { return hi == o.hi && lo == o.lo; }
-};
-
-__device__ __forceinline__ uint64_t seg_of(const ppipe_point& p, const uint64_t* seg_base, int C) {
-  uint64_t off = 0, pw = 1;
-  for (int k = 1; k < p.K; ++k) {
-    pw *= (uint64_t)C;
-    off += pw;
-  }
-  uint64_t idx = 0;
-  for (int d = 0; d < p.K; ++d) idx = idx * C + p.cls[d];
-  return seg_base[p.model] + off + idx;
-}
-
-__device__ __forceinline__ uint32_t gcd32(uint32_t a, uint32_t b) {
-  while (b) {
-    const uint32_t t = a % b;
-    a = b;
-    b = t;
-  }
-  return a;
-}
-
-// Equal-vector key: (segment, b/g, C_1/g, C_2/g, C_3/g), g = gcd(b, C_1..C_K) >= 1:
-// x_p == x_q  <=>  (b, C) proportional  <=>  equal reduced tuples. Bits 28|16|28|28|28.
-__global__ void f2_tie_keys_kernel(const ppipe_point* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t* hi,
-                                   uint64_t* lo, uint32_t* idx) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const ppipe_point p = in[i];
-    uint32_t g = p.batch;
-    for (int d = 0; d < p.K; ++d) g = gcd32(g, p.stage_us[d]);
-    const uint64_t c1 = p.stage_us[0] / g, c2 = p.stage_us[1] / g, c3 = p.stage_us[2] / g;
-    hi[i] = (seg_of(p, seg_base, C) << 36) | ((uint64_t)(p.batch / g) << 20) | (c1 >> 8);
-    lo[i] = ((c1 & 0xFF) << 56) | (c2 << 28) | c3;
-    idx[i] = (uint32_t)i;
-  }
-}
-
-// Canonical output key: (segment) then (b, c_1, c_2).
-__global__ void f2_out_keys_kernel(const ppipe_point* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t* hi,
-                                   uint64_t* lo, uint32_t* idx) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const ppipe_point p = in[i];
-    hi[i] = seg_of(p, seg_base, C);
-    lo[i] = ((uint64_t)p.batch << 32) | ((uint64_t)p.cut[0] << 16) | p.cut[1];
-    idx[i] = (uint32_t)i;
-  }
-}
-
-__global__ void gather_u64_kernel(const uint64_t* src, const uint32_t* idx, uint64_t n, uint64_t* dst) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    dst[i] = src[idx[i]];
-}
-
-__global__ void make_k128_kernel(const uint64_t* hi, const uint64_t* lo_src, const uint32_t* idx, uint64_t n,
-                                 K128* out) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    out[i] = K128{hi[i], lo_src[idx[i]]};
-}
-
-__global__ void gather_pts_kernel(const ppipe_point* in, const uint32_t* idx, uint64_t n, ppipe_point* out) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    out[i] = in[idx[i]];
-}
-
-// Canonical key in one word: segment << 40 | b << 24 | c_1 << 12 | c_2 (M <= 4096).
-__global__ void f2_out_key64_kernel(const ppipe_point* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t* key,
-                                    uint32_t* idx) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const ppipe_point p = in[i];
-    key[i] = (seg_of(p, seg_base, C) << 40) | ((uint64_t)p.batch << 24) | ((uint64_t)p.cut[0] << 12) | p.cut[1];
-    idx[i] = (uint32_t)i;
-  }
-}
-
-// Output records: gathered into canonical order, the tie flag cleared.
-__global__ void gather_final_kernel(const ppipe_point* in, const uint32_t* idx, uint64_t n, ppipe_point* out) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    ppipe_point p = in[idx[i]];
-    p.reserved = 0;
-    out[i] = p;
-  }
-}
-
-struct TieFlag {
-  uint16_t want;
-  __device__ __forceinline__ bool operator()(const ppipe_point& p) const { return p.reserved == want; }
-};
-
-// Of two records with the same vector: the smaller (E, b, c_1, c_2).
-struct PickMinE {
-  const ppipe_point* r;
-  __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const {
-    const ppipe_point &p = r[a], &q = r[b];
-    if (p.e2e_us != q.e2e_us) return p.e2e_us < q.e2e_us ? a : b;
-    if (p.batch != q.batch) return p.batch < q.batch ? a : b;
-    if (p.cut[0] != q.cut[0]) return p.cut[0] < q.cut[0] ? a : b;
-    return p.cut[1] <= q.cut[1] ? a : b;
-  }
-};
-
-inline int grid_for(uint64_t n) { return (int)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 8)); }
-
-inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
-
-}  // namespace
-
-cudaError_t f2_finalize(const ppipe_point* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t n_seg,
-                        ppipe_point* out, ppipe_point* tmp_pts, uint64_t* seg_offsets, uint64_t* seg_tmp,
-                        uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches) {
-  cudaError_t e;
-  if (n == 0) {
-    *n_out_host = 0;
-    return segment_offsets(out, 0, seg_base, C, n_seg, seg_offsets, seg_tmp, s, n_launches);
-  }
-  const int ni = (int)n;
-  // scratch: hi, lo, k2, k3 (u64 x n), idx, idx2, agg (u32 x n), keys, ukeys (K128 x n), counters, cub temp
-  size_t b_sort = 0, b_red = 0, b_sel = 0;
-  e = cub::DeviceRadixSort::SortPairs(nullptr, b_sort, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
-                                      (uint32_t*)nullptr, ni, 0, 64, s);
-  if (e != cudaSuccess) return e;
-  e = cub::DeviceReduce::ReduceByKey(nullptr, b_red, (K128*)nullptr, (K128*)nullptr, (uint32_t*)nullptr,
-                                     (uint32_t*)nullptr, (uint64_t*)nullptr, PickMinE{nullptr}, ni, s);
-  if (e != cudaSuccess) return e;
-  e = cub::DeviceSelect::If(nullptr, b_sel, (const ppipe_point*)nullptr, (ppipe_point*)nullptr, (uint64_t*)nullptr,
-                            ni, TieFlag{0}, s);
-  if (e != cudaSuccess) return e;
-  const size_t o_hi = 0, o_lo = o_hi + align_up(8 * n), o_k2 = o_lo + align_up(8 * n), o_k3 = o_k2 + align_up(8 * n),
-               o_idx = o_k3 + align_up(8 * n), o_idx2 = o_idx + align_up(4 * n), o_agg = o_idx2 + align_up(4 * n),
-               o_keys = o_agg + align_up(4 * n), o_ukeys = o_keys + align_up(16 * n),
-               o_cnt = o_ukeys + align_up(16 * n), o_tmp = o_cnt + 256,
-               total = o_tmp + align_up(std::max(std::max(b_sort, b_red), b_sel));
-  if (scratch->bytes < total) {
-    if (scratch->buf) cudaFree(scratch->buf);
-    scratch->buf = nullptr;
-    scratch->bytes = 0;
-    if ((e = cudaMalloc(&scratch->buf, total)) != cudaSuccess) return e;
-    scratch->bytes = total;
-  }
-  char* base = (char*)scratch->buf;
-  uint64_t *hi = (uint64_t*)(base + o_hi), *lo = (uint64_t*)(base + o_lo), *k2 = (uint64_t*)(base + o_k2),
-           *k3 = (uint64_t*)(base + o_k3);
-  uint32_t *idx = (uint32_t*)(base + o_idx), *idx2 = (uint32_t*)(base + o_idx2), *agg = (uint32_t*)(base + o_agg);
-  K128 *keys = (K128*)(base + o_keys), *ukeys = (K128*)(base + o_ukeys);
-  uint64_t* cnt = (uint64_t*)(base + o_cnt);
-  void* tmp = base + o_tmp;
-
-  // 1) survivors no other candidate can equal (flag 0) go straight to tmp_pts[0, nu);
-  //    the few that might have an identical vector (flag 1) to out[0, nf)
-  if ((e = cub::DeviceSelect::If(tmp, b_sel, in, tmp_pts, cnt, ni, TieFlag{0}, s)) != cudaSuccess) return e;
-  if ((e = cub::DeviceSelect::If(tmp, b_sel, in, out, cnt + 1, ni, TieFlag{1}, s)) != cudaSuccess) return e;
-  uint64_t hc[3] = {0, 0, 0};
-  if ((e = cudaMemcpyAsync(hc, cnt, 16, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-  const uint64_t nu = hc[0], nf = hc[1];
-  *n_launches += 2;
-  // 2) flagged: sort by the equal-vector key (lo, then hi: LSD radix sort is stable) and
-  //    keep the best record of each run, appended at tmp_pts[nu, nu + nw)
-  uint64_t nw = 0;
-  if (nf) {
-    const int nfi = (int)nf, g = grid_for(nf);
-    f2_tie_keys_kernel<<<g, 256, 0, s>>>(out, nf, seg_base, C, hi, lo, idx);
-    if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, lo, k2, idx, idx2, nfi, 0, 64, s)) != cudaSuccess) return e;
-    gather_u64_kernel<<<g, 256, 0, s>>>(hi, idx2, nf, k3);
-    if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, k3, k2, idx2, idx, nfi, 0, 64, s)) != cudaSuccess) return e;
-    make_k128_kernel<<<g, 256, 0, s>>>(k2, lo, idx, nf, keys);
-    if ((e = cub::DeviceReduce::ReduceByKey(tmp, b_red, keys, ukeys, idx, agg, cnt + 2, PickMinE{out}, nfi, s)) !=
-        cudaSuccess)
-      return e;
-    if ((e = cudaMemcpyAsync(&nw, cnt + 2, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-    gather_pts_kernel<<<grid_for(nw), 256, 0, s>>>(out, agg, nw, tmp_pts + nu);
-    *n_launches += 11;
-  }
-  // 3) canonical order (segment, b, c_1, c_2): one radix sort over the key bits in use
-  const uint64_t nr = nu + nw;
-  const int nri = (int)nr, g = grid_for(nr);
-  int seg_bits = 1;
-  while (seg_bits < 64 && (1ull << seg_bits) < n_seg) ++seg_bits;
-  if (seg_bits + 40 <= 64) {
-    f2_out_key64_kernel<<<g, 256, 0, s>>>(tmp_pts, nr, seg_base, C, lo, idx);
-    if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, lo, k2, idx, idx2, nri, 0, 40 + seg_bits, s)) != cudaSuccess)
-      return e;
-    gather_final_kernel<<<g, 256, 0, s>>>(tmp_pts, idx2, nr, out);
-    *n_launches += 3;
-  } else {
-    f2_out_keys_kernel<<<g, 256, 0, s>>>(tmp_pts, nr, seg_base, C, hi, lo, idx);
-    if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, lo, k2, idx, idx2, nri, 0, 64, s)) != cudaSuccess) return e;
-    gather_u64_kernel<<<g, 256, 0, s>>>(hi, idx2, nr, k3);
-    if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, k3, k2, idx2, idx, nri, 0, 64, s)) != cudaSuccess) return e;
-    gather_final_kernel<<<g, 256, 0, s>>>(tmp_pts, idx, nr, out);
-    *n_launches += 5;
-  }
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  *n_out_host = nr;
-  return segment_offsets(out, nr, seg_base, C, n_seg, seg_offsets, seg_tmp, s, n_launches);
-}
-
 }  // namespace ppipe

@@ -17,7 +17,7 @@
 //             over theta = b / Cmax compared as exact rationals, compaction.
 //
 // DESIGN.md §5 gives the roofline and algorithmic op counts of each kernel.
-#include <cub/cub.cuh>
+#include <algorithm>
 #include <climits>
 
 #include "ppipe_internal.h"
@@ -78,13 +78,15 @@ __global__ void __launch_bounds__(256) pack_p_kernel(Problem pb, int n_btiles) {
     __syncthreads();
     for (int e = threadIdx.x; e < kPackLT * kPackBT; e += blockDim.x) {
       const int l = e / kPackBT, bb = e % kPackBT;
-      tile[l][bb] = (l < nl && bb < nb) ? (int32_t)lat[(size_t)(l0 + l) * B + b0 + bb] : 0;
+      // values are read as unsigned and clamped: unvalidated uploads (ppipe_update_profiles_async
+      // validates on the device, the error surfaces in ppipe_pareto) never make a prefix negative
+      tile[l][bb] = (l < nl && bb < nb) ? (int32_t)min(lat[(size_t)(l0 + l) * B + b0 + bb], (uint32_t)kRangeLimit) : 0;
     }
     __syncthreads();
     if (threadIdx.x < nb) {
       int32_t acc = carry[threadIdx.x];
       for (int l = 0; l < nl; ++l) {
-        acc += tile[l][threadIdx.x];
+        acc = min(acc + tile[l][threadIdx.x], kRangeLimit);  // saturating (exact for valid inputs: totals < 2^28)
         tile[l][threadIdx.x] = acc;
       }
       carry[threadIdx.x] = acc;
@@ -1375,26 +1377,6 @@ cudaError_t launch_score(const Problem& pb, const ScoreOut& out, cudaStream_t s,
 // ---------------------------------------------------------------------------
 // frontier pass
 // ---------------------------------------------------------------------------
-constexpr int kEBits = 28;
-
-__global__ void make_keys_kernel(const ppipe_point* in, uint64_t n, const uint64_t* seg_base, int C,
-                                 uint64_t* keys, uint32_t* vals) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const ppipe_point p = in[i];
-    // segment offset within the model: sum_{K' < K} C^K'
-    uint64_t off = 0, pw = 1;
-    for (int k = 1; k < p.K; ++k) {
-      pw *= (uint64_t)C;
-      off += pw;
-    }
-    uint64_t idx = 0;
-    for (int d = 0; d < p.K; ++d) idx = idx * C + p.cls[d];
-    const uint64_t seg = seg_base[p.model] + off + idx;
-    keys[i] = (seg << kEBits) | (uint64_t)p.e2e_us;
-    vals[i] = (uint32_t)i;
-  }
-}
-
 __global__ void seg_start_kernel(const uint64_t* keys, uint64_t n, uint64_t n_seg, uint64_t* start) {
   const uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (s > n_seg) return;
@@ -1405,190 +1387,6 @@ __global__ void seg_start_kernel(const uint64_t* keys, uint64_t n, uint64_t n_se
     else hi = mid;
   }
   start[s] = lo;
-}
-
-// Weighted bottleneck max_d w_{k_d} C_d (virtual GPUs; w = 1 by default). < 2^32.
-__device__ __forceinline__ uint32_t cmax_of(const ppipe_point& p, uint32_t wpack) {
-  if (wpack == 0x11111111u) {  // no virtual GPUs (uniform branch)
-    uint32_t m = p.stage_us[0];
-    if (p.K >= 2) m = max(m, p.stage_us[1]);
-    if (p.K >= 3) m = max(m, p.stage_us[2]);
-    return m;
-  }
-  uint32_t m = (uint32_t)wt(wpack, p.cls[0]) * p.stage_us[0];
-  if (p.K >= 2) m = max(m, (uint32_t)wt(wpack, p.cls[1]) * p.stage_us[1]);
-  if (p.K >= 3) m = max(m, (uint32_t)wt(wpack, p.cls[2]) * p.stage_us[2]);
-  return m;
-}
-
-// theta_p > theta_q  <=>  b_p * Cmax_q > b_q * Cmax_p (exact; Cmax = 0 reads as +inf)
-__device__ __forceinline__ bool theta_gt(uint64_t bp, uint64_t cp, uint64_t bq, uint64_t cq) {
-  return bp * cq > bq * cp;
-}
-
-// Is p canonically better than q among records with the same (segment, E)?
-// theta desc, then batch asc, then (c_1, c_2) asc: a strict total order on candidates.
-__device__ __forceinline__ bool better(const ppipe_point& p, const ppipe_point& q, uint32_t wpack) {
-  const uint64_t cp = cmax_of(p, wpack), cq = cmax_of(q, wpack);
-  if (theta_gt(p.batch, cp, q.batch, cq)) return true;
-  if (theta_gt(q.batch, cq, p.batch, cp)) return false;
-  if (p.batch != q.batch) return p.batch < q.batch;
-  if (p.cut[0] != q.cut[0]) return p.cut[0] < q.cut[0];
-  return p.cut[1] < q.cut[1];
-}
-
-struct PickBetter {  // associative and commutative: "the better of two" under a total order
-  uint32_t wpack;
-  __device__ __forceinline__ ppipe_point operator()(const ppipe_point& a, const ppipe_point& b) const {
-    return better(b, a, wpack) ? b : a;
-  }
-};
-
-// The same choice over record indices: ReduceByKey moves 4-byte indices instead of
-// 32-byte records (CUB may also apply the operator to the unused slots of a partial
-// tile, so an index is clamped to the array).
-struct PickBetterIdx {
-  const ppipe_point* r;
-  uint32_t n;
-  uint32_t wpack;
-  __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const {
-    a = min(a, n - 1);
-    b = min(b, n - 1);
-    return better(r[b], r[a], wpack) ? b : a;
-  }
-};
-
-struct Theta {
-  uint32_t b, c;  // theta = b / c
-};
-
-struct MaxTheta {
-  __device__ __forceinline__ Theta operator()(const Theta& x, const Theta& y) const {
-    return theta_gt(y.b, y.c, x.b, x.c) ? y : x;
-  }
-};
-
-__global__ void gather_kernel(const ppipe_point* in, const uint32_t* idx, uint64_t n, ppipe_point* out) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    out[i] = in[idx[i]];
-}
-
-__global__ void group_theta_kernel(const uint64_t* gkeys, const ppipe_point* best, uint64_t ng, uint64_t* segk,
-                                   Theta* th, uint32_t wpack) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ng; i += (uint64_t)gridDim.x * blockDim.x) {
-    segk[i] = gkeys[i] >> kEBits;
-    th[i] = Theta{best[i].batch, cmax_of(best[i], wpack)};
-  }
-}
-
-__global__ void keep_kernel(const Theta* th, const Theta* prefix, uint64_t ng, uint8_t* keep) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ng; i += (uint64_t)gridDim.x * blockDim.x)
-    keep[i] = theta_gt(th[i].b, th[i].c, prefix[i].b, prefix[i].c) ? 1 : 0;  // strictly above every earlier E
-}
-
-static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-
-// Frontier of n records: sort by (segment, E); best record per (segment, E) by
-// (theta desc, b asc, cuts asc) [reduce-by-key]; keep it iff its theta strictly
-// exceeds the max theta of every smaller E in its segment [exclusive max-scan by
-// segment]; compact; CSR offsets by binary search. All stages are data-parallel.
-cudaError_t frontier_pass(const ppipe_point* in, uint64_t n, const uint64_t* seg_base_by_model, int C,
-                          uint64_t n_seg, ppipe_point* out, uint64_t* seg_offsets, uint64_t* n_out_host,
-                          FrontierScratch* scratch, cudaStream_t s, int* n_launches, uint32_t wpack) {
-  int seg_bits = 1;
-  while ((1ull << seg_bits) <= n_seg) ++seg_bits;
-  const int end_bit = kEBits + seg_bits;
-  const int64_t ni = (int64_t)n;
-  size_t b_sort = 0, b_red = 0, b_scan = 0, b_sel = 0;
-  cudaError_t e;
-  e = cub::DeviceRadixSort::SortPairs(nullptr, b_sort, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
-                                      (uint32_t*)nullptr, ni, 0, end_bit, s);
-  if (e != cudaSuccess) return e;
-  e = cub::DeviceReduce::ReduceByKey(nullptr, b_red, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
-                                     (uint32_t*)nullptr, (int64_t*)nullptr, PickBetterIdx{nullptr, 1, wpack}, ni, s);
-  if (e != cudaSuccess) return e;
-  e = cub::DeviceScan::ExclusiveScanByKey(nullptr, b_scan, (uint64_t*)nullptr, (Theta*)nullptr, (Theta*)nullptr,
-                                          MaxTheta(), Theta{0, 1}, ni, cub::Equality(), s);
-  if (e != cudaSuccess) return e;
-  e = cub::DeviceSelect::Flagged(nullptr, b_sel, (ppipe_point*)nullptr, (uint8_t*)nullptr, (ppipe_point*)nullptr,
-                                 (int64_t*)nullptr, ni, s);
-  if (e != cudaSuccess) return e;
-  size_t b_sel2 = 0;
-  e = cub::DeviceSelect::Flagged(nullptr, b_sel2, (uint64_t*)nullptr, (uint8_t*)nullptr, (uint64_t*)nullptr,
-                                 (int64_t*)nullptr, ni, s);
-  if (e != cudaSuccess) return e;
-  const size_t tmpb = std::max(std::max(b_sort, b_red), std::max(b_scan, std::max(b_sel, b_sel2)));
-  const size_t nn = n > 0 ? n : 1;
-  size_t off = 0;
-  auto take = [&](size_t bytes) {
-    const size_t o = off;
-    off = align_up(off + bytes, 256);
-    return o;
-  };
-  const size_t o_k1 = take(nn * 8), o_k2 = take(nn * 8), o_v1 = take(nn * 4), o_v2 = take(nn * 4);
-  const size_t o_best = take(nn * 32), o_gk = take(nn * 8), o_sk = take(nn * 8);
-  const size_t o_th = take(nn * 8), o_pre = take(nn * 8), o_keep = take(nn), o_num = take(16);
-  const size_t o_tmp = take(tmpb);
-  if (scratch->bytes < off) {
-    if (scratch->buf) cudaFree(scratch->buf);
-    scratch->buf = nullptr;
-    scratch->bytes = 0;
-    e = cudaMalloc(&scratch->buf, off);
-    if (e != cudaSuccess) return e;
-    scratch->bytes = off;
-  }
-  char* base = (char*)scratch->buf;
-  uint64_t* keys = (uint64_t*)(base + o_k1);
-  uint64_t* keys2 = (uint64_t*)(base + o_k2);
-  uint32_t* vals = (uint32_t*)(base + o_v1);
-  uint32_t* vals2 = (uint32_t*)(base + o_v2);
-  ppipe_point* best = (ppipe_point*)(base + o_best);
-  uint64_t* gkeys = (uint64_t*)(base + o_gk);
-  uint64_t* segk = (uint64_t*)(base + o_sk);
-  Theta* th = (Theta*)(base + o_th);
-  Theta* pre = (Theta*)(base + o_pre);
-  uint8_t* keep = (uint8_t*)(base + o_keep);
-  int64_t* d_num = (int64_t*)(base + o_num);
-  void* tmp = base + o_tmp;
-
-  int64_t ng = 0, nk = 0;
-  if (n > 0) {
-    const int blocks = (int)std::min<uint64_t>((n + 255) / 256, 148 * 16);
-    make_keys_kernel<<<blocks, 256, 0, s>>>(in, n, seg_base_by_model, C, keys, vals);
-    e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, keys, keys2, vals, vals2, ni, 0, end_bit, s);
-    if (e != cudaSuccess) return e;
-    // best record per (segment, E): reduce the sorted record indices, then gather the winners
-    e = cub::DeviceReduce::ReduceByKey(tmp, b_red, keys2, gkeys, vals2, vals, d_num,
-                                       PickBetterIdx{in, (uint32_t)n, wpack}, ni, s);
-    if (e != cudaSuccess) return e;
-    e = cudaMemcpyAsync(&ng, d_num, 8, cudaMemcpyDeviceToHost, s);
-    if (e != cudaSuccess) return e;
-    e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return e;
-    const int gb = (int)std::min<int64_t>((ng + 255) / 256, 148 * 16);
-    gather_kernel<<<gb, 256, 0, s>>>(in, vals, (uint64_t)ng, best);
-    group_theta_kernel<<<gb, 256, 0, s>>>(gkeys, best, (uint64_t)ng, segk, th, wpack);
-    e = cub::DeviceScan::ExclusiveScanByKey(tmp, b_scan, segk, th, pre, MaxTheta(), Theta{0, 1}, ng,
-                                            cub::Equality(), s);
-    if (e != cudaSuccess) return e;
-    keep_kernel<<<gb, 256, 0, s>>>(th, pre, (uint64_t)ng, keep);
-    e = cub::DeviceSelect::Flagged(tmp, b_sel, best, keep, out, d_num, ng, s);
-    if (e != cudaSuccess) return e;
-    e = cub::DeviceSelect::Flagged(tmp, b_sel2, segk, keep, keys, d_num + 1, ng, s);  // segment of each kept point
-    if (e != cudaSuccess) return e;
-    e = cudaMemcpyAsync(&nk, d_num, 8, cudaMemcpyDeviceToHost, s);
-    if (e != cudaSuccess) return e;
-    *n_launches += 12;
-  }
-  const unsigned sb = (unsigned)((n_seg + 1 + 255) / 256);
-  seg_start_kernel<<<sb, 256, 0, s>>>(keys, (uint64_t)nk, n_seg, seg_offsets);
-  ++*n_launches;
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return e;
-  *n_out_host = (uint64_t)nk;
-  return cudaSuccess;
 }
 
 __global__ void seg_of_kernel(const ppipe_point* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t* seg) {
@@ -1615,82 +1413,6 @@ cudaError_t segment_offsets(const ppipe_point* pts, uint64_t n, const uint64_t* 
   }
   seg_start_kernel<<<(unsigned)((n_seg + 1 + 255) / 256), 256, 0, s>>>(seg_tmp, n, n_seg, seg_offsets);
   ++*n_launches;
-  return cudaGetLastError();
-}
-
-// Per segment: how many of its (E-ascending) points satisfy E <= T_new[model].
-__global__ void trunc_count_kernel(const ppipe_point* in, const uint64_t* off, uint64_t n_seg, const uint32_t* T_new,
-                                   uint64_t* cnt) {
-  const uint64_t sg = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (sg > n_seg) return;
-  if (sg == n_seg) {
-    cnt[sg] = 0;
-    return;
-  }
-  uint64_t lo = off[sg], hi = off[sg + 1];
-  if (lo == hi) {
-    cnt[sg] = 0;
-    return;
-  }
-  const uint32_t T = T_new[in[lo].model];
-  const uint64_t base = lo;
-  while (lo < hi) {  // first point with E > T
-    const uint64_t mid = (lo + hi) >> 1;
-    if (in[mid].e2e_us <= T) lo = mid + 1;
-    else hi = mid;
-  }
-  cnt[sg] = lo - base;
-}
-
-struct KeepBelowT {
-  const uint32_t* T_new;
-  __device__ bool operator()(const ppipe_point& p) const { return p.e2e_us <= T_new[p.model]; }
-};
-
-cudaError_t truncate_frontier(const ppipe_point* in, const uint64_t* seg_offsets_in, uint64_t n_in, uint64_t n_seg,
-                              const uint32_t* T_new, ppipe_point* out, uint64_t* seg_offsets_out,
-                              uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches) {
-  const int64_t ns = (int64_t)n_seg + 1, ni = (int64_t)n_in;
-  size_t b_scan = 0, b_sel = 0;
-  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, b_scan, (uint64_t*)nullptr, (uint64_t*)nullptr, ns, s);
-  if (e != cudaSuccess) return e;
-  e = cub::DeviceSelect::If(nullptr, b_sel, (const ppipe_point*)nullptr, (ppipe_point*)nullptr, (int64_t*)nullptr,
-                            ni, KeepBelowT{T_new}, s);
-  if (e != cudaSuccess) return e;
-  size_t off = 0;
-  auto take = [&](size_t bytes) {
-    const size_t o = off;
-    off = align_up(off + bytes, 256);
-    return o;
-  };
-  const size_t o_cnt = take(8 * (size_t)ns), o_num = take(16), o_tmp = take(std::max(b_scan, b_sel));
-  if (scratch->bytes < off) {
-    if (scratch->buf) cudaFree(scratch->buf);
-    scratch->buf = nullptr;
-    scratch->bytes = 0;
-    e = cudaMalloc(&scratch->buf, off);
-    if (e != cudaSuccess) return e;
-    scratch->bytes = off;
-  }
-  char* base = (char*)scratch->buf;
-  uint64_t* cnt = (uint64_t*)(base + o_cnt);
-  int64_t* d_num = (int64_t*)(base + o_num);
-  void* tmp = base + o_tmp;
-  trunc_count_kernel<<<(unsigned)((ns + 255) / 256), 256, 0, s>>>(in, seg_offsets_in, n_seg, T_new, cnt);
-  e = cub::DeviceScan::ExclusiveSum(tmp, b_scan, cnt, seg_offsets_out, ns, s);
-  if (e != cudaSuccess) return e;
-  int64_t nk = 0;
-  if (n_in > 0) {
-    e = cub::DeviceSelect::If(tmp, b_sel, in, out, d_num, ni, KeepBelowT{T_new}, s);
-    if (e != cudaSuccess) return e;
-    e = cudaMemcpyAsync(&nk, d_num, 8, cudaMemcpyDeviceToHost, s);
-    if (e != cudaSuccess) return e;
-    ++*n_launches;
-  }
-  *n_launches += 2;
-  e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return e;
-  *n_out_host = (uint64_t)nk;
   return cudaGetLastError();
 }
 

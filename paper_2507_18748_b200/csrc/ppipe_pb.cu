@@ -20,9 +20,9 @@
 // so the drop is exact and the survivors' frontier is the unit's. pb_frontier_pass
 // reduces all survivors: sort by (segment, E), best per (segment, E), strict
 // staircase over theta, CSR.
-#include <cub/cub.cuh>
 #include <climits>
 
+#include "ppipe_block.cuh"
 #include "ppipe_internal.h"
 
 namespace ppipe {
@@ -102,9 +102,8 @@ __device__ __forceinline__ unsigned long long pb_key(const Problem& pb, const Pb
 
 template <int K>
 __global__ void __launch_bounds__(kPbThreads) pb_score_kernel(Problem pb, int ml, PbOut out) {
-  using Scan = cub::BlockScan<unsigned long long, kPbThreads>;
   __shared__ unsigned long long tab[kPbBuckets];
-  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ unsigned long long scan_sh[kPbThreads / 32];
   const DevModel md = pb.models[ml];
   const int M = (int)md.M, C = pb.C, B = pb.B;
   const int32_t T = md.T;
@@ -152,7 +151,18 @@ __global__ void __launch_bounds__(kPbThreads) pb_score_kernel(Problem pb, int ml
     unsigned long long v[kPbBuckets / kPbThreads];
 #pragma unroll
     for (int i = 0; i < kPbBuckets / kPbThreads; ++i) v[i] = tab[threadIdx.x * (kPbBuckets / kPbThreads) + i];
-    Scan(scan_tmp).ExclusiveScan(v, v, 0ull, cub::Max());
+    {  // exclusive prefix maximum over the blocked arrangement
+      unsigned long long agg = 0ull;
+#pragma unroll
+      for (int i = 0; i < kPbBuckets / kPbThreads; ++i) agg = max(agg, v[i]);
+      unsigned long long pre = block_exclusive_scan<kPbThreads>(agg, 0ull, OpMax(), scan_sh);
+#pragma unroll
+      for (int i = 0; i < kPbBuckets / kPbThreads; ++i) {
+        const unsigned long long t = v[i];
+        v[i] = pre;
+        pre = max(pre, t);
+      }
+    }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < kPbBuckets / kPbThreads; ++i) tab[threadIdx.x * (kPbBuckets / kPbThreads) + i] = v[i];
@@ -210,9 +220,8 @@ __global__ void __launch_bounds__(kPbThreads) pb_score_kernel(Problem pb, int ml
 // O(pairs + feasible candidates) instead of O(candidates), with no division or global
 // load per candidate.
 __global__ void __launch_bounds__(kPbThreads) pb_score3_kernel(Problem pb, int ml, PbOut out) {
-  using Scan = cub::BlockScan<unsigned long long, kPbThreads>;
   __shared__ unsigned long long tab[kPbBuckets];
-  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ unsigned long long scan_sh[kPbThreads / 32];
   __shared__ int32_t sA1[256];
   __shared__ unsigned long long sTh1[256];
   __shared__ uint8_t sIdx1[256];
@@ -286,7 +295,18 @@ __global__ void __launch_bounds__(kPbThreads) pb_score3_kernel(Problem pb, int m
     unsigned long long v[kPbBuckets / kPbThreads];
 #pragma unroll
     for (int i = 0; i < kPbBuckets / kPbThreads; ++i) v[i] = tab[threadIdx.x * (kPbBuckets / kPbThreads) + i];
-    Scan(scan_tmp).ExclusiveScan(v, v, 0ull, cub::Max());
+    {  // exclusive prefix maximum over the blocked arrangement
+      unsigned long long agg = 0ull;
+#pragma unroll
+      for (int i = 0; i < kPbBuckets / kPbThreads; ++i) agg = max(agg, v[i]);
+      unsigned long long pre = block_exclusive_scan<kPbThreads>(agg, 0ull, OpMax(), scan_sh);
+#pragma unroll
+      for (int i = 0; i < kPbBuckets / kPbThreads; ++i) {
+        const unsigned long long t = v[i];
+        v[i] = pre;
+        pre = max(pre, t);
+      }
+    }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < kPbBuckets / kPbThreads; ++i) tab[threadIdx.x * (kPbBuckets / kPbThreads) + i] = v[i];
@@ -335,83 +355,6 @@ __global__ void __launch_bounds__(kPbThreads) pb_score3_kernel(Problem pb, int m
 // ---------------------------------------------------------------------------
 // frontier pass over per-stage-batch survivors
 // ---------------------------------------------------------------------------
-constexpr int kEBitsPb = 28;
-
-__device__ __forceinline__ uint64_t seg_of_pb(const ppipe_point_pb& p, const uint64_t* seg_base, int C) {
-  uint64_t off = 0, pw = 1;
-  for (int k = 1; k < p.K; ++k) {
-    pw *= (uint64_t)C;
-    off += pw;
-  }
-  uint64_t idx = 0;
-  for (int d = 0; d < p.K; ++d) idx = idx * C + p.cls[d];
-  return seg_base[p.model] + off + idx;
-}
-
-// theta key of a record. CUB's reduce-by-key may also apply its operator to the unused
-// slots of a partial tile, so K and the batch indices are clamped: garbage in, no fault.
-__device__ __forceinline__ unsigned long long rec_key(const ppipe_point_pb& p, const uint16_t* batches, int B) {
-  const int K = min((int)p.K, 3);
-  double th = stage_theta(batches[min((int)p.bidx[0], B - 1)], (int32_t)p.stage_us[0]);
-  for (int d = 1; d < K; ++d) th = fmin(th, stage_theta(batches[min((int)p.bidx[d], B - 1)], (int32_t)p.stage_us[d]));
-  return theta_key(th);
-}
-
-__global__ void pb_keys_kernel(const ppipe_point_pb* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t* keys,
-                               uint32_t* vals) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    keys[i] = (seg_of_pb(in[i], seg_base, C) << kEBitsPb) | (uint64_t)in[i].e2e_us;
-    vals[i] = (uint32_t)i;
-  }
-}
-
-__global__ void pb_gather_kernel(const ppipe_point_pb* in, const uint32_t* idx, uint64_t n, ppipe_point_pb* out) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    out[i] = in[idx[i]];
-}
-
-// Among records with the same (segment, E): theta desc, then batch indices asc, then cuts asc.
-struct PickBetterPb {
-  const uint16_t* batches;
-  int B;
-  __device__ __forceinline__ ppipe_point_pb operator()(const ppipe_point_pb& a, const ppipe_point_pb& b) const {
-    const unsigned long long ka = rec_key(a, batches, B), kb = rec_key(b, batches, B);
-    if (ka != kb) return ka > kb ? a : b;
-    for (int d = 0; d < min((int)a.K, 3); ++d)
-      if (a.bidx[d] != b.bidx[d]) return a.bidx[d] < b.bidx[d] ? a : b;
-    if (a.cut[0] != b.cut[0]) return a.cut[0] < b.cut[0] ? a : b;
-    return a.cut[1] <= b.cut[1] ? a : b;
-  }
-};
-
-__global__ void pb_group_kernel(const uint64_t* gkeys, const ppipe_point_pb* best, uint64_t ng,
-                                const uint16_t* batches, int B, uint64_t* segk, unsigned long long* th) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ng; i += (uint64_t)gridDim.x * blockDim.x) {
-    segk[i] = gkeys[i] >> kEBitsPb;
-    th[i] = rec_key(best[i], batches, B);
-  }
-}
-
-__global__ void pb_keep_kernel(const unsigned long long* th, const unsigned long long* prefix, uint64_t ng,
-                               uint8_t* keep) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ng; i += (uint64_t)gridDim.x * blockDim.x)
-    keep[i] = th[i] > prefix[i] ? 1 : 0;  // strictly above every smaller E of the segment
-}
-
-__global__ void pb_seg_start_kernel(const uint64_t* segs, uint64_t n, uint64_t n_seg, uint64_t* start) {
-  const uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (s > n_seg) return;
-  uint64_t lo = 0, hi = n;
-  while (lo < hi) {
-    const uint64_t mid = (lo + hi) >> 1;
-    if (segs[mid] < s) lo = mid + 1;
-    else hi = mid;
-  }
-  start[s] = lo;
-}
-
-inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
-
 }  // namespace
 
 // SD[k2][k3][b2][b3][c] = min_{c <= c' <= M - 1} (P_{k2,b2}[c'] + Y_{k2->k3,b2}[c'] - P_{k3,b3}[c'])
@@ -450,92 +393,6 @@ cudaError_t launch_pb_model(const Problem& pb, int ml, uint32_t M, int Kmax, con
     ++*n_launches;
   }
   return cudaGetLastError();
-}
-
-cudaError_t pb_frontier_pass(const ppipe_point_pb* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t n_seg,
-                             const uint16_t* batches, int B, ppipe_point_pb* out, uint64_t* seg_offsets,
-                             uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches) {
-  int seg_bits = 1;
-  while ((1ull << seg_bits) <= n_seg) ++seg_bits;
-  const int end_bit = kEBitsPb + seg_bits;
-  const int64_t ni = (int64_t)n;
-  size_t b_sort = 0, b_red = 0, b_scan = 0, b_sel = 0, b_sel2 = 0;
-  cudaError_t e;
-  if ((e = cub::DeviceRadixSort::SortPairs(nullptr, b_sort, (uint64_t*)nullptr, (uint64_t*)nullptr,
-                                           (uint32_t*)nullptr, (uint32_t*)nullptr, ni, 0, end_bit, s)) != cudaSuccess)
-    return e;
-  if ((e = cub::DeviceReduce::ReduceByKey(nullptr, b_red, (uint64_t*)nullptr, (uint64_t*)nullptr,
-                                          (ppipe_point_pb*)nullptr, (ppipe_point_pb*)nullptr, (int64_t*)nullptr,
-                                          PickBetterPb{nullptr, 1}, ni, s)) != cudaSuccess)
-    return e;
-  if ((e = cub::DeviceScan::ExclusiveScanByKey(nullptr, b_scan, (uint64_t*)nullptr, (unsigned long long*)nullptr,
-                                               (unsigned long long*)nullptr, cub::Max(), 0ull, ni, cub::Equality(),
-                                               s)) != cudaSuccess)
-    return e;
-  if ((e = cub::DeviceSelect::Flagged(nullptr, b_sel, (ppipe_point_pb*)nullptr, (uint8_t*)nullptr,
-                                      (ppipe_point_pb*)nullptr, (int64_t*)nullptr, ni, s)) != cudaSuccess)
-    return e;
-  if ((e = cub::DeviceSelect::Flagged(nullptr, b_sel2, (uint64_t*)nullptr, (uint8_t*)nullptr, (uint64_t*)nullptr,
-                                      (int64_t*)nullptr, ni, s)) != cudaSuccess)
-    return e;
-  const size_t tmpb = std::max(std::max(b_sort, b_red), std::max(b_scan, std::max(b_sel, b_sel2)));
-  const size_t nn = n > 0 ? n : 1;
-  size_t off = 0;
-  auto take = [&](size_t bytes) {
-    const size_t o = off;
-    off = align256(off + bytes);
-    return o;
-  };
-  const size_t o_k1 = take(nn * 8), o_k2 = take(nn * 8), o_v1 = take(nn * 4), o_v2 = take(nn * 4);
-  const size_t o_rec = take(nn * 32), o_best = take(nn * 32), o_gk = take(nn * 8), o_sk = take(nn * 8);
-  const size_t o_th = take(nn * 8), o_pre = take(nn * 8), o_keep = take(nn), o_num = take(16);
-  const size_t o_tmp = take(tmpb);
-  if (scratch->bytes < off) {
-    if (scratch->buf) cudaFree(scratch->buf);
-    scratch->buf = nullptr;
-    scratch->bytes = 0;
-    if ((e = cudaMalloc(&scratch->buf, off)) != cudaSuccess) return e;
-    scratch->bytes = off;
-  }
-  char* base = (char*)scratch->buf;
-  uint64_t *keys = (uint64_t*)(base + o_k1), *keys2 = (uint64_t*)(base + o_k2);
-  uint32_t *vals = (uint32_t*)(base + o_v1), *vals2 = (uint32_t*)(base + o_v2);
-  ppipe_point_pb *rec = (ppipe_point_pb*)(base + o_rec), *best = (ppipe_point_pb*)(base + o_best);
-  uint64_t *gkeys = (uint64_t*)(base + o_gk), *segk = (uint64_t*)(base + o_sk);
-  unsigned long long *th = (unsigned long long*)(base + o_th), *pre = (unsigned long long*)(base + o_pre);
-  uint8_t* keep = (uint8_t*)(base + o_keep);
-  int64_t* d_num = (int64_t*)(base + o_num);
-  void* tmp = base + o_tmp;
-  int64_t ng = 0, nk = 0;
-  if (n > 0) {
-    const int blocks = (int)std::min<uint64_t>((n + 255) / 256, 148 * 16);
-    pb_keys_kernel<<<blocks, 256, 0, s>>>(in, n, seg_base, C, keys, vals);
-    if ((e = cub::DeviceRadixSort::SortPairs(tmp, b_sort, keys, keys2, vals, vals2, ni, 0, end_bit, s)) !=
-        cudaSuccess)
-      return e;
-    pb_gather_kernel<<<blocks, 256, 0, s>>>(in, vals2, n, rec);
-    if ((e = cub::DeviceReduce::ReduceByKey(tmp, b_red, keys2, gkeys, rec, best, d_num, PickBetterPb{batches, B}, ni,
-                                            s)) != cudaSuccess)
-      return e;
-    if ((e = cudaMemcpyAsync(&ng, d_num, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-    const int gb = (int)std::min<int64_t>((ng + 255) / 256, 148 * 16);
-    pb_group_kernel<<<gb, 256, 0, s>>>(gkeys, best, (uint64_t)ng, batches, B, segk, th);
-    if ((e = cub::DeviceScan::ExclusiveScanByKey(tmp, b_scan, segk, th, pre, cub::Max(), 0ull, ng, cub::Equality(),
-                                                 s)) != cudaSuccess)
-      return e;
-    pb_keep_kernel<<<gb, 256, 0, s>>>(th, pre, (uint64_t)ng, keep);
-    if ((e = cub::DeviceSelect::Flagged(tmp, b_sel, best, keep, out, d_num, ng, s)) != cudaSuccess) return e;
-    if ((e = cub::DeviceSelect::Flagged(tmp, b_sel2, segk, keep, keys, d_num + 1, ng, s)) != cudaSuccess) return e;
-    if ((e = cudaMemcpyAsync(&nk, d_num, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
-    *n_launches += 10;
-  }
-  pb_seg_start_kernel<<<(unsigned)((n_seg + 1 + 255) / 256), 256, 0, s>>>(keys, (uint64_t)nk, n_seg, seg_offsets);
-  ++*n_launches;
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-  *n_out_host = (uint64_t)nk;
-  return cudaSuccess;
 }
 
 }  // namespace ppipe

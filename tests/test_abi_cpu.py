@@ -160,3 +160,15 @@ def test_partition_covers_every_row_once_and_balances(pplib, world):
     for r in range(world):
         wr = _weights(Ms, C, B, parts[r])
         assert abs(wr - total / world) <= maxrow
+
+
+@pytest.mark.parametrize("fn", ["update_profiles", "update_profiles_async"])
+def test_update_rejects_arrays_that_do_not_match_the_context(pplib, fn):
+    """The C side copies C*M*B values from the caller's pointer; the binding must
+    refuse arrays with fewer classes or batches than the loaded context (EINVAL)
+    before any pointer reaches the library."""
+    ctx = pplib.Context(None, 1, n_classes=3, n_batches=4)
+    for shape in [(2, 5, 4), (3, 5, 2), (3, 5)]:
+        with pytest.raises(pplib.PPipeError) as e:
+            getattr(pplib, fn)(ctx, [np.ones(shape, np.uint32)], [np.zeros(5, np.uint64)])
+        assert e.value.code == -1

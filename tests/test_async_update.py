@@ -71,3 +71,28 @@ def test_async_upload_errors_surface_in_pareto(oracle_built):
         assert_same_result(pp.pareto(ctx), run_oracle(w), "recovered")
     finally:
         pp.free(ctx)
+
+
+@pytest.mark.parametrize("value", [0xFFFFFFFF, 0x80000000, (1 << 28)])
+def test_async_upload_of_wrapping_latencies_fails_cleanly(oracle_built, value):
+    """Values that would wrap an int32 prefix sum (UINT32_MAX markers, 2^31) are packed
+    and scored before the device validation result is read: the pack saturates, so
+    pareto reports ERANGE (not an illegal address) and the context recovers."""
+    w = config3()
+    lat = [m.lat_us.copy() for m in w.models]
+    S = [m.act_bytes.copy() for m in w.models]
+    bad = [x.copy() for x in lat]
+    bad[5][1, :, :] = np.uint32(value)
+    bad[6][0, 0, 0] = np.uint32(value)
+    ctx = pp.load_workload(w)
+    try:
+        pp.update_profiles_async(ctx, bad, S)
+        pp.enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
+        with pytest.raises(pp.PPipeError) as e:
+            pp.pareto(ctx)
+        assert e.value.code == -2 and "model 5 class 1 batch" in str(e.value)
+        pp.update_profiles(ctx, lat, S)
+        pp.enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
+        assert_same_result(pp.pareto(ctx), run_oracle(w), "recovered after wrapping values")
+    finally:
+        pp.free(ctx)

@@ -275,3 +275,15 @@ def test_update_profiles_validates_on_device(oracle_built):
         assert_same_result(pp.pareto(ctx), run_oracle(w), "after a good update")
     finally:
         pp.free(ctx)
+
+
+@pytest.mark.parametrize("split", ["1", "3"])
+def test_frontier_pass_large_segment_paths(oracle_built, monkeypatch, split):
+    """Segments above the CTA path's shared-memory capacity (kFpCap = 4096 survivors)
+    are split by E ranges into sub-segments; PPIPE_FP_SPLIT fixes the number of
+    sub-segments so that the last-resort global-memory merge sort (split = 1: every
+    large segment whole) and uneven splits run. Result: bit-exact vs the oracle."""
+    monkeypatch.setenv("PPIPE_FP_SPLIT", split)
+    w = config4()
+    g = pp.run(w)
+    assert_same_result(g, run_oracle(w), f"config 4, PPIPE_FP_SPLIT={split}")

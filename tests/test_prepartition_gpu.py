@@ -85,3 +85,16 @@ def test_errors():
         with pytest.raises(pp.PPipeError) as e:
             pp.prepartition(lats, Ss, **bad)
         assert e.value.code == -1, bad
+
+
+def test_hand_worked_ties(oracle_built):
+    """The hand-worked tie cases of tests/test_prepartition_pins.py on the GPU (ties take the layer)."""
+    lat = np.array([[[3, 6], [2, 4], [2, 5], [5, 9]], [[30, 60], [20, 40], [20, 50], [50, 90]]], dtype=np.uint32)
+    S = np.array([11, 12, 13, 14], np.uint64)
+    b, _, _ = _check([lat], [S], 2, 0, 0, "tie [3,2,2,5]")
+    assert b[0].tolist() == [0, 3, 4]
+    b, _, _ = _check([lat], [S], 2, 0, 1, "no tie at b=2")
+    assert b[0].tolist() == [0, 2, 4]
+    one = np.array([1, 2, 1], np.uint32).reshape(1, 3, 1)
+    b, _, _ = _check([one], [np.zeros(3, np.uint64)], 2, 0, 0, "tie [1,2,1]")
+    assert b[0].tolist() == [0, 2, 3]

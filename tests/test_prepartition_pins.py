@@ -88,3 +88,37 @@ def test_rejects_bad_block_counts(oracle_built):
         prepartition_oracle(_lat([1, 2, 3]), np.zeros(3, np.uint64), 4, 0, 0)
     with pytest.raises(ValueError):
         prepartition_oracle(_lat([1, 2, 3]), np.zeros(3, np.uint64), 0, 0, 0)
+
+
+def test_hand_worked_ties_take_the_layer(oracle_built):
+    """Hand-worked ties of the greedy rule (PAPER.md:1005-1010 "as close as possible";
+    ties include the layer, SPEC.md:138 / DESIGN.md reading of §5.2).
+
+    t = [3, 2, 2, 5] (us), N = 2, total 12, target 12/2 = 6, compared as |N*acc - total|:
+      block 1 starts with layer 0: acc = 3 (|6 - 12| = 6)
+      layer 1: |2*5 - 12| = 2 <= 6  -> take, acc = 5
+      layer 2: |2*7 - 12| = 2 <= 2  -> TIE, take, acc = 7
+      layer 3 must stay for block 2 (one layer per remaining block) -> bounds [0, 3, 4]
+    A strict "closer" rule would stop at [0, 2, 4]; a dropped tie rule fails here.
+    Per-class / per-batch sums and the last layer's bytes follow by hand."""
+    lat = np.array([[[3, 6], [2, 4], [2, 5], [5, 9]],        # class 0 (reference), b = 1, 2
+                    [[30, 60], [20, 40], [20, 50], [50, 90]]], dtype=np.uint32)
+    S = np.array([11, 12, 13, 14], np.uint64)
+    b, blat, bS = prepartition_oracle(lat, S, 2, 0, 0)
+    assert b.tolist() == [0, 3, 4]
+    assert blat[0].tolist() == [[7, 15], [5, 9]]
+    assert blat[1].tolist() == [[70, 150], [50, 90]]
+    assert bS.tolist() == [13, 14]
+    # the same tie at the reference batch b = 2: t = [6, 4, 5, 9], total 24, N*acc - total:
+    #   acc 6 (|12-24| = 12); +4 -> |20-24| = 4 take; +5 -> |30-24| = 6 > 4 stop -> [0, 2, 4]
+    b2, _, _ = prepartition_oracle(lat, S, 2, 0, 1)
+    assert b2.tolist() == [0, 2, 4]
+    # a tie at the very first comparison: t = [1, 2, 1], N = 2, total 4:
+    #   acc 1 (|2-4| = 2); +2 -> |6-4| = 2 tie -> take; layer 2 left for block 2 -> [0, 2, 3]
+    b3, blat3, _ = prepartition_oracle(_lat([1, 2, 1]), np.zeros(3, np.uint64), 2, 0, 0)
+    assert b3.tolist() == [0, 2, 3] and blat3[0, :, 0].tolist() == [3, 1]
+    # three blocks, tie in the middle block: t = [4, 2, 2, 2, 2], N = 3, total 12 (target 4):
+    #   block 1: acc 4 (|12-12| = 0); +2 -> |18-12| = 6 > 0 stop -> layer 1 starts block 2
+    #   block 2: acc 2 (|6-12| = 6); +2 -> |12-12| = 0 take; +2 -> 6 > 0 stop -> [0, 1, 3, 5]
+    b4, _, _ = prepartition_oracle(_lat([4, 2, 2, 2, 2]), np.zeros(5, np.uint64), 3, 0, 0)
+    assert b4.tolist() == [0, 1, 3, 5]

@@ -173,8 +173,9 @@ def config2() -> Workload:
                     [ModelProfile("resnet50-blocks", lat, S)], np.array([200000], dtype=np.uint32), 400, 3)
 
 
-def _prepartition(lat: np.ndarray, S: np.ndarray, n_blocks: int, ref_class: int, b1: int):
-    """Greedy equal-runtime pre-partitioning (§5.2).
+def _prepartition_input_step(lat: np.ndarray, S: np.ndarray, n_blocks: int, ref_class: int, b1: int):
+    """INPUT STEP (not the method under test): build config 3's block profiles by
+    greedy equal-runtime grouping (§5.2).
 
     Extend the current block while doing so brings its batch-1 runtime on the
     reference class closer to total/N (ties include the layer), leaving at least
@@ -224,7 +225,7 @@ def config3(n_models: int = 18, n_blocks: Optional[int] = 10) -> Workload:
         if n_blocks is None:
             models.append(ModelProfile(f"cnn{m:02d}", lat, S))
         else:
-            blat, bS, _ = _prepartition(lat, S, n_blocks, classes.index("L4"), 0)
+            blat, bS, _ = _prepartition_input_step(lat, S, n_blocks, classes.index("L4"), 0)
             models.append(ModelProfile(f"cnn{m:02d}-N{n_blocks}", blat, bS))
         slos.append(slo)
     return Workload(3, CONFIG_NAMES[3], classes, batches, _bw_matrix(classes), models,
