@@ -238,6 +238,7 @@ struct ppipe_ctx {
   DevBuf<unsigned long long> d_err;
   // F2 (ppipe_pareto_f2)
   DevBuf<int32_t> d_G, d_F, d_E23, d_pbsd, d_minA;
+  DevBuf<unsigned long long> d_gfold;  // cross-batch fold of the K = 3 segments (Problem::gfold)
   DevBuf<uint16_t> d_inv;  // F2 inverse stage tables PF, PFs, SF, SFs
   DevBuf<ppipe_point> d_f2surv, d_f2tmp;
   uint64_t f2_cap = 1ull << 20;
@@ -322,6 +323,7 @@ void free_ctx(ppipe_ctx* c) {
   c->d_E23.release();
   c->d_pbsd.release();
   c->d_minA.release();
+  c->d_gfold.release();
   c->d_inv.release();
   c->d_f2surv.release();
   c->d_f2tmp.release();
@@ -865,6 +867,12 @@ static int run_enumerate(ppipe_ctx* c) {
   const size_t tab_words = hot_unit_table_bytes(pb) / 8;
   CU(c, c->d_hot.reserve(c->hot_cap));
   CU(c, c->d_hot_tab.reserve(c->hot_cap * tab_words));
+  if (pb.Kmax >= 3 && !getenv("PPIPE_NO_GFOLD")) {  // (the env switch is for measurements only)
+    const size_t ng = gfold_elems(pb);
+    CU(c, c->d_gfold.reserve(ng));
+    CU(c, cudaMemsetAsync(c->d_gfold.p, 0, sizeof(unsigned long long) * ng, c->stream));
+    pb.gfold = c->d_gfold.p;
+  }
   ScoreOut so{c->d_surv.p, c->d_counters.p, (unsigned long long)c->d_surv.n, c->d_hot.p, c->d_hot_tab.p,
               (unsigned long long)c->hot_cap};
   c->launches_i = 0;

@@ -56,6 +56,13 @@ struct Problem {
   // A = C_1 + Y_1 - P[k2][c_1] (written by the pack launch; nullptr = not kept)
   int32_t* minA;
   int max_tiles;
+  // Cross-batch fold of the K = 3 segments (nullptr = off): per (local model, k1, k2, k3)
+  // row of nb + 1 entries, the best theta = b / Cmax (bits of the double) of any unit's
+  // bucket-best point per E-bucket, pushed by score3a; turned into an exclusive prefix
+  // maximum by gfold_prefix before score3b, which folds it into every hot unit's bound
+  // U(E) (a candidate at or below the best theta of a strictly smaller E-bucket of any
+  // batch is dominated).
+  unsigned long long* gfold;
 };
 
 struct ScoreOut {
@@ -68,6 +75,10 @@ struct ScoreOut {
 };
 
 size_t hot_unit_table_bytes(const Problem& pb);
+// E-buckets of the K = 3 fold tables (the same for every unit of a problem)
+int score_nb(const Problem& pb);
+// Problem::gfold elements: n_local * C^3 * (nb + 1)
+size_t gfold_elems(const Problem& pb);
 
 // F2 (ppipe_f2.cu): per-model strict-dominance queries append the candidates no
 // other feasible candidate beats in every stage (ties left in) to surv.

@@ -257,13 +257,23 @@ __device__ __forceinline__ int wmul(int w, int c) {
   return v > INT_MAX ? INT_MAX : (int)v;
 }
 
-// raw [nc][nb + 2] -> fin [nc][nb + 2] (fin may be global memory). One warp per k_1.
+// theta = b / C as the bits of the double (C = 0: +inf). Exact order for b < 2^16,
+// C < 2^32: distinct fractions differ by a relative >= 2^-48 > 2^-53.
+__device__ __forceinline__ unsigned long long theta_bits(uint32_t b, uint32_t C) {
+  return C ? (unsigned long long)__double_as_longlong((double)b / (double)C) : 0x7FF0000000000000ull;
+}
+
+// raw [nc][nb + 2] -> fin [nc][nb + 2] (fin may be global memory; nullptr: not written).
+// One warp per k_1. With gf (the unit's K = 3 global-fold rows, k1-major, stride
+// gf_stride), every bucket-best point that improves on all earlier buckets of the unit
+// (a step of the unit's staircase) pushes its theta = b / Cmax into gf[k1][bucket].
 __device__ __noinline__ void tables_finalize(const uint32_t* raw, uint2* fin, int nc, int nb, int sh, int warp,
-                                             int nwarps) {
+                                             int nwarps, unsigned long long* gf = nullptr, size_t gf_stride = 0,
+                                             uint32_t b = 0, int q = 0) {
   const int lane = threadIdx.x & 31;
   for (int k = warp; k < nc; k += nwarps) {
     const uint32_t* r = raw + (size_t)k * (nb + 2);
-    uint2* f = fin + (size_t)k * (nb + 2);
+    uint2* f = fin ? fin + (size_t)k * (nb + 2) : nullptr;
     uint32_t run = kEmpty;
     for (int r0 = 0; r0 < nb; r0 += 32) {
       const uint32_t key = r[r0 + lane];
@@ -276,11 +286,50 @@ __device__ __noinline__ void tables_finalize(const uint32_t* raw, uint2* fin, in
       }
       uint32_t excl = __shfl_up_sync(FULL_MASK, incl, 1);
       if (lane == 0) excl = kEmpty;
-      f[r0 + lane] = make_uint2(min(run, excl), key);
+      if (f) f[r0 + lane] = make_uint2(min(run, excl), key);
+      // the bucket's best point is a real candidate with Cmax <= c << q (rounded up when
+      // q > 0, so its theta is at least b / (c << q))
+      if (gf && c != kEmpty && c < min(run, excl))
+        atomicMax(gf + (size_t)k * gf_stride + r0 + lane, theta_bits(b, c << q));
       run = min(run, __shfl_sync(FULL_MASK, incl, 31));
     }
-    if (lane == 0) f[nb] = make_uint2(run, kEmpty);
+    if (f && lane == 0) f[nb] = make_uint2(run, kEmpty);
   }
+}
+
+// Exclusive prefix maximum of every global-fold row (nb + 1 entries) in place: entry j
+// = the best theta of buckets < j. Warp per row.
+__global__ void __launch_bounds__(256) gfold_prefix_kernel(unsigned long long* gf, size_t rows, int nb1) {
+  const int lane = threadIdx.x & 31;
+  const size_t row = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= rows) return;
+  unsigned long long* g = gf + row * nb1;
+  unsigned long long run = 0ull;
+  for (int j0 = 0; j0 < nb1; j0 += 32) {
+    const int j = j0 + lane;
+    const unsigned long long v = j < nb1 ? g[j] : 0ull;
+    unsigned long long incl = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long o = __shfl_up_sync(FULL_MASK, incl, d);
+      if (lane >= d) incl = max(incl, o);
+    }
+    unsigned long long excl = __shfl_up_sync(FULL_MASK, incl, 1);
+    if (lane == 0) excl = 0ull;
+    if (j < nb1) g[j] = max(run, excl);
+    run = max(run, __shfl_sync(FULL_MASK, incl, 31));
+  }
+}
+
+// The smallest Cmax a candidate of batch b must reach to be dominated by a point of
+// theta g (a double b' / C' from the global fold): any Cmax >= bound has b / Cmax <
+// b' / C'. Conservative by a relative 2^-30 against the rounding of g (so it never
+// drops a candidate that is not strictly dominated); 0 for g = +inf.
+__device__ __forceinline__ uint32_t gfold_bound(unsigned long long gbits, uint32_t b) {
+  const double g = __longlong_as_double((long long)gbits);
+  if (gbits >= 0x7FF0000000000000ull) return 0u;
+  const double c = (double)b / g * (1.0 + 0x1p-30);
+  return c >= 4294967294.0 ? 0xffffffffu : (uint32_t)c + 1u;
 }
 
 // Is a feasible candidate (E, Cmax) kept by the finalized row (see above)?
@@ -1160,9 +1209,14 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
                                          (unsigned)s_tmask, (unsigned)(s_tmask >> 32));
         }
         __syncthreads();
-        if (s_slot < out.hot_cap)  // finalized tables straight to the unit's global slot
-          tables_finalize(sm.raw, reinterpret_cast<uint2*>(out.hot_tab) + s_slot * (unsigned long long)ntab, NC, nb,
-                          cx.sh, warp, kWarps);
+        // finalized tables straight to the unit's global slot; staircase steps to the
+        // cross-batch fold of the unit's segments (k1, k2, k3)
+        unsigned long long* gf = pb.gfold ? pb.gfold + ((size_t)ml * NC * NC * NC + (size_t)k2 * NC + k3) * (nb + 1)
+                                          : nullptr;
+        tables_finalize(sm.raw,
+                        s_slot < out.hot_cap ? reinterpret_cast<uint2*>(out.hot_tab) + s_slot * (unsigned long long)ntab
+                                             : nullptr,
+                        NC, nb, cx.sh, warp, kWarps, gf, (size_t)NC * NC * (nb + 1), (uint32_t)cx.b, cx.q);
       }
       __syncthreads();
       reset_raw(sm.raw, ntab, tid, 32 * kWarps);
@@ -1203,7 +1257,26 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
     cx.row_len = row_len;
     const K3Range r = k3_range(md);
     const uint2* src = reinterpret_cast<const uint2*>(out.hot_tab) + u * (unsigned long long)ntab;
-    for (int i = tid; i < ntab; i += 32 * kWarps) sm.fin[i] = src[i];
+    if (pb.gfold) {
+      // U'(j) = min(U(j), ceil(bound_j / 2^q)): the unit's own bound and the cross-batch one
+      const unsigned long long* gf = pb.gfold + ((size_t)ml * NC * NC * NC + (size_t)k2 * NC + k3) * (nb + 1);
+      for (int i = tid; i < ntab; i += 32 * kWarps) {
+        uint2 e = src[i];
+        const int k1 = i / (nb + 2), j = i - k1 * (nb + 2);
+        if (j <= nb) {
+          const unsigned long long g = gf[(size_t)k1 * NC * NC * (nb + 1) + j];
+          if (g) {
+            const uint32_t bnd = gfold_bound(g, (uint32_t)cx.b);
+            // bounds at or above 2^31 exceed every feasible (weighted) Cmax: no bound
+            const uint32_t ub = bnd >= 0x80000000u ? kEmpty : (uint32_t)(((uint64_t)bnd + ((1ull << cx.q) - 1)) >> cx.q);
+            e.x = min(e.x, ub);
+          }
+        }
+        sm.fin[i] = e;
+      }
+    } else {
+      for (int i = tid; i < ntab; i += 32 * kWarps) sm.fin[i] = src[i];
+    }
     stage_rows(cx, sm, k3, r.c2_from, r.c2_to, true);
     if (tid == 0) s_tile = 0;
     __syncthreads();
@@ -1308,6 +1381,11 @@ static cudaError_t launch_score_w(const Problem& pb, const ScoreOut& out, cudaSt
     cudaEventRecord(ss->fork, s);
     cudaStreamWaitEvent(s12, ss->fork, 0);
   }
+  if (pb.Kmax >= 3 && pb.gfold && pb.n_local > 0) {
+    const size_t rows = (size_t)pb.n_local * NC * NC * NC;
+    gfold_prefix_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(pb.gfold, rows, (1 << nb_log2) + 1);
+    ++*n_launches;
+  }
   if (pb.Kmax >= 3) {
     int dev = 0, n_sm = 148, smem_sm = 227 * 1024;
     cudaGetDevice(&dev);
@@ -1333,6 +1411,12 @@ static cudaError_t launch_score_nc(const Problem& pb, const ScoreOut& out, cudaS
                                   int part) {
   return pb.wpack == 0x11111111u ? launch_score_w<NC, false>(pb, out, s, n_launches, part)
                                  : launch_score_w<NC, true>(pb, out, s, n_launches, part);
+}
+
+int score_nb(const Problem& pb) { return (int)(hot_unit_table_bytes(pb) / (8 * (size_t)pb.C)) - 2; }
+
+size_t gfold_elems(const Problem& pb) {
+  return (size_t)std::max(pb.n_local, 1) * pb.C * pb.C * pb.C * (score_nb(pb) + 1);
 }
 
 // Bytes of one hot unit's tables for this problem (the ABI sizes its buffer with it).
