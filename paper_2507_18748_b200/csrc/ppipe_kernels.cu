@@ -522,17 +522,26 @@ struct SlotData {
   int32_t* p1s;    // [kJ1][32] P[k2][c1]
   uint16_t* list;  // [kJ1 * NC * 32] (lane << 5 | slot) of the current c2
 };
+#ifndef PPIPE_SLOT_SMEM
+#define PPIPE_SLOT_SMEM 0  // 1: pass-2 slot values staged in shared memory (else re-read through L1)
+#endif
 template <int NC>
 __host__ __device__ constexpr size_t slot_bytes() {
-  return (size_t)kJ1 * 32 * (2 * sizeof(int32_t) * NC + sizeof(int32_t) + sizeof(uint16_t) * NC);
+  return PPIPE_SLOT_SMEM ? (size_t)kJ1 * 32 * (2 * sizeof(int32_t) * NC + sizeof(int32_t) + sizeof(uint16_t) * NC)
+                         : (size_t)kJ1 * 32 * sizeof(uint16_t) * NC;
 }
 template <int NC>
 __device__ __forceinline__ SlotData carve_slot(uint8_t* base) {
   SlotData d;
+#if PPIPE_SLOT_SMEM
   d.As = reinterpret_cast<int32_t*>(base);
   d.C1s = d.As + kJ1 * NC * 32;
   d.p1s = d.C1s + kJ1 * NC * 32;
   d.list = reinterpret_cast<uint16_t*>(d.p1s + kJ1 * 32);
+#else
+  d.As = d.C1s = d.p1s = nullptr;
+  d.list = reinterpret_cast<uint16_t*>(base);
+#endif
   return d;
 }
 
@@ -625,13 +634,17 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
           }
         }
         // this lane's slot data for the dense survivor pass (E = A + B(c2) exactly)
+#if PPIPE_SLOT_SMEM
         sd.As[(j * NC + k1) * 32 + lane] = valid ? C1 + y - p1[j] : 0;
         sd.C1s[(j * NC + k1) * 32 + lane] = C1;
+#endif
       }
       thr[j][k1] = t;
       c1r[j][k1] = wmul(wtw<W>(wp, k1), C1);  // weighted: only Cmax uses it
     }
+#if PPIPE_SLOT_SMEM
     if (pass == 2) sd.p1s[j * 32 + lane] = p1[j];
+#endif
     if (pass == 1 && valid) cand += (unsigned long long)(cx.M - 1 - c1) * NC;
   }
   const int m1 = cx.m1;
@@ -872,9 +885,19 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
             const unsigned e = sd.list[i];
             const int src = (int)(e >> 5), sl = (int)(e & 31u);
             const int j = sl / NC, k1 = sl - j * NC;
+#if PPIPE_SLOT_SMEM
             const int E = sd.As[sl * 32 + src] + Bv;
             const int C1 = sd.C1s[sl * 32 + src];
             const int C2 = Q - sd.p1s[j * 32 + src];
+#else
+            // the listed candidate's first-cut terms, re-read through L1 (the tile's rows
+            // are a few KB): C_1 = P[k1][c1], Y_1 and P[k2][c1]
+            const int c1 = c1_base + 32 * j + src;
+            const int C1 = __ldg(cx.Prow(k1) + c1);
+            const int pc1 = __ldg(cx.P2 + c1);
+            const int E = C1 + __ldg(cx.Yrow(k1, cx.k2) + c1) - pc1 + Bv;
+            const int C2 = Q - pc1;
+#endif
             // listed candidates are feasible: C_1, C_2 <= E <= T_eff and w * T_eff < 2^31
             const int Cmax = max(max(wtw<W>(wp, k1) * C1, w2 * C2), Rw);
             PPIPE_DCHECK(E >= 0 && E <= cx.T && (E >> cx.sh) < nb + 2 && src < 32 && j < kJ1);
@@ -1151,7 +1174,7 @@ __global__ void __launch_bounds__(32 * kWarps, PPIPE_12_CTAS_PER_SM)
 #endif
 constexpr int k3aCtasPerSm = PPIPE_3A_CTAS_PER_SM;
 #ifndef PPIPE_3B_CTAS_PER_SM
-#define PPIPE_3B_CTAS_PER_SM 6
+#define PPIPE_3B_CTAS_PER_SM 7
 #endif
 constexpr int k3bCtasPerSm = PPIPE_3B_CTAS_PER_SM;  // pass 2 holds more live state: fewer, fatter warps
 template <int NC, bool W>
