@@ -168,6 +168,22 @@ typedef struct {
  * done. Errors: PPIPE_ESTATE (no prior ppipe_enumerate), PPIPE_ECUDA, PPIPE_ENCCL. */
 int ppipe_pareto(ppipe_ctx *ctx, int copy_to_host, ppipe_frontier *out);
 
+/* Merge the LOCAL frontiers of n_shards shard-mode contexts into the global frontier
+ * (the decomposability F(A u B) = F(F(A) u F(B)) of the (E, theta)
+ * staircase). shards[r] must be rank r of world n_shards loaded WITHOUT an NCCL id (shard
+ * mode), on the same device, with the same models / classes / batches, each after a
+ * successful ppipe_enumerate (same max_partitions, slo_us, margin_permille, vGPU
+ * weights) and ppipe_pareto. This runs the same merge the NCCL path runs after its two
+ * all-gathers -- counters and padded local frontiers in rank order, re-reduction of the
+ * models that straddle a rank boundary, rank-ordered assembly, CSR -- with the
+ * all-gathers replaced by device-to-device copies, so one GPU can check the multi-GPU
+ * merge. The result (byte-identical to a one-rank ppipe_pareto of the same workload) is
+ * owned by shards[0] like a ppipe_pareto result and replaces its local result; the other
+ * shards are unchanged. n_candidates / n_feasible are summed over the shards. Errors:
+ * EINVAL (NULL, ranks / shapes / parameters that do not match), ESTATE (a shard without a
+ * local result), ECUDA / ENOMEM. */
+int ppipe_merge_shards(ppipe_ctx *const *shards, int n_shards, int copy_to_host, ppipe_frontier *out);
+
 /* F2, the MILP-lossless frontier (DESIGN.md §3 F2-1..F2-4).
  * PPipe's pooled MILP gives a chosen pipeline g_d GPUs in stage d and gets
  * throughput min_d g_d X_d, X_d = b / C_d the per-GPU throughput of stage d

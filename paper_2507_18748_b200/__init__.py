@@ -15,6 +15,7 @@ from ._binding import (  # noqa: F401
     frontier_at,
     load_profiles,
     load_workload,
+    merge_shards,
     nccl_unique_id,
     pareto,
     pareto_f2,

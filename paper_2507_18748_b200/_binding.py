@@ -103,6 +103,8 @@ def lib():
         L.ppipe_frontier_at.restype = ct.c_int
         L.ppipe_frontier_at.argtypes = [ct.c_void_p, ct.POINTER(ct.c_uint32), ct.c_uint32, ct.c_int,
                                         ct.POINTER(_Frontier)]
+        L.ppipe_merge_shards.restype = ct.c_int
+        L.ppipe_merge_shards.argtypes = [ct.POINTER(ct.c_void_p), ct.c_int, ct.c_int, ct.POINTER(_Frontier)]
         L.ppipe_free.restype = None
         L.ppipe_free.argtypes = [ct.c_void_p]
         L.ppipe_last_error.restype = ct.c_char_p
@@ -263,6 +265,16 @@ def pareto(ctx: Context, copy_to_host: bool = True, zero_copy: bool = False) -> 
     valid only until the next pareto() / frontier_at() / free() on this context."""
     f = _Frontier()
     _check(lib().ppipe_pareto(ctx.handle, 1 if copy_to_host else 0, ct.byref(f)), ctx.handle)
+    return _frontier_from(f, copy_to_host, zero_copy)
+
+
+def merge_shards(ctxs: Sequence[Context], copy_to_host: bool = True, zero_copy: bool = False) -> Frontier:
+    """Merge the local frontiers of shard-mode contexts (rank r of len(ctxs), no NCCL id,
+    one GPU) with the library's multi-GPU merge (include/ppipe.h ppipe_merge_shards).
+    The result is owned by ctxs[0]."""
+    arr = (ct.c_void_p * len(ctxs))(*[c.handle for c in ctxs])
+    f = _Frontier()
+    _check(lib().ppipe_merge_shards(arr, len(ctxs), 1 if copy_to_host else 0, ct.byref(f)), ctxs[0].handle)
     return _frontier_from(f, copy_to_host, zero_copy)
 
 

@@ -216,7 +216,8 @@ struct ppipe_ctx {
   bool have_result = false;
   const ppipe_point* res_pts = nullptr;
   const uint64_t* res_off = nullptr;
-  uint64_t res_n = 0, res_ncand = 0;
+  uint64_t res_n = 0, res_ncand = 0, res_nfeas = 0, res_nsurv = 0;
+  bool res_local = false;
   DevBuf<ppipe_point> d_trunc;
   DevBuf<uint64_t> d_trunc_off;
   DevBuf<uint32_t> d_Tnew;
@@ -724,6 +725,7 @@ PPIPE_API int ppipe_update_profiles(ppipe_ctx* c, uint32_t n_models, const ppipe
   c->profiles_ok = false;
   c->enumerated = false;
   c->have_result = false;
+  c->res_local = false;
   c->pending_upload = false;  // a synchronous update supersedes a pending asynchronous one
   CU(c, cudaSetDevice(c->device));
   for (size_t i = 0; i < c->local.size(); ++i) {
@@ -778,6 +780,7 @@ PPIPE_API int ppipe_update_profiles_async(ppipe_ctx* c, uint32_t n_models, const
   c->profiles_ok = true;  // values are checked on the device; errors surface in ppipe_pareto
   c->enumerated = false;
   c->have_result = false;
+  c->res_local = false;
   return PPIPE_OK;
 }
 
@@ -965,6 +968,7 @@ PPIPE_API int ppipe_enumerate(ppipe_ctx* ctx, const ppipe_enum_params* p) {
   int rc0 = check_params(ctx, p, "ppipe_enumerate");
   if (rc0 != PPIPE_OK) return rc0;
   ctx->have_result = false;
+  ctx->res_local = false;
   ctx->last_params = *p;
   ctx->last_slo.assign(p->slo_us, p->slo_us + ctx->n_models);
   ctx->last_params.slo_us = ctx->last_slo.data();
@@ -972,6 +976,129 @@ PPIPE_API int ppipe_enumerate(ppipe_ctx* ctx, const ppipe_enum_params* p) {
   int rc = run_enumerate(ctx);
   if (rc == PPIPE_OK) ctx->enumerated = true;
   return rc;
+}
+
+// ---- frontier merge ----
+// Per rank: [n_points, n_cand, n_feas, n_surv, first model + 1, last model + 1, points of
+// the first model, points of the last model] of its local frontier (0 models: 0, 0).
+constexpr int kMergeCnt = 8;
+
+static int local_counters(ppipe_ctx* c, uint64_t n_local_pts, uint64_t n_cand, uint64_t n_feas, uint64_t n_surv,
+                          uint64_t out[kMergeCnt]) {
+  int mf = -1, ml = -1;
+  for (int m : c->local) {
+    mf = mf < 0 ? m : std::min(mf, m);
+    ml = std::max(ml, m);
+  }
+  uint64_t nfirst = 0, nlast = 0;
+  if (mf >= 0) {
+    uint64_t b[4];
+    const uint64_t at[4] = {c->h_segbase[mf], c->h_segbase[mf + 1], c->h_segbase[ml], c->h_segbase[ml + 1]};
+    for (int i = 0; i < 4; ++i)
+      CU(c, cudaMemcpyAsync(&b[i], c->d_segoff_local.p + at[i], 8, cudaMemcpyDeviceToHost, c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
+    nfirst = b[1] - b[0];
+    nlast = b[3] - b[2];
+  }
+  const uint64_t hs[kMergeCnt] = {n_local_pts, n_cand, n_feas, n_surv, (uint64_t)(mf + 1), (uint64_t)(ml + 1),
+                                  nfirst, nlast};
+  std::memcpy(out, hs, sizeof hs);
+  return PPIPE_OK;
+}
+
+// Every model lies on one rank except the <= world - 1 models at range boundaries, and
+// each rank's local frontier is in canonical order, so the global frontier is the
+// rank-ordered concatenation of the local ones with only the straddling models' points
+// re-reduced (decomposability: F(A u B) = F(F(A) u F(B))). Input: every rank's counters
+// (cnts, kMergeCnt per rank) and its local frontier at d_gather + r * maxc. Output:
+// d_final / d_segoff_final of c, *n_pts; *n_cand / *n_feas summed over the ranks.
+static int merge_assemble(ppipe_ctx* c, const std::vector<uint64_t>& cnts, uint64_t maxc, int* nl, uint64_t* n_cand,
+                          uint64_t* n_feas, uint64_t* n_pts) {
+  uint64_t tot = 0;
+  *n_cand = *n_feas = 0;
+  for (int r = 0; r < c->world; ++r) {
+    tot += cnts[kMergeCnt * r];
+    *n_cand += cnts[kMergeCnt * r + 1];
+    *n_feas += cnts[kMergeCnt * r + 2];
+  }
+  // pieces in rank order: (model or -1 for a run of whole models, source, count)
+  struct Piece {
+    long long model;
+    uint64_t src, n;
+  };
+  std::vector<Piece> pieces;
+  for (int r = 0; r < c->world; ++r) {
+    const uint64_t* q = &cnts[kMergeCnt * (size_t)r];
+    if (q[4] == 0) continue;  // no rows on rank r
+    const long long f = (long long)q[4] - 1, l = (long long)q[5] - 1;
+    const uint64_t base = (uint64_t)r * maxc, n = q[0];
+    if (f == l) {
+      pieces.push_back({f, base, n});
+    } else {
+      pieces.push_back({f, base, q[6]});
+      pieces.push_back({-1, base + q[6], n - q[6] - q[7]});
+      pieces.push_back({l, base + n - q[7], q[7]});
+    }
+  }
+  // a model with pieces from two or more ranks straddles: re-reduce its points
+  std::vector<char> dirty(pieces.size(), 0);
+  std::vector<long long> straddle;
+  for (size_t i = 0; i < pieces.size(); ++i)
+    for (size_t k = i + 1; k < pieces.size() && pieces[k].model == pieces[i].model && pieces[i].model >= 0; ++k) {
+      dirty[i] = dirty[k] = 1;
+      if (straddle.empty() || straddle.back() != pieces[i].model) straddle.push_back(pieces[i].model);
+    }
+  uint64_t n_dirty = 0;
+  for (size_t i = 0; i < pieces.size(); ++i)
+    if (dirty[i]) n_dirty += pieces[i].n;
+  CU(c, c->d_union.reserve(std::max<uint64_t>(n_dirty, 1)));
+  uint64_t off = 0;
+  for (size_t i = 0; i < pieces.size(); ++i)
+    if (dirty[i] && pieces[i].n) {
+      CU(c, cudaMemcpyAsync(c->d_union.p + off, c->d_gather.p + pieces[i].src, sizeof(ppipe_point) * pieces[i].n,
+                            cudaMemcpyDeviceToDevice, c->stream));
+      off += pieces[i].n;
+    }
+  CU(c, c->d_final.reserve(std::max<uint64_t>(tot, 1)));
+  CU(c, c->d_segoff_final.reserve(c->n_seg_total + 1));
+  CU(c, c->d_merged.reserve(std::max<uint64_t>(n_dirty, 1)));
+  uint64_t n_merged = 0;
+  std::vector<uint64_t> mcount(straddle.size(), 0);
+  if (n_dirty) {
+    CU(c, frontier_pass(c->d_union.p, n_dirty, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_merged.p,
+                        c->d_segoff_final.p, &n_merged, &c->scratch, c->stream, nl, c->wpack));
+    std::vector<uint64_t> b(2 * straddle.size());
+    for (size_t i = 0; i < straddle.size(); ++i) {
+      CU(c, cudaMemcpyAsync(&b[2 * i], c->d_segoff_final.p + c->h_segbase[straddle[i]], 8, cudaMemcpyDeviceToHost,
+                            c->stream));
+      CU(c, cudaMemcpyAsync(&b[2 * i + 1], c->d_segoff_final.p + c->h_segbase[straddle[i] + 1], 8,
+                            cudaMemcpyDeviceToHost, c->stream));
+    }
+    CU(c, cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < straddle.size(); ++i) mcount[i] = b[2 * i + 1] - b[2 * i];
+  }
+  // assemble in order: clean pieces from the gathered frontiers, each straddling
+  // model's merged block in place of its first piece
+  uint64_t w = 0, moff = 0;
+  size_t si = 0;
+  for (size_t i = 0; i < pieces.size(); ++i) {
+    const ppipe_point* src = c->d_gather.p + pieces[i].src;
+    uint64_t n = pieces[i].n;
+    if (dirty[i]) {
+      if (i > 0 && dirty[i - 1] && pieces[i - 1].model == pieces[i].model) continue;
+      src = c->d_merged.p + moff;
+      n = mcount[si];
+      moff += n;
+      ++si;
+    }
+    if (n) CU(c, cudaMemcpyAsync(c->d_final.p + w, src, sizeof(ppipe_point) * n, cudaMemcpyDeviceToDevice, c->stream));
+    w += n;
+  }
+  *n_pts = w;
+  CU(c, c->d_segtmp.reserve(std::max<uint64_t>(w, 1)));
+  CU(c, segment_offsets(c->d_final.p, w, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_segoff_final.p,
+                        c->d_segtmp.p, c->stream, nl));
+  return PPIPE_OK;
 }
 
 PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) {
@@ -1031,43 +1158,21 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
   const uint64_t* d_off = c->d_segoff_local.p;
   uint64_t n_pts = n_local_pts;
   if (c->world > 1 && c->comm) {
-    // Every model lies on one rank except the <= world - 1 models at range
-    // boundaries, and each rank's frontier is in canonical order, so the global
-    // frontier is the rank-ordered concatenation with only the straddling models'
-    // points re-reduced. Per rank: [n_points, n_cand, n_feas, n_surv, first model + 1,
-    // last model + 1, points of the first model, points of the last model].
-    int mf = -1, ml = -1;
-    for (int m : c->local) {
-      mf = mf < 0 ? m : std::min(mf, m);
-      ml = std::max(ml, m);
-    }
-    uint64_t nfirst = 0, nlast = 0;
-    if (mf >= 0) {
-      uint64_t b[4];
-      const uint64_t at[4] = {c->h_segbase[mf], c->h_segbase[mf + 1], c->h_segbase[ml], c->h_segbase[ml + 1]};
-      for (int i = 0; i < 4; ++i)
-        CU(c, cudaMemcpyAsync(&b[i], c->d_segoff_local.p + at[i], 8, cudaMemcpyDeviceToHost, c->stream));
-      CU(c, cudaStreamSynchronize(c->stream));
-      nfirst = b[1] - b[0];
-      nlast = b[3] - b[2];
-    }
-    constexpr int kCnt = 8;
-    CU(c, c->d_cnt_send.reserve(kCnt));
-    CU(c, c->d_cnt_recv.reserve(kCnt * (size_t)c->world));
-    uint64_t hs[kCnt] = {n_local_pts, n_cand, n_feas, n_surv, (uint64_t)(mf + 1), (uint64_t)(ml + 1), nfirst, nlast};
+    // The only multi-GPU-specific step: all-gather every rank's counters and its padded
+    // local frontier over NCCL into d_gather; merge_assemble (shared with the one-GPU
+    // ppipe_merge_shards) does the rest.
+    uint64_t hs[kMergeCnt];
+    int rc = local_counters(c, n_local_pts, n_cand, n_feas, n_surv, hs);
+    if (rc != PPIPE_OK) return rc;
+    CU(c, c->d_cnt_send.reserve(kMergeCnt));
+    CU(c, c->d_cnt_recv.reserve(kMergeCnt * (size_t)c->world));
     CU(c, cudaMemcpyAsync(c->d_cnt_send.p, hs, sizeof hs, cudaMemcpyHostToDevice, c->stream));
-    NC_(c, g_nccl.AllGather(c->d_cnt_send.p, c->d_cnt_recv.p, kCnt, ncclUint64, c->comm, c->stream));
-    std::vector<uint64_t> cnts(kCnt * (size_t)c->world);
+    NC_(c, g_nccl.AllGather(c->d_cnt_send.p, c->d_cnt_recv.p, kMergeCnt, ncclUint64, c->comm, c->stream));
+    std::vector<uint64_t> cnts(kMergeCnt * (size_t)c->world);
     CU(c, cudaMemcpyAsync(cnts.data(), c->d_cnt_recv.p, 8 * cnts.size(), cudaMemcpyDeviceToHost, c->stream));
     CU(c, cudaStreamSynchronize(c->stream));
-    uint64_t maxc = 1, tot = 0;
-    n_cand = n_feas = 0;
-    for (int r = 0; r < c->world; ++r) {
-      maxc = std::max(maxc, cnts[kCnt * r]);
-      tot += cnts[kCnt * r];
-      n_cand += cnts[kCnt * r + 1];
-      n_feas += cnts[kCnt * r + 2];
-    }
+    uint64_t maxc = 1;
+    for (int r = 0; r < c->world; ++r) maxc = std::max(maxc, cnts[kMergeCnt * r]);
     // padded all-gather of local frontiers (32-byte records as bytes)
     if (c->d_local.n < maxc) {
       DevBuf<ppipe_point> tmp;
@@ -1081,85 +1186,9 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
     CU(c, c->d_gather.reserve(maxc * c->world));
     NC_(c, g_nccl.AllGather(c->d_local.p, c->d_gather.p, maxc * sizeof(ppipe_point), ncclUint8, c->comm,
                             c->stream));
-    // pieces in rank order: (model or -1 for a run of whole models, source, count)
-    struct Piece {
-      long long model;
-      uint64_t src, n;
-    };
-    std::vector<Piece> pieces;
-    for (int r = 0; r < c->world; ++r) {
-      const uint64_t* q = &cnts[kCnt * (size_t)r];
-      if (q[4] == 0) continue;  // no rows on rank r
-      const long long f = (long long)q[4] - 1, l = (long long)q[5] - 1;
-      const uint64_t base = (uint64_t)r * maxc, n = q[0];
-      if (f == l) {
-        pieces.push_back({f, base, n});
-      } else {
-        pieces.push_back({f, base, q[6]});
-        pieces.push_back({-1, base + q[6], n - q[6] - q[7]});
-        pieces.push_back({l, base + n - q[7], q[7]});
-      }
-    }
-    // a model with pieces from two or more ranks straddles: re-reduce its points
-    std::vector<char> dirty(pieces.size(), 0);
-    std::vector<long long> straddle;
-    for (size_t i = 0; i < pieces.size(); ++i)
-      for (size_t k = i + 1; k < pieces.size() && pieces[k].model == pieces[i].model && pieces[i].model >= 0; ++k) {
-        dirty[i] = dirty[k] = 1;
-        if (straddle.empty() || straddle.back() != pieces[i].model) straddle.push_back(pieces[i].model);
-      }
-    uint64_t n_dirty = 0;
-    for (size_t i = 0; i < pieces.size(); ++i)
-      if (dirty[i]) n_dirty += pieces[i].n;
-    CU(c, c->d_union.reserve(std::max<uint64_t>(n_dirty, 1)));
-    uint64_t off = 0;
-    for (size_t i = 0; i < pieces.size(); ++i)
-      if (dirty[i] && pieces[i].n) {
-        CU(c, cudaMemcpyAsync(c->d_union.p + off, c->d_gather.p + pieces[i].src, sizeof(ppipe_point) * pieces[i].n,
-                              cudaMemcpyDeviceToDevice, c->stream));
-        off += pieces[i].n;
-      }
-    CU(c, c->d_final.reserve(std::max<uint64_t>(tot, 1)));
-    CU(c, c->d_segoff_final.reserve(c->n_seg_total + 1));
-    CU(c, c->d_merged.reserve(std::max<uint64_t>(n_dirty, 1)));
-    uint64_t n_merged = 0;
-    std::vector<uint64_t> mcount(straddle.size(), 0);
-    if (n_dirty) {
-      CU(c, frontier_pass(c->d_union.p, n_dirty, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_merged.p,
-                          c->d_segoff_final.p, &n_merged, &c->scratch, c->stream, &nl, c->wpack));
-      std::vector<uint64_t> b(2 * straddle.size());
-      for (size_t i = 0; i < straddle.size(); ++i) {
-        CU(c, cudaMemcpyAsync(&b[2 * i], c->d_segoff_final.p + c->h_segbase[straddle[i]], 8,
-                              cudaMemcpyDeviceToHost, c->stream));
-        CU(c, cudaMemcpyAsync(&b[2 * i + 1], c->d_segoff_final.p + c->h_segbase[straddle[i] + 1], 8,
-                              cudaMemcpyDeviceToHost, c->stream));
-      }
-      CU(c, cudaStreamSynchronize(c->stream));
-      for (size_t i = 0; i < straddle.size(); ++i) mcount[i] = b[2 * i + 1] - b[2 * i];
-    }
-    // assemble in order: clean pieces from the gathered frontiers, each straddling
-    // model's merged block in place of its first piece
-    uint64_t w = 0, moff = 0;
-    size_t si = 0;
-    for (size_t i = 0; i < pieces.size(); ++i) {
-      const ppipe_point* src = c->d_gather.p + pieces[i].src;
-      uint64_t n = pieces[i].n;
-      if (dirty[i]) {
-        if (i > 0 && dirty[i - 1] && pieces[i - 1].model == pieces[i].model) continue;
-        src = c->d_merged.p + moff;
-        n = mcount[si];
-        moff += n;
-        ++si;
-      }
-      if (n)
-        CU(c, cudaMemcpyAsync(c->d_final.p + w, src, sizeof(ppipe_point) * n, cudaMemcpyDeviceToDevice, c->stream));
-      w += n;
-    }
-    n_pts = w;
-    CU(c, c->d_segtmp.reserve(std::max<uint64_t>(n_pts, 1)));
-    CU(c, segment_offsets(c->d_final.p, n_pts, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_segoff_final.p,
-                          c->d_segtmp.p, c->stream, &nl));
     nl += 2;  // the two all-gathers
+    rc = merge_assemble(c, cnts, maxc, &nl, &n_cand, &n_feas, &n_pts);
+    if (rc != PPIPE_OK) return rc;
     d_pts = c->d_final.p;
     d_off = c->d_segoff_final.p;
   }
@@ -1185,6 +1214,9 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
   c->res_off = d_off;
   c->res_n = n_pts;
   c->res_ncand = n_cand;
+  c->res_nfeas = n_feas;
+  c->res_nsurv = n_surv;
+  c->res_local = !(c->world > 1 && c->comm);  // a shard's local frontier (ppipe_merge_shards input)
   if (copy_to_host) {
     CU(c, c->h_points.reserve(n_pts));
     CU(c, c->h_segoff.reserve(c->n_seg_total + 1));
@@ -1316,6 +1348,82 @@ static int publish_owned(ppipe_ctx* c, int nl, const ppipe_point* d_pts, const u
   return PPIPE_OK;
 }
 
+PPIPE_API int ppipe_merge_shards(ppipe_ctx* const* shards, int n_shards, int copy_to_host, ppipe_frontier* out) {
+  if (!shards || n_shards < 1 || !out) return fail(nullptr, PPIPE_EINVAL, "ppipe_merge_shards: NULL argument");
+  ppipe_ctx* c = shards[0];
+  if (!c) return fail(nullptr, PPIPE_EINVAL, "ppipe_merge_shards: shard 0 is NULL");
+  for (int r = 0; r < n_shards; ++r) {
+    const ppipe_ctx* x = shards[r];
+    if (!x) return fail(c, PPIPE_EINVAL, "ppipe_merge_shards: shard %d is NULL", r);
+    if (x->world != n_shards || x->rank != r || x->comm)
+      return fail(c, PPIPE_EINVAL, "ppipe_merge_shards: shard %d is rank %d of %d%s; expected rank %d of %d in shard mode",
+                  r, x->rank, x->world, x->comm ? " with NCCL" : "", r, n_shards);
+    if (x->device != c->device || x->n_models != c->n_models || x->C != c->C || x->B != c->B || x->Ms != c->Ms)
+      return fail(c, PPIPE_EINVAL, "ppipe_merge_shards: shard %d was loaded with another device or workload shape", r);
+    if (!x->have_result || !x->res_local)
+      return fail(c, PPIPE_ESTATE, "ppipe_merge_shards: shard %d has no local ppipe_pareto result", r);
+    if (x->last_params.max_partitions != c->last_params.max_partitions ||
+        x->last_params.margin_permille != c->last_params.margin_permille || x->last_slo != c->last_slo ||
+        x->wpack != c->wpack)
+      return fail(c, PPIPE_EINVAL, "ppipe_merge_shards: shard %d was enumerated with other parameters", r);
+  }
+  CU(c, cudaSetDevice(c->device));
+  int nl = 0;
+  CU(c, cudaEventRecord(c->ev[3], c->stream));
+  // the same inputs the NCCL path all-gathers: every shard's counters and its local
+  // frontier, padded to the largest, at d_gather + r * maxc
+  std::vector<uint64_t> cnts(kMergeCnt * (size_t)n_shards);
+  uint64_t maxc = 1;
+  for (int r = 0; r < n_shards; ++r) {
+    ppipe_ctx* x = shards[r];
+    int rc = local_counters(x, x->res_n, x->res_ncand, x->res_nfeas, x->res_nsurv, &cnts[kMergeCnt * (size_t)r]);
+    if (rc != PPIPE_OK) return fail(c, rc, "shard %d: %s", r, x->err.c_str());
+    maxc = std::max(maxc, x->res_n);
+  }
+  CU(c, c->d_gather.reserve(maxc * n_shards));
+  for (int r = 0; r < n_shards; ++r)
+    if (shards[r]->res_n)
+      CU(c, cudaMemcpyAsync(c->d_gather.p + (size_t)r * maxc, shards[r]->res_pts, sizeof(ppipe_point) * shards[r]->res_n,
+                            cudaMemcpyDeviceToDevice, c->stream));
+  uint64_t n_cand = 0, n_feas = 0, n_pts = 0;
+  int rc = merge_assemble(c, cnts, maxc, &nl, &n_cand, &n_feas, &n_pts);
+  if (rc != PPIPE_OK) return rc;
+  CU(c, cudaEventRecord(c->ev[4], c->stream));
+  CU(c, cudaEventSynchronize(c->ev[4]));
+  cudaEventElapsedTime(&c->phase_ms[3], c->ev[3], c->ev[4]);
+  c->launches = (uint64_t)nl;
+  std::memset(out, 0, sizeof *out);
+  out->n_candidates = n_cand;
+  out->n_feasible = n_feas;
+  out->n_points = n_pts;
+  out->n_segments = c->n_seg_total;
+  out->d_points = c->d_final.p;
+  out->d_seg_offsets = c->d_segoff_final.p;
+  out->n_survivors = c->res_nsurv;
+  out->n_candidates_local = c->res_ncand;
+  out->n_feasible_local = c->res_nfeas;
+  c->have_result = true;
+  c->res_local = false;  // now the merged frontier
+  c->res_pts = c->d_final.p;
+  c->res_off = c->d_segoff_final.p;
+  c->res_n = n_pts;
+  c->res_ncand = n_cand;
+  c->res_nfeas = n_feas;
+  if (copy_to_host) {
+    CU(c, c->h_points.reserve(n_pts));
+    CU(c, c->h_segoff.reserve(c->n_seg_total + 1));
+    if (n_pts)
+      CU(c, cudaMemcpyAsync(c->h_points.p, c->d_final.p, sizeof(ppipe_point) * n_pts, cudaMemcpyDeviceToHost,
+                            c->stream));
+    CU(c, cudaMemcpyAsync(c->h_segoff.p, c->d_segoff_final.p, 8 * (c->n_seg_total + 1), cudaMemcpyDeviceToHost,
+                          c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
+    out->points = c->h_points.p;
+    out->seg_offsets = c->h_segoff.p;
+  }
+  return PPIPE_OK;
+}
+
 // Shared prologue of the whole-model paths: parameter checks, owned models, problem setup.
 static int whole_model_setup(ppipe_ctx* c, const ppipe_enum_params* p, const char* who, std::vector<int>* own,
                              Problem* pb) {
@@ -1327,6 +1435,7 @@ static int whole_model_setup(ppipe_ctx* c, const ppipe_enum_params* p, const cha
   owned_models(c, own, who);
   CU(c, cudaSetDevice(c->device));
   c->have_result = false;
+  c->res_local = false;
   c->enumerated = false;
   c->last_params = *p;
   c->last_slo.assign(p->slo_us, p->slo_us + c->n_models);
@@ -1505,6 +1614,7 @@ PPIPE_API int ppipe_set_vgpu(ppipe_ctx* c, const uint8_t* vgpu) {
   c->w_bits = bits;
   c->enumerated = false;
   c->have_result = false;
+  c->res_local = false;
   return PPIPE_OK;
 }
 
