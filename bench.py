@@ -116,6 +116,88 @@ def cpu_baseline(cfg: int, target_s: float = 12.0, cap_s: float = 30.0):
             "sample": f"config {cfg} model(s) {used[0]}..{used[-1]} in full ({cand} candidates, {t_tot:.1f} s)"}
 
 
+def oracle_rate(w, threads: int, target_s: float = 3.0):
+    """The oracle's candidates/s on a workload: in full if that takes under ~target_s,
+    else on a calibrated range of model 0's first-cut rows (row 0 = the K = 1 candidates)."""
+    from oracle import run_oracle
+    t0 = time.perf_counter()
+    if len(w.models) > 1 or w.models[0].n_layers < 64:
+        r = run_oracle(w, threads=threads)
+        return r.n_candidates / (time.perf_counter() - t0), "in full"
+    M = w.models[0].n_layers
+    rows = 4
+    while True:
+        t0 = time.perf_counter()
+        r = run_oracle(w, threads=threads, row_lo=1, row_hi=1 + rows)
+        dt = time.perf_counter() - t0
+        if dt > target_s / 4 or rows >= M - 1:
+            break
+        rows = min(M - 1, rows * 2)
+    if rows < M - 1:
+        rows = max(1, min(M - 1, int(rows * target_s / max(dt, 1e-3))))
+        t0 = time.perf_counter()
+        r = run_oracle(w, threads=threads, row_lo=1, row_hi=1 + rows)
+        dt = time.perf_counter() - t0
+    return r.n_candidates / dt, f"first-cut rows [1, {1 + rows}) of {M - 1}"
+
+
+def per_config_block(pp, local_rank: int, steps: int = 5, with_oracle: bool = True) -> dict:
+    """Configs 1-4 (BASELINE.json configs[0..3]): device-timed candidates/s of one
+    enumerate + pareto step (inputs resident, CUDA events on the library stream), frontier
+    points, and the oracle's single-thread and all-core rates on the host."""
+    import torch
+    from workloads import CONFIG_NAMES, make_config
+    threads = _host_threads()
+    out = {}
+    for cfg in (1, 2, 3, 4):
+        w = make_config(cfg)
+        ctx = pp.load_workload(w, device=local_rank)
+        try:
+            st = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local_rank))
+            for _ in range(2):
+                pp.enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
+                f = pp.pareto(ctx, copy_to_host=False)
+            ms = []
+            for _ in range(steps):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                pp.enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
+                f = pp.pareto(ctx, copy_to_host=False)
+                e1.record(st)
+                e1.synchronize()
+                ms.append(e0.elapsed_time(e1))
+        finally:
+            pp.free(ctx)
+        med = statistics.median(ms)
+        d = {"workload": CONFIG_NAMES[cfg], "candidates": f.n_candidates, "feasible": f.n_feasible,
+             "frontier_points": f.n_points, "ms_per_step": med, "candidates_per_s": f.n_candidates / (med / 1e3)}
+        if with_oracle:
+            r1, s1 = oracle_rate(w, 1)
+            rn, sn = oracle_rate(w, threads)
+            d["oracle_1_thread"] = {"candidates_per_s": r1, "sample": s1}
+            d["oracle_all_cores"] = {"candidates_per_s": rn, "threads": threads, "sample": sn}
+        out[f"config {cfg}"] = d
+    out["timing"] = (f"median of {steps} device-timed enumerate + pareto steps per config (2 warm-up), inputs "
+                     "resident; oracle rates on the host (single thread and all cores, in full or on a "
+                     "calibrated first-cut-row range of the model)")
+    return out
+
+
+def score_profile(config: int):
+    """ncu counters of the score kernels of one config-5 step of this build
+    (profiles/r2_score_ncu.json, written by scripts/profile_score.py from an ncu --set full
+    capture): executed warp-instructions and DRAM bytes per step."""
+    path = os.path.join(ROOT, "profiles", "r2_score_ncu.json")
+    try:
+        pj = json.load(open(path))
+    except Exception:
+        return None
+    if int(pj.get("config", 5)) != config:
+        return None
+    return pj
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle on bounded samples of the same workload."""
     rank = int(os.environ.get("RANK", "0"))
@@ -188,6 +270,7 @@ def main():
     ap.add_argument("--no-pb", action="store_true", help="skip the per-stage batch (App. A.1) measurement")
     ap.add_argument("--models", type=int, default=None, help="config 5 only: first N models (profiling)")
     ap.add_argument("--margin", type=int, default=None, help="override margin_permille (experiments)")
+    ap.add_argument("--no-per-config", action="store_true", help="skip the configs 1-4 block")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -314,15 +397,14 @@ def main():
     achieved = allsum(achieved_local) / world  # per-GPU average of per-launch rates
     # a stricter floor: one compare per candidate + 3 more ops per feasible one
     min_achieved = allsum((f.n_candidates_local + 3 * f.n_feasible_local) / (kern_avg / 1000.0)) / world
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "score_kernel_dram.json")
-    if os.path.exists(prof):
-        try:
-            pj = json.load(open(prof))
-            if int(pj.get("config", 5)) == args.config and not args.models:
-                traffic = pj.get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    # Work-based roofline (the integer-issue ceiling): the score phase's executed
+    # warp-instructions per step (ncu, profiles/r2_score_ncu.json, this build, config 5 at
+    # N = 1; deterministic for the workload) x 32 lanes / the live score-phase time.
+    prof = score_profile(args.config) if (world == 1 and not args.models and args.margin is None) else None
+    traffic = issue = None
+    if prof is not None:
+        traffic = prof["total"]["dram_bytes"]
+        issue = prof["total"]["inst_executed"] * 32 / (kern_max / 1000.0)
     launches_tot = int(allsum(launches))
 
     # ---- e2e: through the public API with HOST buffers, H2D + D2H inside the timed region ----
@@ -442,6 +524,19 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config)
+        g5 = os.path.join(ROOT, "tests", "golden", "config5_oracle.json")
+        if args.config == 5 and os.path.exists(g5):  # the whole config 5 on the oracle (scripts/golden_config5.py)
+            try:
+                gj = json.load(open(g5))
+                cpu["config5_in_full"] = {"oracle_sec": gj["total"]["oracle_sec"], "threads": gj["threads"],
+                                          "host_cores": gj["host_cores"],
+                                          "candidates_per_s": gj["total"]["n_cand"] / gj["total"]["oracle_sec"],
+                                          "source": "tests/golden/config5_oracle.json (build host, not this box)"}
+            except Exception:
+                pass
+    per_cfg = None
+    if world == 1 and not args.no_per_config and args.config == 5 and not args.models:
+        per_cfg = per_config_block(pp, local_rank, with_oracle=not args.no_cpu_baseline)
     from workloads import CONFIG_NAMES
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -453,19 +548,23 @@ def main():
                    "l2": "inputs > L2 (P, Y tables ~1.1 GB at N=1) and a 256 MiB L2 flush between timed steps",
                    "parallelism": f"dp{world}: first-cut-row shards + NCCL all-gather frontier merge"
                    if world > 1 else "dp1"},
-        "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
-                     "frac": achieved / peak_ops, "traffic": traffic,
-                     "kernel": "score_kernel", "kernel_ms": kern_max,
-                     "ops_per_launch": "SURVEY.md §8(d) W: 4 int32 ops per K=2,3 candidate, 2 per K=1 candidate "
-                                       "(DESIGN.md §5); the prefilter decides two candidates per 32-bit lane-op "
-                                       "(16-bit fields) and the tile skip decides whole tiles with one compare, so frac can "
-                                       "exceed the one-candidate-per-op model (issue-active from ncu: "
-                                       "profiles/r1_ncu_summary_v4.md)",
-                     "frac_one_cmp_plus_3_per_feasible": min_achieved / peak_ops,
-                     "issue_active_ncu": {"score3a": 0.534, "score3b": 0.374, "score12": 0.606,
-                                          "source": "smsp__issue_active from ncu --set full of this build "
-                                                    "(profiles/r1_ncu_summary_v4.md); the measured issue side "
-                                                    "of the integer-issue roofline"},
+        "roofline": {"bound": "alu", "achieved": (issue if issue is not None else achieved) / 1e12,
+                     "peak": peak_ops / 1e12, "unit": "Tops/s",
+                     "frac": (issue if issue is not None else achieved) / peak_ops, "traffic": traffic,
+                     "kernel": "score phase (score3a + gfold_prefix + score3b + score12), one step",
+                     "kernel_ms": kern_max,
+                     "achieved_basis": ("executed warp-instructions of the score kernels per step x 32 lanes / the live "
+                                        "score-phase time; instruction and DRAM counts from ncu --set full of this build "
+                                        f"({prof['source']})" if prof is not None else
+                                        "no ncu profile for this configuration: W-model ops (below) instead"),
+                     "issue_frac": (issue / peak_ops) if issue is not None else None,
+                     "per_kernel_ncu": prof["kernels"] if prof is not None else None,
+                     "w_model": {"ops_per_candidate": "SURVEY.md §8(d) W: 4 int32 ops per K=2,3 candidate, 2 per K=1",
+                                 "achieved": achieved / 1e12, "frac": achieved / peak_ops,
+                                 "note": "effective ops/candidate: above 1 because the 16-bit prefilter decides two "
+                                         "candidates per lane-op and the tile bounds decide whole tiles with one "
+                                         "compare, so this does not measure executed work",
+                                 "frac_one_cmp_plus_3_per_feasible": min_achieved / peak_ops},
                      "peak_basis": f"{SM_COUNT} SMs x {ISSUE_LANES_PER_CLK_PER_SM} int lane-ops/clk (issue) x "
                                    f"{f_clk / 1e6:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"},
         "cpu_baseline": cpu,
@@ -477,6 +576,7 @@ def main():
         "prepartition": prepart,
         "f2": f2,
         "per_stage_batch": pbm,
+        "per_config": per_cfg,
     }
     emit_line(line)
     if world > 1:

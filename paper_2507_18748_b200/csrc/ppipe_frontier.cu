@@ -1007,33 +1007,34 @@ __global__ void __launch_bounds__(kFpThreads) fp_stream_kernel(const typename T:
 // ---------------------------------------------------------------------------
 // huge segments, batched: every segment with more than kFpCap items is split by
 // ranges of its primary sort key (E for the staircase; monotone under the order)
-// into nb sub-segments of expected size kFpCap / 2; the sub-segments run through
-// the warp / CTA paths like segments; a fix-up per huge segment walks its
-// sub-segments in order and (staircase) keeps a locally kept item only if its theta
-// also exceeds the maximum theta of every earlier sub-segment.
-// hdesc[2h] = {segment, lo, n, hoff}, hdesc[2h + 1] = {hbase, nb, 0, 0}
+// into nb sub-segments of about kHkTarget items (splitters at the quantiles of a
+// sorted sample); the sub-segments run through the warp / CTA paths like segments;
+// then (staircase) a locally kept item stays only if its theta also exceeds the
+// maximum theta of every earlier sub-segment of its segment, and the sub-segments'
+// kept lists are concatenated in order. Every step is spread over many CTAs:
+// chunks of kHkChunk items for counting and scattering, a CTA per sub-segment for the
+// filter and the gather.
+// hdesc[2h] = {segment, lo, n, hoff}, hdesc[2h + 1] = {hbase, nb, 0, 0};
+// hchunk[c] = {h, first item, end item, 0}.
 // ---------------------------------------------------------------------------
 constexpr uint32_t kHkSample = 2048;    // primary keys sampled per huge segment
 constexpr uint32_t kHkTarget = 512;     // expected items per sub-segment (the medium path)
 constexpr uint32_t kHkMaxSplit = 4096;  // sub-segments per huge segment
+constexpr uint32_t kHkChunk = 4096;     // items per counting / scattering CTA
 
 template <class T>
-__global__ void __launch_bounds__(kFpThreads) hk_count_kernel(const typename T::Item* items, const uint4* hdesc,
-                                                               uint32_t* subcnt, uint2* hsr) {
-  // splitters at the quantiles of a sorted sample of the primary keys: sub-segment
-  // b holds the items with spl[b-1] <= key < spl[b] (equal keys share a sub-segment)
+__global__ void __launch_bounds__(kFpThreads) hk_split_kernel(const typename T::Item* items, const uint4* hdesc,
+                                                               uint32_t* spl, uint32_t* sub2h) {
   __shared__ uint32_t smp[kHkSample];
-  __shared__ uint32_t spl[kHkMaxSplit];
   const uint4 d0 = hdesc[2 * blockIdx.x], d1 = hdesc[2 * blockIdx.x + 1];
-  const uint32_t lo = d0.y, n = d0.z, hoff = d0.w, hbase = d1.x, nb = min(d1.y, (uint32_t)kHkMaxSplit);
-  const int lane = threadIdx.x & 31;
+  const uint32_t lo = d0.y, n = d0.z, hbase = d1.x, nb = d1.y;
   for (uint32_t t = threadIdx.x; t < kHkSample; t += blockDim.x)
     smp[t] = T::primary(items[lo + (uint32_t)((uint64_t)t * n / kHkSample)]);
   __syncthreads();
   for (uint32_t k = 2; k <= kHkSample; k <<= 1) {
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
       for (uint32_t t = threadIdx.x; t < kHkSample / 2; t += blockDim.x) {
-        const uint32_t i = 2 * j * (t / j) + (t % j), l = i + j;
+        const uint32_t i = ((t & ~(j - 1)) << 1) | (t & (j - 1)), l = i + j;
         const uint32_t a = smp[i], b = smp[l];
         if (((i & k) == 0) ? (b < a) : (a < b)) {
           smp[i] = b;
@@ -1043,11 +1044,27 @@ __global__ void __launch_bounds__(kFpThreads) hk_count_kernel(const typename T::
       __syncthreads();
     }
   }
-  for (uint32_t b = threadIdx.x; b + 1 < nb; b += blockDim.x) spl[b] = smp[(uint32_t)((uint64_t)(b + 1) * kHkSample / nb)];
+  // sub-segment b holds the keys with spl[b-1] <= key < spl[b] (equal keys share one)
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
+    if (b + 1 < nb) spl[hbase + b] = smp[(uint32_t)((uint64_t)(b + 1) * kHkSample / nb)];
+    sub2h[hbase + b] = blockIdx.x;
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kFpThreads) hk_count_kernel(const typename T::Item* items, const uint4* hdesc,
+                                                               const uint4* hchunk, const uint32_t* spl_g,
+                                                               uint32_t* subcnt, uint2* hsr) {
+  __shared__ uint32_t spl[kHkMaxSplit];
+  const uint4 ch = hchunk[blockIdx.x];
+  const uint4 d0 = hdesc[2 * ch.x], d1 = hdesc[2 * ch.x + 1];
+  const uint32_t lo = d0.y, hoff = d0.w, hbase = d1.x, nb = d1.y;
+  const int lane = threadIdx.x & 31;
+  for (uint32_t b = threadIdx.x; b + 1 < nb; b += blockDim.x) spl[b] = spl_g[hbase + b];
   __syncthreads();
-  for (uint32_t i0 = threadIdx.x & ~31u; i0 < n; i0 += blockDim.x) {
+  for (uint32_t i0 = ch.y + (threadIdx.x & ~31u); i0 < ch.z; i0 += blockDim.x) {
     const uint32_t i = i0 + lane;
-    const bool valid = i < n;
+    const bool valid = i < ch.z;
     uint32_t sub = 0xffffffffu;
     if (valid) {
       const uint32_t key = T::primary(items[lo + i]);
@@ -1070,12 +1087,13 @@ __global__ void __launch_bounds__(kFpThreads) hk_count_kernel(const typename T::
 
 template <class T>
 __global__ void __launch_bounds__(kFpThreads) hk_scatter_kernel(const typename T::Item* items, const uint32_t* idx,
-                                                                 const uint4* hdesc, const uint2* hsr,
-                                                                 const uint64_t* substart,
+                                                                 const uint4* hdesc, const uint4* hchunk,
+                                                                 const uint2* hsr, const uint64_t* substart,
                                                                  typename T::Item* hitems, uint32_t* hidx) {
-  const uint4 d0 = hdesc[2 * blockIdx.x];
-  const uint32_t lo = d0.y, n = d0.z, hoff = d0.w;
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+  const uint4 ch = hchunk[blockIdx.x];
+  const uint4 d0 = hdesc[2 * ch.x];
+  const uint32_t lo = d0.y, hoff = d0.w;
+  for (uint32_t i = ch.y + threadIdx.x; i < ch.z; i += blockDim.x) {
     const uint2 sr = hsr[hoff + i];
     const uint64_t pos = substart[sr.x] + sr.y;
     hitems[pos] = items[lo + i];
@@ -1083,64 +1101,113 @@ __global__ void __launch_bounds__(kFpThreads) hk_scatter_kernel(const typename T
   }
 }
 
+// thread per huge segment, over its sub-segments in order: pre[sub] = the maximum theta
+// of every earlier sub-segment of the segment (staircase only)
 template <class T>
-__global__ void __launch_bounds__(kFpThreads) hk_fixup_kernel(const typename T::Rec* in, typename T::Params q,
-                                                               const uint4* hdesc, const uint64_t* substart,
-                                                               const uint32_t* hkept, const uint32_t* kc_sub,
-                                                               const typename T::Th* tmax_sub, uint32_t* kept,
-                                                               uint32_t* kc) {
-  using Th = typename T::Th;
-  __shared__ uint32_t wk[kFpThreads / 32];
-  const uint4 d0 = hdesc[2 * blockIdx.x], d1 = hdesc[2 * blockIdx.x + 1];
-  const uint32_t seg = d0.x, lo = d0.y, hbase = d1.x, nb = d1.y;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  Th prefix = T::zero();
-  uint32_t count = 0;
-  for (uint32_t b = 0; b < nb; ++b) {
-    const uint32_t sub = hbase + b, k = kc_sub[sub];
-    const uint64_t base = substart[sub];
-    for (uint32_t t0 = 0; t0 < k; t0 += blockDim.x) {
-      const uint32_t j = t0 + threadIdx.x;
-      const bool valid = j < k;
-      const uint32_t r = valid ? hkept[base + j] : 0u;
-      bool keep = valid;
-      if constexpr (T::kMode == kStaircase)
-        if (valid) keep = T::gt(T::theta(T::item_of(in[r], q)), prefix);
-      const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      if (lane == 0) wk[warp] = __popc(bal);
-      __syncthreads();
-      uint32_t off = count, tot = 0;
-      for (int w = 0; w < nw; ++w) {
-        if (w < warp) off += wk[w];
-        tot += wk[w];
-      }
-      if (keep) kept[lo + off + __popc(bal & lanemask_lt_())] = r;
-      count += tot;
-      __syncthreads();
-    }
-    if constexpr (T::kMode == kStaircase) {
-      const Th t = tmax_sub[sub];
-      if (T::gt(t, prefix)) prefix = t;
-    }
+__global__ void hk_pre_kernel(const uint4* hdesc, uint32_t nh, const typename T::Th* tmax_sub,
+                              typename T::Th* pre) {
+  const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= nh) return;
+  const uint4 d1 = hdesc[2 * h + 1];
+  typename T::Th run = T::zero();
+  for (uint32_t b = 0; b < d1.y; ++b) {
+    pre[d1.x + b] = run;
+    const typename T::Th t = tmax_sub[d1.x + b];
+    if (T::gt(t, run)) run = t;
   }
-  if (threadIdx.x == 0) kc[seg] = count;
+}
+
+// CTA per sub-segment: keep the locally kept items whose theta exceeds pre[sub]
+// (staircase; other modes keep all), compacted in place; fcnt[sub] = how many
+template <class T>
+__global__ void __launch_bounds__(128) hk_filter_kernel(const typename T::Rec* in, typename T::Params q,
+                                                        const uint64_t* substart, uint32_t* hkept,
+                                                        const uint32_t* kc_sub, const typename T::Th* pre,
+                                                        uint32_t* fcnt) {
+  __shared__ uint32_t wk[4];
+  const uint32_t sub = blockIdx.x, k = kc_sub[sub];
+  const uint64_t base = substart[sub];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t count = 0;
+  for (uint32_t t0 = 0; t0 < k; t0 += blockDim.x) {
+    const uint32_t j = t0 + threadIdx.x;
+    const bool valid = j < k;
+    const uint32_t r = valid ? hkept[base + j] : 0u;
+    bool keep = valid;
+    if constexpr (T::kMode == kStaircase)
+      if (valid) keep = T::gt(T::theta(T::item_of(in[r], q)), pre[sub]);
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wk[warp] = __popc(bal);
+    __syncthreads();  // every read of this tile precedes its writes (write index <= read index)
+    uint32_t off = count, tot = 0;
+    for (int w = 0; w < 4; ++w) {
+      if (w < warp) off += wk[w];
+      tot += wk[w];
+    }
+    if (keep) hkept[base + off + __popc(bal & lanemask_lt_())] = r;
+    count += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) fcnt[sub] = count;
+}
+
+// thread per huge segment: output offsets of its sub-segments and the segment's count
+__global__ void hk_offsets_kernel(const uint4* hdesc, uint32_t nh, const uint32_t* fcnt, uint32_t* suboff,
+                                  uint32_t* kc) {
+  const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= nh) return;
+  const uint4 d0 = hdesc[2 * h], d1 = hdesc[2 * h + 1];
+  uint32_t run = 0;
+  for (uint32_t b = 0; b < d1.y; ++b) {
+    suboff[d1.x + b] = run;
+    run += fcnt[d1.x + b];
+  }
+  kc[d0.x] = run;
+}
+
+// CTA per sub-segment: its filtered list into the segment's kept range
+__global__ void __launch_bounds__(128) hk_gather_kernel(const uint4* hdesc, const uint32_t* sub2h,
+                                                        const uint64_t* substart, const uint32_t* hkept,
+                                                        const uint32_t* fcnt, const uint32_t* suboff,
+                                                        uint32_t* kept) {
+  const uint32_t sub = blockIdx.x;
+  const uint32_t lo = hdesc[2 * sub2h[sub]].y, n = fcnt[sub];
+  const uint64_t src = substart[sub];
+  uint32_t* dst = kept + lo + suboff[sub];
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = hkept[src + i];
 }
 
 // ---------------------------------------------------------------------------
-// 8. compaction: warp per segment
+// 8. compaction: CTA per chunk of kFpThreads output records (thread per record), so a
+// few very large segments do not serialise; the chunk's first segment comes from one
+// binary search over the output CSR, each thread walks forward from it
 // ---------------------------------------------------------------------------
 template <class T, class Rec = typename T::Rec>
 __global__ void __launch_bounds__(kFpThreads) fp_compact_kernel(const Rec* in, const uint32_t* kept,
                                                                  const uint64_t* start, const uint64_t* out_off,
                                                                  uint64_t n_seg, Rec* out) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t s = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (s >= n_seg) return;
-  const uint64_t src = start[s], dst = out_off[s], n = out_off[s + 1] - dst;
-  for (uint64_t k = lane; k < n; k += 32) {
-    Rec r = in[kept[src + k]];
-    T::finalize(r);
-    out[dst + k] = r;
+  __shared__ uint64_t s0;
+  const uint64_t total = out_off[n_seg];
+  for (uint64_t c0 = (uint64_t)blockIdx.x * blockDim.x; c0 < total; c0 += (uint64_t)gridDim.x * blockDim.x) {
+    if (threadIdx.x == 0) {
+      uint64_t lo = 0, hi = n_seg;  // last segment with out_off[s] <= c0
+      while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (out_off[mid] <= c0) lo = mid;
+        else hi = mid;
+      }
+      s0 = lo;
+    }
+    __syncthreads();
+    const uint64_t i = c0 + threadIdx.x;
+    if (i < total) {
+      uint64_t sg = s0;
+      while (out_off[sg + 1] <= i) ++sg;
+      Rec r = in[kept[start[sg] + (i - out_off[sg])]];
+      T::finalize(r);
+      out[i] = r;
+    }
+    __syncthreads();
   }
 }
 
@@ -1252,12 +1319,13 @@ cudaError_t frontier_generic(const typename T::Rec* in, uint64_t n, const uint64
   const uint64_t sub_tiles = (max_sub + kScanTile - 1) / kScanTile + 1;
   struct Arrays {
     uint32_t *cnt, *idx, *kept, *kc, *large, *posA, *posB, *hidx, *hkept, *subcnt, *kc_sub, *large2;
+    uint32_t *spl, *sub2h, *fcnt, *suboff;
     uint64_t *start, *partial, *substart;
     uint2 *segrank, *hsr;
     Item *items, *hitems;
     unsigned long long *ctr, *ctr2;
-    uint4 *huge, *huge2, *hdesc;
-    Th* tmax_sub;
+    uint4 *huge, *huge2, *hdesc, *hchunk;
+    Th *tmax_sub, *pre_sub;
   } A;
   auto layout = [&](Scratch& sc) {
     A.cnt = sc.take<uint32_t>(n_seg + 1);
@@ -1277,6 +1345,12 @@ cudaError_t frontier_generic(const typename T::Rec* in, uint64_t n, const uint64
     A.substart = sc.take<uint64_t>(max_sub + 1);
     A.kc_sub = sc.take<uint32_t>(max_sub + 1);
     A.tmax_sub = sc.take<Th>(max_sub + 1);
+    A.pre_sub = sc.take<Th>(max_sub + 1);
+    A.spl = sc.take<uint32_t>(max_sub + 1);
+    A.sub2h = sc.take<uint32_t>(max_sub + 1);
+    A.fcnt = sc.take<uint32_t>(max_sub + 1);
+    A.suboff = sc.take<uint32_t>(max_sub + 1);
+    A.hchunk = sc.take<uint4>(n / kHkChunk + max_huge + 1);
     A.large2 = sc.take<uint32_t>(2 * (max_sub + 1));
     A.huge2 = sc.take<uint4>(max_sub + 1);
     A.hsr = sc.take<uint2>(n);
@@ -1350,22 +1424,30 @@ cudaError_t frontier_generic(const typename T::Rec* in, uint64_t n, const uint64
     uint32_t split = 0;
     if (const char* v = getenv("PPIPE_FP_SPLIT")) split = (uint32_t)atoi(v);
     uint32_t hoff = 0, hbase = 0;
+    std::vector<uint4> hc;
     for (uint32_t h = 0; h < nh; ++h) {
       const uint32_t m = hl[h].z, nb = std::min<uint32_t>(kHkMaxSplit, split ? split : (m + kHkTarget - 1) / kHkTarget);
       hd[2 * h] = make_uint4(hl[h].x, hl[h].y, m, hoff);
       hd[2 * h + 1] = make_uint4(hbase, nb, 0, 0);
+      for (uint32_t i0 = 0; i0 < m; i0 += kHkChunk) hc.push_back(make_uint4(h, i0, std::min(m, i0 + kHkChunk), 0));
       hoff += m;
       hbase += nb;
     }
     const uint64_t S = hbase;
+    const unsigned nchunk = (unsigned)hc.size();
     if ((e = cudaMemcpyAsync(A.hdesc, hd.data(), sizeof(uint4) * hd.size(), cudaMemcpyHostToDevice, s)) !=
         cudaSuccess)
       return e;
+    if ((e = cudaMemcpyAsync(A.hchunk, hc.data(), sizeof(uint4) * hc.size(), cudaMemcpyHostToDevice, s)) !=
+        cudaSuccess)
+      return e;
     if ((e = cudaMemsetAsync(A.subcnt, 0, sizeof(uint32_t) * (S + 1), s)) != cudaSuccess) return e;
-    hk_count_kernel<T><<<nh, kFpThreads, 0, s>>>(A.items, A.hdesc, A.subcnt, A.hsr);
-    ++*n_launches;
+    hk_split_kernel<T><<<nh, kFpThreads, 0, s>>>(A.items, A.hdesc, A.spl, A.sub2h);
+    hk_count_kernel<T><<<nchunk, kFpThreads, 0, s>>>(A.items, A.hdesc, A.hchunk, A.spl, A.subcnt, A.hsr);
+    *n_launches += 2;
     if ((e = scan_counts(A.subcnt, S, A.substart, A.partial, s, n_launches)) != cudaSuccess) return e;
-    hk_scatter_kernel<T><<<nh, kFpThreads, 0, s>>>(A.items, A.idx, A.hdesc, A.hsr, A.substart, A.hitems, A.hidx);
+    hk_scatter_kernel<T><<<nchunk, kFpThreads, 0, s>>>(A.items, A.idx, A.hdesc, A.hchunk, A.hsr, A.substart,
+                                                       A.hitems, A.hidx);
     ++*n_launches;
     const Level<T> L2{A.hitems, A.hidx, A.substart, S, A.hkept, A.kc_sub, A.tmax_sub, A.large2, A.huge2, A.ctr2};
     if ((e = launch_level(L2, s, n_launches)) != cudaSuccess) return e;
@@ -1386,16 +1468,21 @@ cudaError_t frontier_generic(const typename T::Rec* in, uint64_t n, const uint64
                                     A.kc_sub + d.x, A.tmax_sub + d.x, s, n_launches)) != cudaSuccess)
           return e;
     }
-    hk_fixup_kernel<T><<<nh, kFpThreads, 0, s>>>(in, q, A.hdesc, A.substart, A.hkept, A.kc_sub, A.tmax_sub, A.kept,
-                                                 A.kc);
-    ++*n_launches;
+    if constexpr (T::kMode == kStaircase) {
+      hk_pre_kernel<T><<<(nh + 127) / 128, 128, 0, s>>>(A.hdesc, nh, A.tmax_sub, A.pre_sub);
+      ++*n_launches;
+    }
+    hk_filter_kernel<T><<<(unsigned)S, 128, 0, s>>>(in, q, A.substart, A.hkept, A.kc_sub, A.pre_sub, A.fcnt);
+    hk_offsets_kernel<<<(nh + 127) / 128, 128, 0, s>>>(A.hdesc, nh, A.fcnt, A.suboff, A.kc);
+    hk_gather_kernel<<<(unsigned)S, 128, 0, s>>>(A.hdesc, A.sub2h, A.substart, A.hkept, A.fcnt, A.suboff, A.kept);
+    *n_launches += 3;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   mark(4);
   if ((e = scan_counts(A.kc, n_seg, seg_offsets, A.partial, s, n_launches)) != cudaSuccess) return e;
   if (n && n_seg) {
-    fp_compact_kernel<T><<<(unsigned)((n_seg * 32 + kFpThreads - 1) / kFpThreads), kFpThreads, 0, s>>>(
-        in, A.kept, A.start, seg_offsets, n_seg, out);
+    fp_compact_kernel<T><<<(unsigned)std::min<uint64_t>((n + kFpThreads - 1) / kFpThreads, 148 * 16), kFpThreads, 0,
+                           s>>>(in, A.kept, A.start, seg_offsets, n_seg, out);
     ++*n_launches;
   }
   uint64_t nk = 0;
