@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kPbThreads) pb_score_kernel(Problem pb, int ml
 // only the prefix of b_1 with A1 <= T - A2 - C3 (the feasible ones): the work is
 // O(pairs + feasible candidates) instead of O(candidates), with no division or global
 // load per candidate.
-__global__ void __launch_bounds__(kPbThreads) pb_score3_kernel(Problem pb, int ml, PbOut out) {
+__global__ void __launch_bounds__(kPbThreads, 4) pb_score3_kernel(Problem pb, int ml, PbOut out) {
   __shared__ unsigned long long tab[kPbBuckets];
   __shared__ unsigned long long scan_sh[kPbThreads / 32];
   __shared__ int32_t sA1[256];
