@@ -378,6 +378,15 @@ def main():
 
     phase_avg = {k: allmax(sum(p[i] for p in phases) / len(phases))
                  for i, k in enumerate(["pack", "score", "frontier", "merge"])}
+    # per-rank phase breakdown: where a missed scaling target goes
+    mine = [sum(p[i] for p in phases) / len(phases) for i in range(4)] + [sum(step_ms) / len(step_ms)]
+    if world > 1:
+        t = torch.tensor(mine, dtype=torch.float64, device=dev)
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        per_rank = [[round(float(x), 3) for x in a.tolist()] for a in allt]
+    else:
+        per_rank = [[round(x, 3) for x in mine]]
     total_ms = allmax(sum(step_ms))
     ms_per_step = total_ms / args.steps
     n_cand = f.n_candidates
@@ -572,6 +581,8 @@ def main():
         "gpu_launches": launches_tot,
         "clocks": clocks,
         "phase_ms": phase_avg,
+        "phase_ms_per_rank": {"columns": ["pack", "score", "frontier", "merge", "step"], "ranks": per_rank,
+                              "note": "merge includes waiting for the slowest rank at the first all-gather"},
         "slo_sweep": sweep,
         "prepartition": prepart,
         "f2": f2,

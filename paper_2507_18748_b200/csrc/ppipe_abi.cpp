@@ -1187,8 +1187,25 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
     NC_(c, g_nccl.AllGather(c->d_local.p, c->d_gather.p, maxc * sizeof(ppipe_point), ncclUint8, c->comm,
                             c->stream));
     nl += 2;  // the two all-gathers
+    const char* dbgs = getenv("PPIPE_DEBUG_FLAGS");
+    const bool dbg = dbgs && (atoi(dbgs) & 32);
+    cudaEvent_t mev[2] = {};
+    if (dbg) {
+      for (auto& x : mev) cudaEventCreate(&x);
+      cudaEventRecord(mev[0], c->stream);
+    }
     rc = merge_assemble(c, cnts, maxc, &nl, &n_cand, &n_feas, &n_pts);
     if (rc != PPIPE_OK) return rc;
+    if (dbg) {
+      cudaEventRecord(mev[1], c->stream);
+      cudaEventSynchronize(mev[1]);
+      float a = 0, b = 0;
+      cudaEventElapsedTime(&a, c->ev[3], mev[0]);
+      cudaEventElapsedTime(&b, mev[0], mev[1]);
+      fprintf(stderr, "ppipe merge rank %d: counters + all-gathers %.3f ms, assemble %.3f ms (maxc %llu)\n", c->rank,
+              a, b, (unsigned long long)maxc);
+      for (auto& x : mev) cudaEventDestroy(x);
+    }
     d_pts = c->d_final.p;
     d_off = c->d_segoff_final.p;
   }

@@ -1201,8 +1201,19 @@ __global__ void __launch_bounds__(kFpThreads) fp_compact_kernel(const Rec* in, c
     __syncthreads();
     const uint64_t i = c0 + threadIdx.x;
     if (i < total) {
-      uint64_t sg = s0;
-      while (out_off[sg + 1] <= i) ++sg;
+      // galloping search from s0 for the segment holding i: a few steps for the usual
+      // short distance, log steps across long runs of empty segments
+      uint64_t sg = s0, step = 1;
+      while (sg + step < n_seg && out_off[sg + step + 1] <= i) {
+        sg += step;
+        step <<= 1;
+      }
+      uint64_t hi = min(sg + step, n_seg - 1);  // out_off[hi + 1] > i
+      while (sg < hi) {  // last s in [sg, hi] with out_off[s] <= i
+        const uint64_t mid = (sg + hi + 1) >> 1;
+        if (out_off[mid] <= i) sg = mid;
+        else hi = mid - 1;
+      }
       Rec r = in[kept[start[sg] + (i - out_off[sg])]];
       T::finalize(r);
       out[i] = r;
