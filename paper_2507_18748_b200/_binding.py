@@ -162,22 +162,41 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+# ppipe_model as a numpy record (u32 n_layers, 4 bytes padding, two pointers): the array
+# of descriptors is built without one ctypes object per model
+_MODEL_REC = np.dtype([("n_layers", "<u4"), ("pad", "<u4"), ("lat_us", "<u8"), ("act_bytes", "<u8")])
+assert _MODEL_REC.itemsize == ct.sizeof(_Model)
+
+
 def _models_array(lat_us, act_bytes, n_classes=None, n_batches=None):
     n = len(lat_us)
-    models = (_Model * n)()
-    keep = []
+    if len(act_bytes) != n:
+        raise PPipeError(PPIPE_EINVAL, f"{n} latency arrays but {len(act_bytes)} act_bytes arrays")
+    rec = np.zeros(max(n, 1), dtype=_MODEL_REC)
+    keep = [rec]
+    nl, pl, ps = [0] * n, [0] * n, [0] * n
     for i in range(n):
-        lat = np.ascontiguousarray(lat_us[i], dtype=np.uint32)
-        S = np.ascontiguousarray(act_bytes[i], dtype=np.uint64)
-        if lat.ndim != 3 or (n_classes is not None and lat.shape[0] != n_classes) or \
-                (n_batches is not None and lat.shape[2] != n_batches) or S.shape != (lat.shape[1],):
+        lat, S = lat_us[i], act_bytes[i]
+        if type(lat) is not np.ndarray or lat.dtype != np.uint32 or not lat.flags.c_contiguous:
+            lat = np.ascontiguousarray(lat, dtype=np.uint32)
+            keep.append(lat)
+        if type(S) is not np.ndarray or S.dtype != np.uint64 or not S.flags.c_contiguous:
+            S = np.ascontiguousarray(S, dtype=np.uint64)
+            keep.append(S)
+        sh = lat.shape
+        if len(sh) != 3 or (n_classes is not None and sh[0] != n_classes) or \
+                (n_batches is not None and sh[2] != n_batches) or S.shape != (sh[1],):
             raise PPipeError(PPIPE_EINVAL, f"model {i}: lat_us must be [n_classes][n_layers][n_batches] and "
-                                           f"act_bytes [n_layers]; got {lat.shape} and {S.shape}")
-        keep += [lat, S]
-        models[i].n_layers = lat.shape[1]
-        models[i].lat_us = _u32p(lat)
-        models[i].act_bytes = S.ctypes.data_as(ct.POINTER(ct.c_uint64))
-    return models, keep
+                                           f"act_bytes [n_layers]; got {sh} and {S.shape}")
+        nl[i] = sh[1]
+        pl[i] = lat.__array_interface__["data"][0]
+        ps[i] = S.__array_interface__["data"][0]
+    if n:
+        rec["n_layers"][:n] = nl
+        rec["lat_us"][:n] = pl
+        rec["act_bytes"][:n] = ps
+    keep += [lat_us, act_bytes]
+    return ct.cast(rec.ctypes.data, ct.POINTER(_Model)), keep
 
 
 def update_profiles(ctx: Context, lat_us: Sequence[np.ndarray], act_bytes: Sequence[np.ndarray]) -> None:

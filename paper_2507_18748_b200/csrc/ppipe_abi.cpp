@@ -229,12 +229,14 @@ struct ppipe_ctx {
   // ppipe_update_profiles_async: host descriptors whose copy the next enumerate
   // issues in chunks on cstream, overlapped with scoring earlier chunks
 #ifndef PPIPE_MAX_CHUNKS
-#define PPIPE_MAX_CHUNKS 4  // measured: 4 chunks 126.9 ms e2e, 6: 127.1, 8: 128.5, 16: 143, 32: 205
+#define PPIPE_MAX_CHUNKS 4  // chunk events (the async upload uses 4 geometric chunks)
 #endif
   static constexpr int kMaxChunks = PPIPE_MAX_CHUNKS;
   bool pending_upload = false, check_err = false;
   std::vector<ppipe_model> pending;
   cudaStream_t cstream = nullptr;
+  cudaStream_t stream2 = nullptr;  // second compute stream: consecutive chunks' score3a overlap (no tail gaps)
+  cudaEvent_t sev[2] = {};         // fork / join between stream and stream2
   cudaEvent_t cev[kMaxChunks + 1] = {};
   DevBuf<unsigned long long> d_err;
   // F2 (ppipe_pareto_f2)
@@ -316,6 +318,9 @@ void free_ctx(ppipe_ctx* c) {
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->cstream) cudaStreamDestroy(c->cstream);
+  if (c->stream2) cudaStreamDestroy(c->stream2);
+  for (auto& e : c->sev)
+    if (e) cudaEventDestroy(e);
   for (auto& e : c->cev)
     if (e) cudaEventDestroy(e);
   c->d_err.release();
@@ -605,6 +610,15 @@ PPIPE_API int ppipe_load_profiles(ppipe_ctx** out, uint32_t n_models, const ppip
       fail(c, PPIPE_ECUDA, "cudaEventCreate failed");
       return bail(PPIPE_ECUDA);
     }
+  if (cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess) {
+    fail(c, PPIPE_ECUDA, "cudaStreamCreate failed");
+    return bail(PPIPE_ECUDA);
+  }
+  for (auto& e : c->sev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      fail(c, PPIPE_ECUDA, "cudaEventCreate failed");
+      return bail(PPIPE_ECUDA);
+    }
   if (cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking) != cudaSuccess) {
     fail(c, PPIPE_ECUDA, "cudaStreamCreate failed");
     return bail(PPIPE_ECUDA);
@@ -890,40 +904,68 @@ static int run_enumerate(ppipe_ctx* c) {
     c->check_err = true;
   }
   if (c->pending_upload) {
-    // Chunked pipeline: the copy stream uploads chunk i + 1 while the compute stream
-    // validates, packs and scores (score3a) chunk i; score3b / score12 follow once.
-    const int nch = std::min<int>(ppipe_ctx::kMaxChunks, pb.n_local);
+    // Chunked pipeline: chunk i is uploaded on the copy stream and, as soon as it lands, validated, packed and scored (score3a) on the compute
+    // stream while chunk i + 1 uploads; score3b / score12 follow once. Chunks grow
+    // geometrically (1/16, 3/16, 1/4, 1/2 of the bytes; local models are heavy-first), so
+    // the upload nobody overlaps is the small first one, and the work for chunk i covers
+    // the upload of chunk i + 1. Launches for a chunk are issued right after its copies,
+    // so the GPU starts scoring while the host still issues later chunks.
     CU(c, c->d_err.reserve(1));
     const unsigned long long none = ~0ull;
     CU(c, cudaMemcpyAsync(c->d_err.p, &none, 8, cudaMemcpyHostToDevice, c->stream));
+    CU(c, cudaEventRecord(c->ev[0], c->stream));
     CU(c, cudaEventRecord(c->cev[ppipe_ctx::kMaxChunks], c->stream));  // earlier readers of the buffers
     CU(c, cudaStreamWaitEvent(c->cstream, c->cev[ppipe_ctx::kMaxChunks], 0));
-    std::vector<int> lo(nch + 1);
-    for (int ch = 0; ch <= nch; ++ch) lo[ch] = (int)((int64_t)pb.n_local * ch / nch);
+    CU(c, cudaMemsetAsync(c->d_counters.p, 0, 16 * sizeof(unsigned long long), c->stream));
+    CU(c, cudaEventRecord(c->sev[0], c->stream));  // fork: stream2 after the resets
+    CU(c, cudaStreamWaitEvent(c->stream2, c->sev[0], 0));
+    // chunk boundaries at cumulative byte fractions
+    std::vector<uint64_t> cum(pb.n_local + 1, 0);
+    for (int i = 0; i < pb.n_local; ++i)
+      cum[i + 1] = cum[i] + sizeof(uint32_t) * (uint64_t)c->C * c->h_models[i].M * c->B + 8ull * c->h_models[i].M;
+    static const double kFrac[4] = {1.0 / 16, 4.0 / 16, 8.0 / 16, 1.0};
+    std::vector<int> lo(1, 0);
+    for (int k = 0; k < 4 && lo.back() < pb.n_local; ++k) {
+      int e = k == 3 ? pb.n_local : (int)(std::lower_bound(cum.begin(), cum.end(), (uint64_t)(kFrac[k] * cum.back())) - cum.begin());
+      e = std::max(e, lo.back() + 1);
+      e = std::min(e, pb.n_local);
+      lo.push_back(e);
+    }
+    const int nch = (int)lo.size() - 1;
+    const uint64_t bmax = c->h_batches[c->B - 1];
+    std::vector<void*> dsts, srcs;
+    std::vector<size_t> sizes;
     for (int ch = 0; ch < nch; ++ch) {
+      dsts.clear();
+      srcs.clear();
+      sizes.clear();
       for (int i = lo[ch]; i < lo[ch + 1]; ++i) {
         const int m = c->local[i];
         const DevModel& d = c->h_models[i];
-        CU(c, cudaMemcpyAsync(c->d_lat.p + d.lat_off, c->pending[m].lat_us, sizeof(uint32_t) * c->C * d.M * c->B,
-                              cudaMemcpyHostToDevice, c->cstream));
-        CU(c, cudaMemcpyAsync(c->d_s.p + d.s_off, c->pending[m].act_bytes, sizeof(uint64_t) * d.M,
-                              cudaMemcpyHostToDevice, c->cstream));
+        dsts.push_back(c->d_lat.p + d.lat_off);
+        srcs.push_back(const_cast<uint32_t*>(c->pending[m].lat_us));
+        sizes.push_back(sizeof(uint32_t) * c->C * d.M * c->B);
+        dsts.push_back(c->d_s.p + d.s_off);
+        srcs.push_back(const_cast<uint64_t*>(c->pending[m].act_bytes));
+        sizes.push_back(sizeof(uint64_t) * d.M);
       }
+      for (size_t k = 0; k < dsts.size(); ++k)
+        CU(c, cudaMemcpyAsync(dsts[k], srcs[k], sizes[k], cudaMemcpyHostToDevice, c->cstream));
       CU(c, cudaEventRecord(c->cev[ch], c->cstream));
-    }
-    CU(c, cudaEventRecord(c->ev[0], c->stream));
-    CU(c, cudaMemsetAsync(c->d_counters.p, 0, 16 * sizeof(unsigned long long), c->stream));
-    const uint64_t bmax = c->h_batches[c->B - 1];
-    for (int ch = 0; ch < nch; ++ch) {
-      CU(c, cudaStreamWaitEvent(c->stream, c->cev[ch], 0));
+      // chunks alternate between the two compute streams (independent models; every shared
+      // output is appended through atomics), so one chunk's score3a tail overlaps the next
+      const cudaStream_t cs = (ch & 1) ? c->stream2 : c->stream;
+      CU(c, cudaStreamWaitEvent(cs, c->cev[ch], 0));
       pb.model_base = lo[ch];
       pb.n_chunk = lo[ch + 1] - lo[ch];
       CU(c, launch_validate(c->d_models.p + lo[ch], pb.n_chunk, c->d_lat.p, c->d_s.p, (int)c->C, (int)c->B,
-                            (uint64_t)INT64_MAX / (8 * bmax), c->d_err.p, c->stream));
-      CU(c, launch_pack(pb, c->stream));
-      CU(c, launch_score_part(pb, so, c->stream, &c->launches_i, 1));
+                            (uint64_t)INT64_MAX / (8 * bmax), c->d_err.p, cs));
+      CU(c, launch_pack(pb, cs));
+      CU(c, launch_score_part(pb, so, cs, &c->launches_i, 1));
       c->launches_i += 1 + pack_launches(pb);
     }
+    CU(c, cudaEventRecord(c->sev[1], c->stream2));  // join
+    CU(c, cudaStreamWaitEvent(c->stream, c->sev[1], 0));
     CU(c, cudaEventRecord(c->ev[1], c->stream));  // phase 0 = upload + pack + score3a, interleaved
     pb.model_base = 0;
     pb.n_chunk = pb.n_local;
