@@ -520,6 +520,7 @@ __device__ __forceinline__ void band_hits(const int (&thr)[kJ1][NC], const int4&
 // each exist once in the code (one pass-generic instance).
 // Pass-2 per-warp slot data: the dense survivor pass reads any lane's slot.
 struct SlotData {
+  const uint32_t* rowoff;  // pass 2: [2 NC] offsets of P[k1][b] (from Pm) and Y[k1 -> k2][b] (from Ym)
   int32_t* As;     // [kJ1 * NC][32] A = C1 + Y1 - P[k2][c1], so E = A + B(c2)
   int32_t* C1s;    // [kJ1 * NC][32] C_1
   int32_t* p1s;    // [kJ1][32] P[k2][c1]
@@ -535,7 +536,7 @@ __host__ __device__ constexpr size_t slot_bytes() {
 }
 template <int NC>
 __device__ __forceinline__ SlotData carve_slot(uint8_t* base) {
-  SlotData d;
+  SlotData d{};
 #if PPIPE_SLOT_SMEM
   d.As = reinterpret_cast<int32_t*>(base);
   d.C1s = d.As + kJ1 * NC * 32;
@@ -543,6 +544,7 @@ __device__ __forceinline__ SlotData carve_slot(uint8_t* base) {
   d.list = reinterpret_cast<uint16_t*>(d.p1s + kJ1 * 32);
 #else
   d.As = d.C1s = d.p1s = nullptr;
+  d.rowoff = nullptr;
   d.list = reinterpret_cast<uint16_t*>(base);
 #endif
   return d;
@@ -907,9 +909,9 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
             // the listed candidate's first-cut terms, re-read through L1 (the tile's rows
             // are a few KB): C_1 = P[k1][c1], Y_1 and P[k2][c1]
             const int c1 = c1_base + 32 * j + src;
-            const int C1 = __ldg(cx.Prow(k1) + c1);
+            const int C1 = __ldg(cx.Pm + sd.rowoff[k1] + c1);
             const int pc1 = __ldg(cx.P2 + c1);
-            const int E = C1 + __ldg(cx.Yrow(k1, cx.k2) + c1) - pc1 + Bv;
+            const int E = C1 + __ldg(cx.Ym + sd.rowoff[NC + k1] + c1) - pc1 + Bv;
             const int C2 = Q - pc1;
 #endif
             // listed candidates are feasible: C_1, C_2 <= E <= T_eff and w * T_eff < 2^31
@@ -1272,6 +1274,7 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ int s_tile;
   __shared__ unsigned long long s_unit;
+  __shared__ uint32_t s_rowoff[2 * NC];
   const int nb = 1 << nb_log2;
   const ScoreSmem sm = carve_smem<NC>(smem_raw, nb, row_len);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1316,6 +1319,10 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
     }
     stage_rows(cx, sm, k3, r.c2_from, r.c2_to, true);
     if (tid == 0) s_tile = 0;
+    if (tid < NC) {
+      s_rowoff[tid] = (uint32_t)(((size_t)tid * cx.B + bi) * cx.Mp);
+      s_rowoff[NC + tid] = (uint32_t)(((size_t)__ldg(cx.pair_v + tid * NC + k2) * cx.B + bi) * cx.Mp);
+    }
     __syncthreads();
     int Bmin = INT_MAX;  // min over the unit's c2 of B(c2) (bounds E from below)
     for (int c2 = r.c1lo + 1 + lane; c2 < cx.M; c2 += 32) Bmin = min(Bmin, sm.Bs[c2]);
@@ -1328,8 +1335,10 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
       t = __shfl_sync(FULL_MASK, t, 0);
       if (t >= r.ntiles) break;
       if (t < 64 && !((tmask >> t) & 1ull)) continue;  // no feasible candidate in pass 1
-      k3_tile<NC, 2, W>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin,
-                     carve_slot<NC>(sm.slot + warp * slot_bytes<NC>()), sm.nb16 + warp * row_len, out, em, feas, cand, Bmin);
+      SlotData sd = carve_slot<NC>(sm.slot + warp * slot_bytes<NC>());
+      sd.rowoff = s_rowoff;
+      k3_tile<NC, 2, W>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin, sd,
+                     sm.nb16 + warp * row_len, out, em, feas, cand, Bmin);
     }
     __syncthreads();
   }
