@@ -1269,6 +1269,31 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
   flush_counters(out, feas, cand);
 }
 
+// ---- bulk copy global -> shared (TMA engine, cp.async.bulk) completing on an mbarrier ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// thread-side: earlier generic-proxy accesses of the destination before the async-proxy write
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // ---- kernel 3: K = 3 pass 2 over the hot units only (persistent CTAs pull units
 // from a counter): reload the unit's tables, re-scan with tightened thresholds and
 // emit the survivors. ----
@@ -1279,6 +1304,7 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
   __shared__ int s_tile;
   __shared__ unsigned long long s_unit;
   __shared__ uint32_t s_rowoff[2 * NC];
+  __shared__ unsigned long long s_bar;  // completion of the unit table's bulk copy
   const int nb = 1 << nb_log2;
   const ScoreSmem sm = carve_smem<NC>(smem_raw, nb, row_len);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1286,12 +1312,21 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
   Emitter em{sm.ebuf + warp * 2 * kEmitBuf, 0};
   unsigned long long feas = 0, cand = 0;
   const unsigned long long n_hot = min(out.counters[3], out.hot_cap);
+  if (tid == 0) mbar_init(&s_bar, 1);
+  unsigned parity = 0;
 #pragma unroll 1
   for (;;) {
     if (tid == 0) s_unit = atomicAdd(&out.counters[4], 1ull);
     __syncthreads();
     const unsigned long long u = s_unit;
     if (u >= n_hot) break;
+    // the unit's finalized tables (NC (nb + 2) x 8 bytes, a multiple of 16) arrive by one
+    // bulk copy on the TMA engine while the threads stage the c2 rows
+    const uint2* src = reinterpret_cast<const uint2*>(out.hot_tab) + u * (unsigned long long)ntab;
+    if (tid == 0) {
+      fence_proxy_async();
+      bulk_load(sm.fin, src, (unsigned)(8 * ntab), &s_bar);
+    }
     const uint4 hu = out.hot[u];
     const int ml = (int)hu.x, k2 = (int)(hu.y & 15u), k3 = (int)((hu.y >> 4) & 15u), bi = (int)(hu.y >> 8);
     const unsigned long long tmask = ((unsigned long long)hu.w << 32) | hu.z;
@@ -1300,12 +1335,13 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
     make_ctx<NC, W>(cx, pb, md, k2, bi, nb);
     cx.row_len = row_len;
     const K3Range r = k3_range(md);
-    const uint2* src = reinterpret_cast<const uint2*>(out.hot_tab) + u * (unsigned long long)ntab;
+    stage_rows(cx, sm, k3, r.c2_from, r.c2_to, true);
+    mbar_wait(&s_bar, parity);
+    parity ^= 1u;
     if (pb.gfold) {
       // U'(j) = min(U(j), ceil(bound_j / 2^q)): the unit's own bound and the cross-batch one
       const unsigned long long* gf = pb.gfold + ((size_t)ml * NC * NC * NC + (size_t)k2 * NC + k3) * (nb + 1);
       for (int i = tid; i < ntab; i += 32 * kWarps) {
-        uint2 e = src[i];
         const int k1 = i / (nb + 2), j = i - k1 * (nb + 2);
         if (j <= nb) {
           const unsigned long long g = gf[(size_t)k1 * NC * NC * (nb + 1) + j];
@@ -1313,15 +1349,11 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
             const uint32_t bnd = gfold_bound(g, (uint32_t)cx.b);
             // bounds at or above 2^31 exceed every feasible (weighted) Cmax: no bound
             const uint32_t ub = bnd >= 0x80000000u ? kEmpty : (uint32_t)(((uint64_t)bnd + ((1ull << cx.q) - 1)) >> cx.q);
-            e.x = min(e.x, ub);
+            if (ub < sm.fin[i].x) sm.fin[i].x = ub;
           }
         }
-        sm.fin[i] = e;
       }
-    } else {
-      for (int i = tid; i < ntab; i += 32 * kWarps) sm.fin[i] = src[i];
     }
-    stage_rows(cx, sm, k3, r.c2_from, r.c2_to, true);
     if (tid == 0) s_tile = 0;
     if (tid < NC) {
       s_rowoff[tid] = (uint32_t)(((size_t)tid * cx.B + bi) * cx.Mp);
