@@ -72,6 +72,7 @@ struct ScoreOut {
   uint4* hot;                    // [hot_cap] (local model, k2 | k3 << 4 | b << 8, tile mask lo, hi) of hot units
   uint64_t* hot_tab;             // [hot_cap][table words] their finalized fold tables
   unsigned long long hot_cap;
+  uint32_t* hot_order;           // [hot_cap] pass-2 processing order, heaviest units first (nullptr: slot order)
 };
 
 size_t hot_unit_table_bytes(const Problem& pb);

@@ -1269,6 +1269,36 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
   flush_counters(out, feas, cand);
 }
 
+// ---- pass-2 order: longest-processing-time first. A hot unit's pass-2 work grows with
+// the tiles that held a feasible candidate (popcount of its tile mask) times the model
+// depth; one CTA counting-sorts the units by that estimate (256 bins, descending) so the
+// persistent score3b CTAs do not end on a heavy unit picked up late. ----
+constexpr int kOrderBins = 256;
+__global__ void __launch_bounds__(1024) hot_order_kernel(ScoreOut out, const DevModel* models) {
+  __shared__ uint32_t cnt[kOrderBins];
+  const uint32_t n = (uint32_t)min(out.counters[3], out.hot_cap);
+  for (int i = threadIdx.x; i < kOrderBins; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  auto bin_of = [&](uint32_t u) {
+    const uint4 h = out.hot[u];
+    const uint32_t tiles = h.z == 0xffffffffu && h.w == 0xffffffffu ? 64u : (uint32_t)(__popc(h.z) + __popc(h.w));
+    const uint32_t work = tiles * models[h.x].M;
+    return kOrderBins - 1 - min((uint32_t)kOrderBins - 1, work >> 5);  // heavy -> low bin
+  };
+  for (uint32_t u = threadIdx.x; u < n; u += blockDim.x) atomicAdd(&cnt[bin_of(u)], 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (int b = 0; b < kOrderBins; ++b) {
+      const uint32_t c = cnt[b];
+      cnt[b] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (uint32_t u = threadIdx.x; u < n; u += blockDim.x) out.hot_order[atomicAdd(&cnt[bin_of(u)], 1u)] = u;
+}
+
 // ---- bulk copy global -> shared (TMA engine, cp.async.bulk) completing on an mbarrier ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
@@ -1318,8 +1348,8 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
   for (;;) {
     if (tid == 0) s_unit = atomicAdd(&out.counters[4], 1ull);
     __syncthreads();
-    const unsigned long long u = s_unit;
-    if (u >= n_hot) break;
+    if (s_unit >= n_hot) break;
+    const unsigned long long u = out.hot_order ? out.hot_order[s_unit] : s_unit;
     // the unit's finalized tables (NC (nb + 2) x 8 bytes, a multiple of 16) arrive by one
     // bulk copy on the TMA engine while the threads stage the c2 rows
     const uint2* src = reinterpret_cast<const uint2*>(out.hot_tab) + u * (unsigned long long)ntab;
@@ -1466,6 +1496,10 @@ static cudaError_t launch_score_w(const Problem& pb, const ScoreOut& out, cudaSt
   if (pb.Kmax >= 3 && pb.gfold && pb.n_local > 0) {
     const size_t rows = (size_t)pb.n_local * NC * NC * NC;
     gfold_prefix_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(pb.gfold, rows, (1 << nb_log2) + 1);
+    ++*n_launches;
+  }
+  if (pb.Kmax >= 3 && out.hot_order && pb.n_local > 0) {
+    hot_order_kernel<<<1, 1024, 0, s>>>(out, pb.models);
     ++*n_launches;
   }
   if (pb.Kmax >= 3) {
