@@ -19,6 +19,7 @@
 // DESIGN.md §5 gives the roofline and algorithmic op counts of each kernel.
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 
 #include "ppipe_internal.h"
 
@@ -1484,10 +1485,17 @@ static cudaError_t launch_score_w(const Problem& pb, const ScoreOut& out, cudaSt
     score12_kernel<NC, W><<<(unsigned)pb.n_local * NC * pb.B, 32 * kWarps, smem12, s12>>>(pb, out, nb12_log2);
     ++*n_launches;
   }
+  // PPIPE_DEBUG_FLAGS & 64: per-kernel event times of this launch sequence on stderr
+  static cudaEvent_t dev_ev[4] = {};
+  const bool tdbg = (pb.debug_flags & 64) != 0;
+  if (tdbg && !dev_ev[0])
+    for (auto& x : dev_ev) cudaEventCreate(&x);
+  if (tdbg) cudaEventRecord(dev_ev[0], s);
   if (k3a) {
     score3a_kernel<NC, W><<<grid, 32 * kWarps, smem_a, s>>>(pb, out, nb_log2, row_len);
     ++*n_launches;
   }
+  if (tdbg) cudaEventRecord(dev_ev[1], s);
   if (part == 1) return cudaGetLastError();
   if (ss != nullptr && !early) {
     cudaEventRecord(ss->fork, s);
@@ -1508,12 +1516,23 @@ static cudaError_t launch_score_w(const Problem& pb, const ScoreOut& out, cudaSt
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     const int ctas = std::max(1, std::min(k3bCtasPerSm, smem_sm / (int)(smem + 1024)));  // persistent: fill the SMs
+    if (tdbg) cudaEventRecord(dev_ev[2], s);
     score3b_kernel<NC, W><<<n_sm * ctas, 32 * kWarps, smem, s>>>(pb, out, nb_log2, row_len);
     ++*n_launches;
   }
+  if (tdbg) cudaEventRecord(dev_ev[3], s);
   if (!early) {
     score12_kernel<NC, W><<<(unsigned)pb.n_local * NC * pb.B, 32 * kWarps, smem12, s12>>>(pb, out, nb12_log2);
     ++*n_launches;
+  }
+  if (tdbg && part == 0) {
+    cudaEventSynchronize(dev_ev[3]);
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, dev_ev[0], dev_ev[1]);
+    cudaEventElapsedTime(&b, dev_ev[1], dev_ev[2]);
+    cudaEventElapsedTime(&c, dev_ev[2], dev_ev[3]);
+    fprintf(stderr, "ppipe score ms: score3a %.3f, prefix+order %.3f, score3b %.3f (local models %d)\n", a, b, c,
+            pb.n_local);
   }
   if (ss != nullptr) {
     cudaEventRecord(ss->join, s12);
