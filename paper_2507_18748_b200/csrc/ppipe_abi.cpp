@@ -594,6 +594,10 @@ PPIPE_API int ppipe_load_profiles(ppipe_ctx** out, uint32_t n_models, const ppip
     const long long v = atoll(cap);
     if (v > 0) c->surv_cap = (uint64_t)v;
   }
+  if (const char* cap = getenv("PPIPE_HOT_CAP")) {  // initial hot-unit capacity (tests of the regrow path)
+    const long long v = atoll(cap);
+    if (v > 0) c->hot_cap = (uint64_t)v;
+  }
   auto bail = [&](int code) {
     g_tls_error = c->err;
     free_ctx(c);

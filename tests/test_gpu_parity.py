@@ -106,6 +106,16 @@ def test_survivor_buffer_regrowth(oracle_built, monkeypatch):
     assert_same_result(g, run_oracle(w), "regrowth")
 
 
+@pytest.mark.parametrize("cap", ["1", "7"])
+def test_hot_unit_buffer_regrowth(oracle_built, monkeypatch, cap):
+    """A hot-unit buffer (pass-1 tables handed to pass 2) that is too small is grown and
+    the enumeration re-run; the result must not change (PPIPE_HOT_CAP sets the initial
+    capacity; the overflowing units still push their staircases into the global fold)."""
+    monkeypatch.setenv("PPIPE_HOT_CAP", cap)
+    for w in (config3(), config5(model_ids=[4, 17])):
+        assert_same_result(pp.run(w), run_oracle(w), f"hot-unit regrowth from {cap}, {w.name}")
+
+
 def test_determinism(oracle_built):
     w = config3()
     a, b = pp.run(w), pp.run(w)
