@@ -169,3 +169,21 @@ def test_f2_errors():
         assert "update_profiles_async" in str(e.value)
     finally:
         pp.free(ctx)
+
+
+def test_f2_config4_whole_vs_oracle_golden():
+    """F2 on the whole of config 4 (994.8M candidates, 2.2M F2 points) against the
+    oracle's literal all-pairs F2, stored as hashes by scripts/golden_f2_config4.py
+    (oracle only; 332 s on 8 host threads)."""
+    import hashlib
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "f2_config4_oracle.json")
+    gold = json.load(open(path))
+    w = config4()
+    g = pp.run(w, frontier=2)
+    assert g.n_candidates == gold["n_cand"] and g.n_feasible == gold["n_feas"]
+    assert g.n_points == gold["n_pts"]
+    assert hashlib.sha256(np.ascontiguousarray(g.points).tobytes()).hexdigest() == gold["sha_pts"]
+    seg = np.diff(g.seg_offsets.astype(np.uint64)).astype("<u8")
+    assert hashlib.sha256(seg.tobytes()).hexdigest() == gold["sha_seg"]
