@@ -1050,31 +1050,43 @@ __device__ __forceinline__ void tile_mina_body(const Problem& pb) {
   const K3Range r = k3_range(md);
   if (r.empty) return;
   const int C = pb.C;
+  constexpr int kMaxV = 8;  // distinct bandwidth values staged per thread (more: read through L1)
   __shared__ int wmin[4][kMaxClasses];
+  // this thread's P[k][b][c_1] and Y[v][b][c_1] (its own column: no barrier between write and
+  // read), and the class-pair -> bandwidth-value map
+  __shared__ int sP[kMaxClasses][32 * kJ1];
+  __shared__ int sY[kMaxV][32 * kJ1];
+  __shared__ uint8_t s_pair[kMaxClasses * kMaxClasses];
   const int32_t* Pm = pb.P + md.p_off;
   const int32_t* Ym = pb.Y + md.y_off;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool fastY = pb.V <= kMaxV;
+  if (tid < C * C) s_pair[tid] = pb.pair_v[tid];
+  __syncthreads();
   for (int t = 0; t < r.ntiles; ++t) {
-    const int c1 = r.c1_base0 + t * 32 * kJ1 + (int)threadIdx.x;
+    const int c1 = r.c1_base0 + t * 32 * kJ1 + tid;
     const bool valid = c1 >= r.c1lo && c1 <= r.c1hi;
-    int P[kMaxClasses];
-#pragma unroll
-    for (int k = 0; k < kMaxClasses; ++k) P[k] = (k < C && valid) ? Pm[((size_t)k * pb.B + bi) * md.Mp + c1] : 0;
-#pragma unroll
-    for (int k2 = 0; k2 < kMaxClasses; ++k2) {
-      if (k2 >= C) break;
+    if (valid) {
+      for (int k = 0; k < C; ++k) sP[k][tid] = Pm[((size_t)k * pb.B + bi) * md.Mp + c1];
+      if (fastY)
+        for (int v = 0; v < pb.V; ++v) sY[v][tid] = Ym[((size_t)v * pb.B + bi) * md.Mp + c1];
+    }
+    for (int k2 = 0; k2 < C; ++k2) {
       int m = INT_MAX;
-      if (valid)
+      if (valid) {
+        const int p2 = sP[k2][tid];
         for (int k1 = 0; k1 < C; ++k1) {
-          const int y = Ym[((size_t)pb.pair_v[k1 * C + k2] * pb.B + bi) * md.Mp + c1];
-          m = min(m, P[k1] + y - P[k2]);
+          const int v = s_pair[k1 * C + k2];
+          const int y = fastY ? sY[v][tid] : Ym[((size_t)v * pb.B + bi) * md.Mp + c1];
+          m = min(m, sP[k1][tid] + y - p2);
         }
+      }
       for (int d = 16; d > 0; d >>= 1) m = min(m, __shfl_xor_sync(FULL_MASK, m, d));
       if (lane == 0) wmin[warp][k2] = m;
     }
     __syncthreads();
-    if ((int)threadIdx.x < C) {
-      const int k2 = threadIdx.x;
+    if (tid < C) {
+      const int k2 = tid;
       pb.minA[((size_t)(ml * C + k2) * pb.B + bi) * pb.max_tiles + t] =
           min(min(wmin[0][k2], wmin[1][k2]), min(wmin[2][k2], wmin[3][k2]));
     }
