@@ -1566,7 +1566,7 @@ PPIPE_API int ppipe_pareto_f2(ppipe_ctx* c, const ppipe_enum_params* p, int copy
   CU(c, c->d_f2tmp.reserve(std::max<uint64_t>(n_surv, 1)));
   CU(c, c->d_local.reserve(std::max<uint64_t>(n_surv, 1)));
   CU(c, c->d_segoff_local.reserve(c->n_seg_total + 1));
-  CU(c, c->d_segtmp.reserve(std::max<uint64_t>(n_surv, 1)));
+  CU(c, c->d_segtmp.reserve(std::max<uint64_t>(n_surv, 2)));  // f2_finalize keeps two cursors there
   uint64_t n_pts = 0;
   CU(c, f2_finalize(c->d_f2surv.p, n_surv, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_local.p, c->d_f2tmp.p,
                     c->d_segoff_local.p, c->d_segtmp.p, &n_pts, &c->scratch, c->stream, &nl));

@@ -1560,17 +1560,56 @@ cudaError_t pb_frontier_pass(const ppipe_point_pb* in, uint64_t n, const uint64_
                                     seg_offsets, n_out_host, scratch, s, n_launches);
 }
 
+// F2 survivors the query kernels could not rule out from having an identical vector carry
+// a flag (reserved != 0); only those need the equal-vector pass. Split: flagged -> fl,
+// unflagged -> un (two atomically advanced cursors; order is restored by the final sort).
+__global__ void f2_split_kernel(const ppipe_point* in, uint64_t n, ppipe_point* fl, ppipe_point* un,
+                                unsigned long long* cur) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t w0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); w0 < n;
+       w0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = w0 + lane;
+    const bool valid = i < n;
+    ppipe_point p{};
+    if (valid) p = in[i];
+    const bool f = valid && p.reserved != 0;
+    const unsigned bf = __ballot_sync(0xffffffffu, f), bu = __ballot_sync(0xffffffffu, valid && !f);
+    unsigned long long bF = 0, bU = 0;
+    if (lane == 0) {
+      if (bf) bF = atomicAdd(&cur[0], (unsigned long long)__popc(bf));
+      if (bu) bU = atomicAdd(&cur[1], (unsigned long long)__popc(bu));
+    }
+    bF = __shfl_sync(0xffffffffu, bF, 0);
+    bU = __shfl_sync(0xffffffffu, bU, 0);
+    if (f) fl[bF + __popc(bf & lanemask_lt_())] = p;
+    else if (valid) un[bU + __popc(bu & lanemask_lt_())] = p;
+  }
+}
+
 cudaError_t f2_finalize(const ppipe_point* in, uint64_t n, const uint64_t* seg_base, int C, uint64_t n_seg,
                         ppipe_point* out, ppipe_point* tmp_pts, uint64_t* seg_offsets, uint64_t* seg_tmp,
                         uint64_t* n_out_host, FrontierScratch* scratch, cudaStream_t s, int* n_launches) {
-  (void)seg_tmp;
   const UniTraits::Params q{0x11111111u, nullptr, 1};
-  uint64_t n1 = 0;
-  cudaError_t e = frontier_generic<F2DedupTraits>(in, n, seg_base, C, n_seg, q, tmp_pts, seg_offsets, &n1, scratch,
-                                                  s, n_launches);
+  // 1) split: flagged survivors to `out` (scratch here), unflagged straight to tmp_pts
+  cudaError_t e = cudaMemsetAsync(seg_tmp, 0, 16, s);
   if (e != cudaSuccess) return e;
-  return frontier_generic<F2OrderTraits>(tmp_pts, n1, seg_base, C, n_seg, q, out, seg_offsets, n_out_host, scratch, s,
-                                         n_launches);
+  unsigned long long* cur = reinterpret_cast<unsigned long long*>(seg_tmp);
+  if (n) {
+    f2_split_kernel<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 8), 256, 0, s>>>(in, n, out, tmp_pts, cur);
+    ++*n_launches;
+  }
+  unsigned long long hc[2] = {0, 0};
+  if ((e = cudaMemcpyAsync(hc, cur, 16, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  const uint64_t nf = hc[0], nu = hc[1];
+  // 2) equal-vector runs among the flagged ones, appended after the unflagged
+  uint64_t n1 = 0;
+  if ((e = frontier_generic<F2DedupTraits>(out, nf, seg_base, C, n_seg, q, tmp_pts + nu, seg_offsets, &n1, scratch, s,
+                                           n_launches)) != cudaSuccess)
+    return e;
+  // 3) canonical order (segment, b, c_1, c_2) and the CSR
+  return frontier_generic<F2OrderTraits>(tmp_pts, nu + n1, seg_base, C, n_seg, q, out, seg_offsets, n_out_host,
+                                         scratch, s, n_launches);
 }
 
 cudaError_t truncate_frontier(const ppipe_point* in, const uint64_t* seg_offsets_in, uint64_t n_in, uint64_t n_seg,
