@@ -1427,7 +1427,10 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
 // Shared memory per CTA: the fold tables take what the budget leaves after the
 // three staged c2 rows (B, Q, R), the emit buffers and the pass-2 slot data,
 // rounded down to a power of two (128..2048 buckets).
-constexpr size_t kSmemBudget = 32 * 1024;  // sized for the pass-2 kernel (7 CTAs per SM)
+#ifndef PPIPE_SMEM_BUDGET
+#define PPIPE_SMEM_BUDGET (32 * 1024)
+#endif
+constexpr size_t kSmemBudget = PPIPE_SMEM_BUDGET;  // table-size policy (nb = 256 for config 5)
 
 #ifndef PPIPE_CONCURRENT_12
 #define PPIPE_CONCURRENT_12 0
