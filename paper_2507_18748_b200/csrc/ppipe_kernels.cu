@@ -989,12 +989,28 @@ __device__ __forceinline__ ScoreSmem carve_smem(uint8_t* raw, int nb, int row_le
   return m;
 }
 
-// pass-1 kernel: tables + rows; pass-2 kernel: + emit buffers, tightening buckets and slot data.
+// pass-2 kernel: finalized tables (8 B per bucket) + rows + emit buffers + slot data;
+// pass-1 kernel (carve_smem_a): raw tables (4 B per bucket) + rows.
 template <int NC>
 static size_t score_smem_bytes(int nb, int row_len, bool pass2 = true) {
+  if (!pass2)
+    return ((4 * (size_t)NC * (nb + 2) + 15) & ~(size_t)15) + sizeof(int32_t) * (3 + kWarps) * (size_t)row_len;
   const size_t base = 8 * (size_t)NC * (nb + 2) + sizeof(int32_t) * (3 + kWarps) * (size_t)row_len;
-  if (!pass2) return base;
   return base + (size_t)kWarps * kEmitBuf * 32 + (size_t)kWarps * slot_bytes<NC>();
+}
+
+template <int NC>
+__device__ __forceinline__ ScoreSmem carve_smem_a(uint8_t* raw, int nb, int row_len) {
+  ScoreSmem m;
+  m.fin = nullptr;
+  m.raw = reinterpret_cast<uint32_t*>(raw);
+  m.Bs = reinterpret_cast<int32_t*>(raw + ((4 * (size_t)NC * (nb + 2) + 15) & ~(size_t)15));
+  m.Qs = m.Bs + row_len;
+  m.Rs = m.Qs + row_len;
+  m.nb16 = reinterpret_cast<uint32_t*>(m.Rs + row_len);
+  m.ebuf = nullptr;
+  m.slot = nullptr;
+  return m;
 }
 
 // The bucket count (table resolution) follows a fixed smem policy, independent of
@@ -1218,7 +1234,7 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
   __shared__ unsigned long long s_slot;
   __shared__ unsigned long long s_tmask;  // tiles (t < 64) of this unit with a feasible candidate
   const int nb = 1 << nb_log2;
-  const ScoreSmem sm = carve_smem<NC>(smem_raw, nb, row_len);
+  const ScoreSmem sm = carve_smem_a<NC>(smem_raw, nb, row_len);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ntab = NC * (nb + 2);
   const int k2 = blockIdx.x % NC;
@@ -1228,7 +1244,7 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
   CtaCtx<NC> cx;
   make_ctx<NC, W>(cx, pb, md, k2, bi, nb);
   cx.row_len = row_len;
-  Emitter em{sm.ebuf + warp * 2 * kEmitBuf, 0};  // unused in pass 1
+  Emitter em{nullptr, 0};  // unused in pass 1
   unsigned long long feas = 0, cand = 0;
   const K3Range r = k3_range(md);
   if (pb.Kmax >= 3 && !r.empty) {
