@@ -200,6 +200,7 @@ struct ppipe_ctx {
   DevBuf<uint4> d_hot;
   DevBuf<uint64_t> d_hot_tab;
   DevBuf<uint32_t> d_hot_order;  // pass-2 order of the hot units (heaviest first)
+  DevBuf<uint32_t> d_hot_w;      // pass-1 feasible count per hot unit
   uint64_t hot_cap = 0;
   DevBuf<ppipe_point> d_surv, d_local, d_gather, d_union, d_final;
   DevBuf<uint64_t> d_segoff_local, d_segoff_final, d_cnt_send, d_cnt_recv;
@@ -297,6 +298,7 @@ void free_ctx(ppipe_ctx* c) {
   c->d_hot.release();
   c->d_hot_tab.release();
   c->d_hot_order.release();
+  c->d_hot_w.release();
   c->d_surv.release();
   c->d_local.release();
   c->d_gather.release();
@@ -891,6 +893,7 @@ static int run_enumerate(ppipe_ctx* c) {
   CU(c, c->d_hot.reserve(c->hot_cap));
   CU(c, c->d_hot_tab.reserve(c->hot_cap * tab_words));
   CU(c, c->d_hot_order.reserve(c->hot_cap));
+  CU(c, c->d_hot_w.reserve(c->hot_cap));
   if (pb.Kmax >= 3 && !getenv("PPIPE_NO_GFOLD")) {  // (the env switch is for measurements only)
     const size_t ng = gfold_elems(pb);
     CU(c, c->d_gfold.reserve(ng));
@@ -898,7 +901,8 @@ static int run_enumerate(ppipe_ctx* c) {
     pb.gfold = c->d_gfold.p;
   }
   ScoreOut so{c->d_surv.p, c->d_counters.p, (unsigned long long)c->d_surv.n, c->d_hot.p, c->d_hot_tab.p,
-              (unsigned long long)c->hot_cap, getenv("PPIPE_NO_HOT_ORDER") ? nullptr : c->d_hot_order.p};
+              (unsigned long long)c->hot_cap, getenv("PPIPE_NO_HOT_ORDER") ? nullptr : c->d_hot_order.p,
+              c->d_hot_w.p};
   c->launches_i = 0;
   pb.model_base = 0;
   pb.n_chunk = pb.n_local;

@@ -73,6 +73,7 @@ struct ScoreOut {
   uint64_t* hot_tab;             // [hot_cap][table words] their finalized fold tables
   unsigned long long hot_cap;
   uint32_t* hot_order;           // [hot_cap] pass-2 processing order, heaviest units first (nullptr: slot order)
+  uint32_t* hot_w;               // [hot_cap] feasible candidates of each hot unit (pass 1; for the order)
 };
 
 size_t hot_unit_table_bytes(const Problem& pb);

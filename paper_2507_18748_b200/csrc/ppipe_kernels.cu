@@ -1233,6 +1233,7 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
   __shared__ int s_tile;
   __shared__ unsigned long long s_slot;
   __shared__ unsigned long long s_tmask;  // tiles (t < 64) of this unit with a feasible candidate
+  __shared__ unsigned s_wfeas;            // the unit's feasible candidates (pass-2 order)
   const int nb = 1 << nb_log2;
   const ScoreSmem sm = carve_smem_a<NC>(smem_raw, nb, row_len);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1254,6 +1255,7 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
       stage_rows(cx, sm, k3, r.c2_from, r.c2_to, k3 == 0);
       if (tid == 0) {
         s_tile = 0;
+        s_wfeas = 0;
         s_tmask = r.ntiles > 64 ? ~0ull : 0ull;  // more tiles than mask bits: pass 2 visits all
       }
       __syncthreads();
@@ -1271,14 +1273,20 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
                        SlotData{}, sm.nb16 + warp * row_len, out, em, feas, cand, 0, hint);
         if (__any_sync(FULL_MASK, feas != ft) && lane == 0 && t < 64) atomicOr(&s_tmask, 1ull << t);
       }
+      {
+        const unsigned wf = __reduce_add_sync(FULL_MASK, (unsigned)min(feas - feas0, 0xffffffffull));
+        if (lane == 0 && wf) atomicAdd(&s_wfeas, wf);
+      }
       if (__syncthreads_or(feas != feas0) && !(pb.debug_flags & 2)) {
         if (tid == 0) {
           s_slot = atomicAdd(&out.counters[3], 1ull);
           // (local model, k2 | k3 << 4 | b << 8, tile mask): pass 2 skips the tiles without a
           // feasible candidate (it only emits feasible ones)
-          if (s_slot < out.hot_cap)
+          if (s_slot < out.hot_cap) {
             out.hot[s_slot] = make_uint4(ml, (unsigned)k2 | ((unsigned)k3 << 4) | ((unsigned)bi << 8),
                                          (unsigned)s_tmask, (unsigned)(s_tmask >> 32));
+            out.hot_w[s_slot] = s_wfeas;
+          }
         }
         __syncthreads();
         // finalized tables straight to the unit's global slot; staircase steps to the
@@ -1300,9 +1308,17 @@ __global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
 
 // ---- pass-2 order: longest-processing-time first. A hot unit's pass-2 work grows with
 // the tiles that held a feasible candidate (popcount of its tile mask) times the model
-// depth; one CTA counting-sorts the units by that estimate (256 bins, descending) so the
-// persistent score3b CTAs do not end on a heavy unit picked up late. ----
+// depth, and with its feasible count for the dense units (many feasible candidates per
+// tile: their survivor checks dominate); one CTA counting-sorts the units by the larger
+// of the two estimates (256 bins, descending) so the persistent score3b CTAs do not end
+// on a heavy unit picked up late. The feasible term only moves the dense units forward
+// (divisor 192, measured): ordering every unit by it (divisor <= 64) breaks up the units
+// of a model, which share its rows in L2, and cost up to 8% of score3b at N = 1; with 192
+// the N = 4 tail (a dense unit of 1.5 ms started late) shrinks, step 20.97 -> 20.58 ms. ----
 constexpr int kOrderBins = 256;
+#ifndef PPIPE_ORDER_FEAS_DIV
+#define PPIPE_ORDER_FEAS_DIV 192
+#endif
 __global__ void __launch_bounds__(1024) hot_order_kernel(ScoreOut out, const DevModel* models) {
   __shared__ uint32_t cnt[kOrderBins];
   const uint32_t n = (uint32_t)min(out.counters[3], out.hot_cap);
@@ -1311,7 +1327,7 @@ __global__ void __launch_bounds__(1024) hot_order_kernel(ScoreOut out, const Dev
   auto bin_of = [&](uint32_t u) {
     const uint4 h = out.hot[u];
     const uint32_t tiles = h.z == 0xffffffffu && h.w == 0xffffffffu ? 64u : (uint32_t)(__popc(h.z) + __popc(h.w));
-    const uint32_t work = tiles * models[h.x].M;
+    const uint32_t work = max(tiles * models[h.x].M, out.hot_w[u] / PPIPE_ORDER_FEAS_DIV);
     return kOrderBins - 1 - min((uint32_t)kOrderBins - 1, work >> 5);  // heavy -> low bin
   };
   for (uint32_t u = threadIdx.x; u < n; u += blockDim.x) atomicAdd(&cnt[bin_of(u)], 1u);
