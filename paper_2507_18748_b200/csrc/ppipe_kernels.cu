@@ -923,6 +923,16 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
             const int Cmax = max(max(wtw<W>(wp, k1) * C1, w2 * C2), Rw);
             PPIPE_DCHECK(E >= 0 && E <= cx.T && (E >> cx.sh) < nb + 2 && src < 32 && j < kJ1);
             cond = survives(fin + (size_t)k1 * (nb + 2), E >> cx.sh, E, Cmax, cx.sh, cx.q);
+#ifdef PPIPE_COUNT_LISTED
+            {
+              const int Elo = min(cx.T, Bv + tmax_hint);  // tmax_hint = the tile's min A in pass 2
+              const uint32_t U0 = fin[(size_t)k1 * (nb + 2) + (Elo >> cx.sh)].x;
+              const unsigned Ub0 = U0 == kEmpty ? 0xffffffffu : (U0 << cx.q);
+              const bool cr = (unsigned)Rw >= Ub0, cc2 = (unsigned)(w2 * C2) >= Ub0;
+              atomicAdd(&out.counters[cr ? 10 : (cc2 ? 11 : 12)], 1ull);
+              if (tmax_hint > E - Bv) atomicAdd(&out.counters[13], 1ull);  // minA not a lower bound?!
+            }
+#endif
             if (cond) rec = make_rec(cx.model, 3, c1_base + 32 * j + src, c2u, k1, cx.k2, k3, cx.b, E, C1, C2, R);
           }
           if (__any_sync(FULL_MASK, cond)) emit_warp(out, em, cond, rec);
@@ -1448,8 +1458,13 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
       if (t < 64 && !((tmask >> t) & 1ull)) continue;  // no feasible candidate in pass 1
       SlotData sd = carve_slot<NC>(sm.slot + warp * slot_bytes<NC>());
       sd.rowoff = s_rowoff;
+#ifdef PPIPE_COUNT_LISTED
+      const int mina_t = pb.minA && t < pb.max_tiles ? __ldg(pb.minA + ((size_t)(ml * NC + k2) * pb.B + bi) * pb.max_tiles + t) : 0;
+#else
+      const int mina_t = INT_MAX;
+#endif
       k3_tile<NC, 2, W>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin, sd,
-                     sm.nb16 + warp * row_len, out, em, feas, cand, Bmin);
+                     sm.nb16 + warp * row_len, out, em, feas, cand, Bmin, mina_t);
     }
     __syncthreads();
   }
