@@ -1198,10 +1198,6 @@ PPIPE_API int ppipe_pareto(ppipe_ctx* c, int copy_to_host, ppipe_frontier* out) 
       fprintf(stderr, "ppipe debug: hot units %llu, pass-2 tiles %llu, visits %llu, slot-hits %llu, emit-calls %llu, "
               "survivors %llu, feasible %llu\n", c->h_counters[3], c->h_counters[7], c->h_counters[5],
               c->h_counters[6], c->h_counters[8], c->h_counters[0], c->h_counters[1]);
-  if (const char* dbg = getenv("PPIPE_DEBUG_FLAGS"))
-    if (atoi(dbg) & 8)
-      fprintf(stderr, "ppipe listed vs tile minA bound: R catches %llu, C2 (not R) catches %llu, neither %llu, bad %llu\n",
-              c->h_counters[10], c->h_counters[11], c->h_counters[12], c->h_counters[13]);
   uint64_t n_feas = c->h_counters[1], n_cand = c->h_counters[2];
   int nl = c->launches_i;
   // local frontier

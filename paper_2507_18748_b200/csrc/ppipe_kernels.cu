@@ -561,6 +561,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
                         const SlotData& sd, uint32_t* nb16, const ScoreOut& out, Emitter& em,
                         unsigned long long& feas, unsigned long long& cand, int Bmin = 0,
                         int tmax_hint = INT_MAX) {
+  // tmax_hint: pass 1, T_eff - (the tile's minimum A) or INT_MAX; pass 2, the tile's minimum A
   const int lane = threadIdx.x & 31;
   const int nb = cx.nb;
   if (pass == 1 && tmax_hint != INT_MAX) {
@@ -874,12 +875,32 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
         // against the finalized tables (survives()) and emitted.
         const int c2u = c2 + u;
         const int Rw = wmul(wtw<W>(wp, k3), R);  // per c2 (may exceed T_eff for unlisted ones)
+        // k_1 columns dead at this c2: every candidate of the tile has E >= Elo = B(c2) +
+        // minA, so with U nonincreasing, C_3 = R(c2) >= U_k1(Elo) means Cmax >= U_k1(E):
+        // dominated (removes ~35% of the listed pairs; lane k1 tests column k1)
+        unsigned live;
+        {
+          const int Elo = max(0, min(cx.T, Bv + tmax_hint));
+          bool dead = false;
+          if (lane < NC) {
+            const uint32_t U0 = fin[(size_t)lane * (nb + 2) + (Elo >> cx.sh)].x;
+            dead = U0 != kEmpty && (unsigned)Rw >= (U0 << cx.q);
+          }
+          live = ~__ballot_sync(FULL_MASK, dead) & ((1u << NC) - 1u);
+        }
+        if (live == 0u) continue;
         unsigned fm = 0;
 #pragma unroll
         for (int j = 0; j < kJ1; ++j) {
           const bool v = 32 * j + lane < relu;
 #pragma unroll
           for (int k1 = 0; k1 < NC; ++k1) fm |= (v && Bv <= thr[j][k1]) ? (1u << (j * NC + k1)) : 0u;
+        }
+        {
+          unsigned cols = 0;
+#pragma unroll
+          for (int j = 0; j < kJ1; ++j) cols |= live << (j * NC);
+          fm &= cols;
         }
         const int cnt = __popc(fm);
         int incl = cnt;
@@ -923,16 +944,6 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
             const int Cmax = max(max(wtw<W>(wp, k1) * C1, w2 * C2), Rw);
             PPIPE_DCHECK(E >= 0 && E <= cx.T && (E >> cx.sh) < nb + 2 && src < 32 && j < kJ1);
             cond = survives(fin + (size_t)k1 * (nb + 2), E >> cx.sh, E, Cmax, cx.sh, cx.q);
-#ifdef PPIPE_COUNT_LISTED
-            {
-              const int Elo = min(cx.T, Bv + tmax_hint);  // tmax_hint = the tile's min A in pass 2
-              const uint32_t U0 = fin[(size_t)k1 * (nb + 2) + (Elo >> cx.sh)].x;
-              const unsigned Ub0 = U0 == kEmpty ? 0xffffffffu : (U0 << cx.q);
-              const bool cr = (unsigned)Rw >= Ub0, cc2 = (unsigned)(w2 * C2) >= Ub0;
-              atomicAdd(&out.counters[cr ? 10 : (cc2 ? 11 : 12)], 1ull);
-              if (tmax_hint > E - Bv) atomicAdd(&out.counters[13], 1ull);  // minA not a lower bound?!
-            }
-#endif
             if (cond) rec = make_rec(cx.model, 3, c1_base + 32 * j + src, c2u, k1, cx.k2, k3, cx.b, E, C1, C2, R);
           }
           if (__any_sync(FULL_MASK, cond)) emit_warp(out, em, cond, rec);
@@ -1458,11 +1469,10 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
       if (t < 64 && !((tmask >> t) & 1ull)) continue;  // no feasible candidate in pass 1
       SlotData sd = carve_slot<NC>(sm.slot + warp * slot_bytes<NC>());
       sd.rowoff = s_rowoff;
-#ifdef PPIPE_COUNT_LISTED
-      const int mina_t = pb.minA && t < pb.max_tiles ? __ldg(pb.minA + ((size_t)(ml * NC + k2) * pb.B + bi) * pb.max_tiles + t) : 0;
-#else
-      const int mina_t = INT_MAX;
-#endif
+      // the tile's minimum A (pack launch): E >= B(c2) + minA for every candidate of the tile
+      const int mina_t = pb.minA && t < pb.max_tiles
+                             ? __ldg(pb.minA + ((size_t)(ml * NC + k2) * pb.B + bi) * pb.max_tiles + t)
+                             : INT_MIN / 2;
       k3_tile<NC, 2, W>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin, sd,
                      sm.nb16 + warp * row_len, out, em, feas, cand, Bmin, mina_t);
     }
