@@ -877,14 +877,17 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
         const int Rw = wmul(wtw<W>(wp, k3), R);  // per c2 (may exceed T_eff for unlisted ones)
         // k_1 columns dead at this c2: every candidate of the tile has E >= Elo = B(c2) +
         // minA, so with U nonincreasing, C_3 = R(c2) >= U_k1(Elo) means Cmax >= U_k1(E):
-        // dominated (removes ~35% of the listed pairs; lane k1 tests column k1)
+        // dominated (lane k1 tests column k1)
         unsigned live;
         {
           const int Elo = max(0, min(cx.T, Bv + tmax_hint));
+          // and C_2 = Q(c2) - P[k2][c1] >= Q(c2) - P[k2][min(c2 - 1, last c1 of the tile)]
+          const int c2lo = Q - Qs[min(c2u - 1, min(c1_base + 32 * kJ1 - 1, c1_hi))];
+          const unsigned cm = (unsigned)max(Rw, wmul(w2, max(0, c2lo)));
           bool dead = false;
           if (lane < NC) {
             const uint32_t U0 = fin[(size_t)lane * (nb + 2) + (Elo >> cx.sh)].x;
-            dead = U0 != kEmpty && (unsigned)Rw >= (U0 << cx.q);
+            dead = U0 != kEmpty && cm >= (U0 << cx.q);
           }
           live = ~__ballot_sync(FULL_MASK, dead) & ((1u << NC) - 1u);
         }
