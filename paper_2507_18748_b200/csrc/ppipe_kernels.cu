@@ -561,7 +561,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
                         const SlotData& sd, uint32_t* nb16, const ScoreOut& out, Emitter& em,
                         unsigned long long& feas, unsigned long long& cand, int Bmin = 0,
                         int tmax_hint = INT_MAX) {
-  // tmax_hint: pass 1, T_eff - (the tile's minimum A) or INT_MAX; pass 2, the tile's minimum A
+  // tmax_hint (pass 1): T_eff - (the tile's minimum A) or INT_MAX
   const int lane = threadIdx.x & 31;
   const int nb = cx.nb;
   if (pass == 1 && tmax_hint != INT_MAX) {
@@ -588,6 +588,9 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
   int c1r[kJ1][NC];
   int p1[kJ1];
   int wlo = INT_MAX, whi = -1;  // pass 2: c2 range that can hold survivors
+  int amin_k[NC];               // pass 2: per k1, the minimum A of the tile (reduced below)
+#pragma unroll
+  for (int k1 = 0; k1 < NC; ++k1) amin_k[k1] = INT_MAX;
 #pragma unroll
   for (int j = 0; j < kJ1; ++j) {
     const int c1 = c1_base + 32 * j + lane;
@@ -600,6 +603,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
       // E = A + B(c2) with A = C1 + Y1 - P[k2][c1]  =>  feasible iff B(c2) <= T - A
       int t = valid ? cx.T - (C1 + y - p1[j]) : kInvalidThr;
       if (pass == 2) {
+        if (valid) amin_k[k1] = min(amin_k[k1], C1 + y - p1[j]);
         int b0 = nb;
         if (valid) {
           const uint2* frow = fin + (size_t)k1 * (nb + 2);
@@ -662,11 +666,19 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
   const int M = cx.M;
   unsigned nfeas = 0;
   int c2_start = c1_base + 1, c2_end = M;
+  int amin_col = INT_MAX;  // pass 2, lane k1 < NC: the tile's minimum A of column k1
   if (pass == 2) {
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
       wlo = min(wlo, __shfl_xor_sync(FULL_MASK, wlo, d));
       whi = max(whi, __shfl_xor_sync(FULL_MASK, whi, d));
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < NC; ++k1) {
+      int a = amin_k[k1];
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) a = min(a, __shfl_xor_sync(FULL_MASK, a, d));
+      if (lane == k1) amin_col = a;
     }
     if (whi < 0) return;  // no slot of this tile can hold a survivor
     c2_start = c1_base + 1 + (max(0, wlo - (c1_base + 1)) & ~3);  // keep groups aligned
@@ -875,12 +887,12 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
         // against the finalized tables (survives()) and emitted.
         const int c2u = c2 + u;
         const int Rw = wmul(wtw<W>(wp, k3), R);  // per c2 (may exceed T_eff for unlisted ones)
-        // k_1 columns dead at this c2: every candidate of the tile has E >= Elo = B(c2) +
-        // minA, so with U nonincreasing, C_3 = R(c2) >= U_k1(Elo) means Cmax >= U_k1(E):
-        // dominated (lane k1 tests column k1)
+        // k_1 columns dead at this c2: every candidate of column k1 in the tile has E >= Elo
+        // = B(c2) + (the column's minimum A over the tile), so with U nonincreasing, C_3 =
+        // R(c2) >= U_k1(Elo) means Cmax >= U_k1(E): dominated (lane k1 tests column k1)
         unsigned live;
         {
-          const int Elo = max(0, min(cx.T, Bv + tmax_hint));
+          const int Elo = (int)max(0ll, min((long long)cx.T, (long long)Bv + amin_col));
           // and C_2 = Q(c2) - P[k2][c1] >= Q(c2) - P[k2][min(c2 - 1, last c1 of the tile)]
           const int c2lo = Q - Qs[min(c2u - 1, min(c1_base + 32 * kJ1 - 1, c1_hi))];
           const unsigned cm = (unsigned)max(Rw, wmul(w2, max(0, c2lo)));
@@ -1472,12 +1484,8 @@ __global__ void __launch_bounds__(32 * kWarps, k3bCtasPerSm)
       if (t < 64 && !((tmask >> t) & 1ull)) continue;  // no feasible candidate in pass 1
       SlotData sd = carve_slot<NC>(sm.slot + warp * slot_bytes<NC>());
       sd.rowoff = s_rowoff;
-      // the tile's minimum A (pack launch): E >= B(c2) + minA for every candidate of the tile
-      const int mina_t = pb.minA && t < pb.max_tiles
-                             ? __ldg(pb.minA + ((size_t)(ml * NC + k2) * pb.B + bi) * pb.max_tiles + t)
-                             : INT_MIN / 2;
       k3_tile<NC, 2, W>(cx, k3, r.c1_base0 + t * 32 * kJ1, r.c1lo, r.c1hi, sm.Bs, sm.Qs, sm.Rs, sm.raw, sm.fin, sd,
-                     sm.nb16 + warp * row_len, out, em, feas, cand, Bmin, mina_t);
+                     sm.nb16 + warp * row_len, out, em, feas, cand, Bmin);
     }
     __syncthreads();
   }
