@@ -409,11 +409,14 @@ def main():
     # Work-based roofline (the integer-issue ceiling): the score phase's executed
     # warp-instructions per step (ncu, profiles/r2_score_ncu.json, this build, config 5 at
     # N = 1; deterministic for the workload) x 32 lanes / the live score-phase time.
-    prof = score_profile(args.config) if (world == 1 and not args.models and args.margin is None) else None
+    # At N > 1 the ranks split the same work (first-cut-row shards): the per-GPU figure
+    # takes 1/N of the N = 1 count over the slowest rank's score time (an approximation:
+    # the count is not re-measured per rank).
+    prof = score_profile(args.config) if (not args.models and args.margin is None) else None
     traffic = issue = None
     if prof is not None:
-        traffic = prof["total"]["dram_bytes"]
-        issue = prof["total"]["inst_executed"] * 32 / (kern_max / 1000.0)
+        traffic = prof["total"]["dram_bytes"] / world
+        issue = prof["total"]["inst_executed"] / world * 32 / (kern_max / 1000.0)
     launches_tot = int(allsum(launches))
 
     # ---- e2e: through the public API with HOST buffers, H2D + D2H inside the timed region ----
@@ -568,7 +571,9 @@ def main():
                      "kernel_ms": kern_max,
                      "achieved_basis": ("executed warp-instructions of the score kernels per step x 32 lanes / the live "
                                         "score-phase time; instruction and DRAM counts from ncu --set full of this build "
-                                        f"({prof['source']})" if prof is not None else
+                                        f"({prof['source']})" + (f"; per GPU: 1/{world} of the N = 1 count over the slowest "
+                                                                 "rank's score time" if world > 1 else "")
+                                        if prof is not None else
                                         "no ncu profile for this configuration: W-model ops (below) instead"),
                      "issue_frac": (issue / peak_ops) if issue is not None else None,
                      "per_kernel_ncu": prof["kernels"] if prof is not None else None,
