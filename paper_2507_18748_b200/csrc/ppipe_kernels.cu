@@ -180,10 +180,16 @@ __device__ __forceinline__ Rec make_rec(uint32_t model, int K, int c1, int c2, i
 #ifndef PPIPE_P1_FOLD_EVERY
 #define PPIPE_P1_FOLD_EVERY 4  // pass 1 folds one c2 in 4 of a hit group (1: every feasible candidate)
 #endif
-#ifndef PPIPE_U_UNROLL
-#define PPIPE_U_UNROLL 2  // unroll of the per-c2 slow path over a hit group's 4 c2 (measured: 2 best)
+// unroll of the per-c2 slow path over a hit group's 4 c2, per pass (measured, config 5:
+// pass 1 at 1 / 2 / 4: score3a 34.9 / 32.8 / 32.4 ms; pass 2 at 1 / 2 / 4: score3b 24.1 /
+// 27.1 / 36.9 ms -- pass 2's body is large, unrolled it spills)
+#ifndef PPIPE_U_UNROLL_P1
+#define PPIPE_U_UNROLL_P1 4
 #endif
-constexpr int kUUnroll = PPIPE_U_UNROLL;
+#ifndef PPIPE_U_UNROLL_P2
+#define PPIPE_U_UNROLL_P2 1
+#endif
+constexpr int kUUnrollP1 = PPIPE_U_UNROLL_P1, kUUnrollP2 = PPIPE_U_UNROLL_P2;
 #ifndef PPIPE_SCAN_UNROLL
 #define PPIPE_SCAN_UNROLL 2
 #endif
@@ -845,7 +851,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
     const int4 r4 = *reinterpret_cast<const int4*>(Rs + c2);
     // Some lane passed at some c2 of the group. Slot j of this lane is a real
     // pair iff 32 j + lane < c2 - c1_base.
-#pragma unroll kUUnroll
+#pragma unroll(pass == 1 ? kUUnrollP1 : kUUnrollP2)
     for (int u = 0; u < 4; ++u) {
       const int hu = u == 0 ? h0 : (u == 1 ? h1 : (u == 2 ? h2 : h3));
       if (!__any_sync(FULL_MASK, hu)) continue;
