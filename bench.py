@@ -309,15 +309,23 @@ def main():
         dist.broadcast(t, 0)
         nccl_id = bytes(t.cpu().numpy().tobytes())
 
-    # pinned host copies of the inputs (the e2e leg copies them H2D every step)
+    # pinned host copies of the inputs (the e2e leg copies them H2D every step): one
+    # page-locked buffer per kind, sliced per model (the library merges the copies of
+    # adjacent models)
+    lat_all = torch.empty(sum(mp.lat_us.size for mp in w.models), dtype=torch.int32, pin_memory=True)
+    S_all = torch.empty(sum(mp.act_bytes.size for mp in w.models), dtype=torch.int64, pin_memory=True)
+    lat_np, S_np = lat_all.numpy().view(np.uint32), S_all.numpy().view(np.uint64)
     lat_h, S_h = [], []
+    ol = os_ = 0
     for mp in w.models:
-        lt = torch.empty(mp.lat_us.shape, dtype=torch.int32, pin_memory=True)
-        lt.numpy().view(np.uint32)[...] = mp.lat_us
-        st = torch.empty(mp.act_bytes.shape, dtype=torch.int64, pin_memory=True)
-        st.numpy().view(np.uint64)[...] = mp.act_bytes
-        lat_h.append(lt.numpy().view(np.uint32))
-        S_h.append(st.numpy().view(np.uint64))
+        lt = lat_np[ol:ol + mp.lat_us.size].reshape(mp.lat_us.shape)
+        lt[...] = mp.lat_us
+        st = S_np[os_:os_ + mp.act_bytes.size].reshape(mp.act_bytes.shape)
+        st[...] = mp.act_bytes
+        ol += mp.lat_us.size
+        os_ += mp.act_bytes.size
+        lat_h.append(lt)
+        S_h.append(st)
 
     ctx = pp.load_profiles(lat_h, S_h, w.n_classes, w.batches, w.bw, rank=rank, world=world, device=local_rank,
                            nccl_id=nccl_id)

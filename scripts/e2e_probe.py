@@ -15,13 +15,26 @@ from workloads import make_config  # noqa: E402
 
 w = make_config(5)
 lat_h, S_h = [], []
-for mp in w.models:
-    lt = torch.empty(mp.lat_us.shape, dtype=torch.int32, pin_memory=True)
-    lt.numpy().view(np.uint32)[...] = mp.lat_us
-    st = torch.empty(mp.act_bytes.shape, dtype=torch.int64, pin_memory=True)
-    st.numpy().view(np.uint64)[...] = mp.act_bytes
-    lat_h.append(lt.numpy().view(np.uint32))
-    S_h.append(st.numpy().view(np.uint64))
+if "--separate" in sys.argv:  # one pinned allocation per model array
+    for mp in w.models:
+        lt = torch.empty(mp.lat_us.shape, dtype=torch.int32, pin_memory=True)
+        lt.numpy().view(np.uint32)[...] = mp.lat_us
+        st = torch.empty(mp.act_bytes.shape, dtype=torch.int64, pin_memory=True)
+        st.numpy().view(np.uint64)[...] = mp.act_bytes
+        lat_h.append(lt.numpy().view(np.uint32))
+        S_h.append(st.numpy().view(np.uint64))
+else:  # one pinned buffer per kind, sliced per model (as bench.py)
+    lat_all = torch.empty(sum(mp.lat_us.size for mp in w.models), dtype=torch.int32, pin_memory=True)
+    S_all = torch.empty(sum(mp.act_bytes.size for mp in w.models), dtype=torch.int64, pin_memory=True)
+    la, sa = lat_all.numpy().view(np.uint32), S_all.numpy().view(np.uint64)
+    ol = os_ = 0
+    for mp in w.models:
+        lat_h.append(la[ol:ol + mp.lat_us.size].reshape(mp.lat_us.shape))
+        lat_h[-1][...] = mp.lat_us
+        S_h.append(sa[os_:os_ + mp.act_bytes.size].reshape(mp.act_bytes.shape))
+        S_h[-1][...] = mp.act_bytes
+        ol += mp.lat_us.size
+        os_ += mp.act_bytes.size
 ctx = pp.load_profiles(lat_h, S_h, w.n_classes, w.batches, w.bw, device=0)
 for it in range(4):
     torch.cuda.synchronize()

@@ -96,3 +96,35 @@ def test_async_upload_of_wrapping_latencies_fails_cleanly(oracle_built, value):
         assert_same_result(pp.pareto(ctx), run_oracle(w), "recovered after wrapping values")
     finally:
         pp.free(ctx)
+
+
+def test_async_upload_same_buffers_new_contents(oracle_built):
+    """A serving loop re-uploads the same (pinned) arrays with new contents: the cached
+    descriptors must point at the live buffers, and slices of one buffer (merged copies)
+    must land per model."""
+    w = config3()
+    lat_all = np.zeros(sum(m.lat_us.size for m in w.models), np.uint32)
+    S_all = np.zeros(sum(m.act_bytes.size for m in w.models), np.uint64)
+    lat, S, ol, os_ = [], [], 0, 0
+    for m in w.models:
+        lat.append(lat_all[ol:ol + m.lat_us.size].reshape(m.lat_us.shape))
+        S.append(S_all[os_:os_ + m.act_bytes.size].reshape(m.act_bytes.shape))
+        ol += m.lat_us.size
+        os_ += m.act_bytes.size
+    for a, m in zip(lat, _scaled(w, 7)):
+        a[...] = m
+    for a, m in zip(S, w.models):
+        a[...] = m.act_bytes
+    ctx = pp.load_profiles(lat, S, w.n_classes, w.batches, w.bw)
+    try:
+        pp.update_profiles_async(ctx, lat, S)
+        pp.enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
+        g7 = pp.pareto(ctx)
+        for a, m in zip(lat, w.models):  # new contents, same array objects
+            a[...] = m.lat_us
+        pp.update_profiles_async(ctx, lat, S)
+        pp.enumerate(ctx, w.kmax, w.slo_us, w.margin_permille)
+        assert_same_result(pp.pareto(ctx), run_oracle(w), "config 3, same buffers with new contents")
+        assert g7.n_points != 0
+    finally:
+        pp.free(ctx)
