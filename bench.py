@@ -457,7 +457,7 @@ def main():
                "h2d_bytes_per_step": int(allsum(h2d)), "d2h_bytes_per_step": int(allsum(d2h)),
                "ms_per_step": e_tot / e2e_steps,
                "path": "ppipe_update_profiles_async (pinned host lat/S) + ppipe_enumerate (uploads the profiles "
-                       "in 4 chunks, each validated/packed/scored as it lands, overlapping the H2D) + "
+                       "in 7 chunks, each packed (with validation) and scored as it lands, overlapping the H2D) + "
                        "ppipe_pareto(copy_to_host) into a page-locked buffer read zero-copy (rank 0; the merged "
                        "frontier is replicated on every rank's device)"}
 

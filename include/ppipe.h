@@ -118,7 +118,7 @@ typedef struct {
 int ppipe_update_profiles(ppipe_ctx *ctx, uint32_t n_models, const ppipe_model *models);
 
 /* Like ppipe_update_profiles, but returns at once after the shape checks: the
- * next ppipe_enumerate uploads the values itself, in up to 4 chunks of models on a
+ * next ppipe_enumerate uploads the values itself, in up to 7 chunks of models on a
  * copy stream, and validates, packs and scores (K = 3 pass 1) each chunk as soon as
  * it has arrived, so the host -> device copy overlaps the scoring of earlier
  * chunks. The host buffers must stay valid and unchanged until the next

@@ -231,7 +231,7 @@ struct ppipe_ctx {
   // ppipe_update_profiles_async: host descriptors whose copy the next enumerate
   // issues in chunks on cstream, overlapped with scoring earlier chunks
 #ifndef PPIPE_MAX_CHUNKS
-#define PPIPE_MAX_CHUNKS 4  // chunk events (the async upload uses 4 geometric chunks)
+#define PPIPE_MAX_CHUNKS 8  // chunk events of the async upload (at most 8 chunks)
 #endif
   static constexpr int kMaxChunks = PPIPE_MAX_CHUNKS;
   bool pending_upload = false, check_err = false;
@@ -915,12 +915,12 @@ static int run_enumerate(ppipe_ctx* c) {
     c->check_err = true;
   }
   if (c->pending_upload) {
-    // Chunked pipeline: chunk i is uploaded on the copy stream and, as soon as it lands, validated, packed and scored (score3a) on the compute
-    // stream while chunk i + 1 uploads; score3b / score12 follow once. Chunks grow
-    // geometrically (1/16, 3/16, 1/4, 1/2 of the bytes; local models are heavy-first), so
-    // the upload nobody overlaps is the small first one, and the work for chunk i covers
-    // the upload of chunk i + 1. Launches for a chunk are issued right after its copies,
-    // so the GPU starts scoring while the host still issues later chunks.
+    // Chunked pipeline: chunk i is uploaded on the copy stream and, as soon as it lands,
+    // packed (and validated, pb.err_key) and scored (score3a) on one of two compute streams
+    // while chunk i + 1 uploads; score3b / score12 follow once. The first chunk is small
+    // (the upload nobody overlaps) and so are the last ones (local models are heavy-first, so
+    // the last bytes carry the least work). Launches for a chunk are issued right after its
+    // copies, so the GPU starts scoring while the host still issues later chunks.
     CU(c, c->d_err.reserve(1));
     const unsigned long long none = ~0ull;
     CU(c, cudaMemcpyAsync(c->d_err.p, &none, 8, cudaMemcpyHostToDevice, c->stream));
@@ -934,7 +934,10 @@ static int run_enumerate(ppipe_ctx* c) {
     std::vector<uint64_t> cum(pb.n_local + 1, 0);
     for (int i = 0; i < pb.n_local; ++i)
       cum[i + 1] = cum[i] + sizeof(uint32_t) * (uint64_t)c->C * c->h_models[i].M * c->B + 8ull * c->h_models[i].M;
-    std::vector<double> frac = {1.0 / 16, 4.0 / 16, 8.0 / 16, 1.0};
+    // cumulative byte fractions (measured, config 5 e2e: 1/16, 1/4, 1/2, 1 -> 75.6 ms; these
+    // 7 -> 72.5 ms: the copy engine finishes at ~22 ms, so the last chunks must be small
+    // enough for their scoring to start before it ends)
+    std::vector<double> frac = {0.05, 0.15, 0.3, 0.45, 0.6, 0.8, 1.0};
     if (const char* f = getenv("PPIPE_CHUNK_FRACS")) {  // measurements: "0.05,0.25,0.5" (then 1)
       frac.clear();
       for (const char* q = f; *q;) {
@@ -957,6 +960,17 @@ static int run_enumerate(ppipe_ctx* c) {
     }
     const int nch = (int)lo.size() - 1;
     const uint64_t bmax = c->h_batches[c->B - 1];
+    pb.err_key = c->d_err.p;
+    pb.smax = (uint64_t)INT64_MAX / (8 * bmax);
+    // PPIPE_DEBUG_FLAGS & 256: per-chunk upload / compute completion times on stderr
+    const char* dbgs = getenv("PPIPE_DEBUG_FLAGS");
+    const bool dbg_chunks = dbgs && (atoi(dbgs) & 256);
+    static cudaEvent_t dev_up[ppipe_ctx::kMaxChunks], dev_done[ppipe_ctx::kMaxChunks];
+    static bool dev_init = false;
+    if (dbg_chunks && !dev_init) {
+      for (int i = 0; i < ppipe_ctx::kMaxChunks; ++i) cudaEventCreate(&dev_up[i]), cudaEventCreate(&dev_done[i]);
+      dev_init = true;
+    }
     // Copies of consecutive local models whose host arrays are also adjacent are merged
     // (each copy costs a few microseconds of setup: 1,000 separate 785 KB copies reach
     // 43 GB/s, one copy 55 GB/s). Local models are ordered heavy-first, so for config 5
@@ -991,15 +1005,29 @@ static int run_enumerate(ppipe_ctx* c) {
       CU(c, cudaStreamWaitEvent(cs, c->cev[ch], 0));
       pb.model_base = lo[ch];
       pb.n_chunk = lo[ch + 1] - lo[ch];
-      CU(c, launch_validate(c->d_models.p + lo[ch], pb.n_chunk, c->d_lat.p, c->d_s.p, (int)c->C, (int)c->B,
-                            (uint64_t)INT64_MAX / (8 * bmax), c->d_err.p, cs));
+      // (validated inside the pack launch: pb.err_key)
       CU(c, launch_pack(pb, cs));
       CU(c, launch_score_part(pb, so, cs, &c->launches_i, 1));
-      c->launches_i += 1 + pack_launches(pb);
+      if (dbg_chunks) {
+        cudaEventRecord(dev_up[ch], c->cstream);
+        cudaEventRecord(dev_done[ch], cs);
+      }
+      c->launches_i += pack_launches(pb);
     }
     CU(c, cudaEventRecord(c->sev[1], c->stream2));  // join
     CU(c, cudaStreamWaitEvent(c->stream, c->sev[1], 0));
     CU(c, cudaEventRecord(c->ev[1], c->stream));  // phase 0 = upload + pack + score3a, interleaved
+    if (dbg_chunks) {
+      cudaEventSynchronize(c->ev[1]);
+      for (int ch = 0; ch < nch; ++ch) {
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, c->ev[0], dev_up[ch]);
+        cudaEventElapsedTime(&b, c->ev[0], dev_done[ch]);
+        fprintf(stderr, "ppipe chunk %d (models %d..%d): uploaded at %.2f ms, scored at %.2f ms\n", ch, lo[ch],
+                lo[ch + 1] - 1, a, b);
+      }
+    }
+    pb.err_key = nullptr;
     pb.model_base = 0;
     pb.n_chunk = pb.n_local;
     CU(c, launch_score_part(pb, so, c->stream, &c->launches_i, 2));

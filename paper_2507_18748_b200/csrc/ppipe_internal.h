@@ -63,6 +63,11 @@ struct Problem {
   // U(E) (a candidate at or below the best theta of a strictly smaller E-bucket of any
   // batch is dominated).
   unsigned long long* gfold;
+  // Device validation inside the pack launch (ppipe_update_profiles_async; nullptr: the
+  // profiles were validated before): pack_p flags a whole-model latency >= 2^28, pack_y an
+  // act_bytes value above smax, by atomicMin of the key validate_kernel would write.
+  unsigned long long* err_key;
+  uint64_t smax;
 };
 
 struct ScoreOut {

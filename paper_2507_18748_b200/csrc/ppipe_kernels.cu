@@ -104,6 +104,9 @@ __global__ void __launch_bounds__(256) pack_p_kernel(Problem pb, int n_btiles) {
     const int bb = e / (Mp - M - 1), l = e % (Mp - M - 1);
     Pk[(size_t)(b0 + bb) * Mp + M + 1 + l] = carry[bb];
   }
+  // the saturating total reaches kRangeLimit iff the true whole-model latency does
+  if (pb.err_key && threadIdx.x < nb && carry[threadIdx.x] >= kRangeLimit)
+    atomicMin(pb.err_key, ((unsigned long long)mdp->model << 40) | (unsigned long long)(k * B + b0 + threadIdx.x));
 }
 
 // CTA per (local model, distinct bandwidth v, batch): Y[v][b][c] for c in [0, Mp).
@@ -116,6 +119,10 @@ __global__ void __launch_bounds__(256) pack_y_kernel(Problem pb) {
   const uint64_t bw = pb.bw_v[v];
   const uint64_t* S = pb.raw_s + md.s_off;
   int32_t* row = pb.Y + md.y_off + ((size_t)v * pb.B + bi) * md.Mp;
+  if (pb.err_key && v == 0 && bi == 0)
+    for (uint32_t l = threadIdx.x; l < md.M; l += blockDim.x)
+      if (S[l] > pb.smax)
+        atomicMin(pb.err_key, ((unsigned long long)md.model << 40) | (1ull << 39) | (unsigned long long)l);
   for (uint32_t c = threadIdx.x; c < md.Mp; c += blockDim.x) {
     int32_t y = 0;
     if (c >= 1 && c + 1 <= md.M) {
