@@ -1167,6 +1167,13 @@ static int merge_assemble(ppipe_ctx* c, const std::vector<uint64_t>& cnts, uint6
   CU(c, c->d_merged.reserve(std::max<uint64_t>(n_dirty, 1)));
   uint64_t n_merged = 0;
   std::vector<uint64_t> mcount(straddle.size(), 0);
+  const char* dbgs_ = getenv("PPIPE_DEBUG_FLAGS");
+  const bool mdbg = dbgs_ && (atoi(dbgs_) & 32);
+  cudaEvent_t aev[4] = {};
+  if (mdbg) {
+    for (auto& x : aev) cudaEventCreate(&x);
+    cudaEventRecord(aev[0], c->stream);
+  }
   if (n_dirty) {
     CU(c, frontier_pass(c->d_union.p, n_dirty, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_merged.p,
                         c->d_segoff_final.p, &n_merged, &c->scratch, c->stream, nl, c->wpack));
@@ -1180,6 +1187,7 @@ static int merge_assemble(ppipe_ctx* c, const std::vector<uint64_t>& cnts, uint6
     CU(c, cudaStreamSynchronize(c->stream));
     for (size_t i = 0; i < straddle.size(); ++i) mcount[i] = b[2 * i + 1] - b[2 * i];
   }
+  if (mdbg) cudaEventRecord(aev[1], c->stream);
   // assemble in order: clean pieces from the gathered frontiers, each straddling
   // model's merged block in place of its first piece
   uint64_t w = 0, moff = 0;
@@ -1198,9 +1206,21 @@ static int merge_assemble(ppipe_ctx* c, const std::vector<uint64_t>& cnts, uint6
     w += n;
   }
   *n_pts = w;
+  if (mdbg) cudaEventRecord(aev[2], c->stream);
   CU(c, c->d_segtmp.reserve(std::max<uint64_t>(w, 1)));
   CU(c, segment_offsets(c->d_final.p, w, c->d_segbase.p, (int)c->C, c->n_seg_total, c->d_segoff_final.p,
                         c->d_segtmp.p, c->stream, nl));
+  if (mdbg) {
+    cudaEventRecord(aev[3], c->stream);
+    cudaEventSynchronize(aev[3]);
+    float a = 0, b = 0, d = 0;
+    cudaEventElapsedTime(&a, aev[0], aev[1]);
+    cudaEventElapsedTime(&b, aev[1], aev[2]);
+    cudaEventElapsedTime(&d, aev[2], aev[3]);
+    fprintf(stderr, "ppipe assemble rank %d: straddlers (%llu records) %.3f ms, concat %.3f ms, offsets %.3f ms\n",
+            c->rank, (unsigned long long)n_dirty, a, b, d);
+    for (auto& x : aev) cudaEventDestroy(x);
+  }
   return PPIPE_OK;
 }
 
