@@ -184,6 +184,13 @@ __device__ __forceinline__ Rec make_rec(uint32_t model, int K, int c1, int c2, i
   return r;
 }
 
+#ifndef PPIPE_P2_PREFILTER
+// Pass 2 scans its (short, tightened) ranges with the exact group tests only: without the
+// two per-warp 16-bit prefilter rows score3b fits 8 CTAs/SM at 128 registers without
+// spills (measured: score3b 24.0 ms with the prefilter at 7 CTAs/SM, 22.4 without at 7,
+// 20.8 without at 8). 1: the prefilter in pass 2 as well.
+#define PPIPE_P2_PREFILTER 0
+#endif
 #ifndef PPIPE_P1_FOLD_EVERY
 #define PPIPE_P1_FOLD_EVERY 4  // pass 1 folds one c2 in 4 of a hit group (1: every feasible candidate)
 #endif
@@ -203,6 +210,7 @@ constexpr int kUUnrollP1 = PPIPE_U_UNROLL_P1, kUUnrollP2 = PPIPE_U_UNROLL_P2;
 constexpr int kScanUnroll = PPIPE_SCAN_UNROLL;  // prefilter groups per vote in the pass-1 scan
 constexpr int kWarps = 2;      // warps per CTA (share the fold tables and the staged rows)
 constexpr int kEmitBuf = 32;   // survivor records staged per warp before a global flush
+static_assert(kEmitBuf >= 32, "emit_warp appends up to one record per lane before it flushes");
 
 // Survivor output: each warp stages records in a shared-memory buffer and flushes
 // it with one global atomicAdd and coalesced 16-byte stores.
@@ -749,6 +757,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
     const long long L = (long long)bmin + 16383;
     // entries past c2_end hold n' = 0 (never pass) so that the unrolled, prefetching
     // scan below may read up to 16 values ahead
+    if (pass == 1 || PPIPE_P2_PREFILTER) {
     const int fill_end = ((c2_end + 3) & ~3) + 8 * kScanUnroll - 4;
     PPIPE_DCHECK(fill_end <= cx.row_len && c2_start >= 0);
     for (int c2 = c2_start + lane; c2 < fill_end; c2 += 32) {
@@ -771,6 +780,7 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
 #pragma unroll
     for (int q = 0; q < kQ64; ++q) thr64[q] = ((unsigned long long)thr16[2 * q + 1] << 32) | thr16[2 * q];
     __syncwarp();
+    }
   }
   // Prefilter hit bits of one aligned group of 4 c2 values (bit 15 / 31 of the result).
   auto group_bits = [&](const uint4& n4) -> unsigned {
@@ -795,7 +805,9 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
   for (int c2 = c2_start; c2 < c2_end; c2 += 4) {
     // Fast scan: two groups per iteration, one vote, next pair prefetched; stops at
     // the first group in which some lane's prefilter passes.
-    if (pass == 2) {  // short tightened ranges: one group per iteration
+    if (pass == 2 && !PPIPE_P2_PREFILTER) {
+      // no prefilter: every group goes to the exact tests below
+    } else if (pass == 2) {  // short tightened ranges: one group per iteration
 #pragma unroll 1
       for (;;) {
         if (__any_sync(FULL_MASK, group_bits(nrow[c2 >> 2]) != 0u)) break;
@@ -1033,7 +1045,7 @@ __device__ __forceinline__ ScoreSmem carve_smem(uint8_t* raw, int nb, int row_le
   m.Qs = m.Bs + row_len;
   m.Rs = m.Qs + row_len;
   m.nb16 = reinterpret_cast<uint32_t*>(m.Rs + row_len);
-  m.ebuf = reinterpret_cast<int4*>(m.nb16 + (size_t)kWarps * row_len);
+  m.ebuf = reinterpret_cast<int4*>(m.nb16 + (PPIPE_P2_PREFILTER ? (size_t)kWarps * row_len : 0));
   m.slot = reinterpret_cast<uint8_t*>(m.ebuf + kWarps * 2 * kEmitBuf);
   return m;
 }
@@ -1044,7 +1056,8 @@ template <int NC>
 static size_t score_smem_bytes(int nb, int row_len, bool pass2 = true) {
   if (!pass2)
     return ((4 * (size_t)NC * (nb + 2) + 15) & ~(size_t)15) + sizeof(int32_t) * (3 + kWarps) * (size_t)row_len;
-  const size_t base = 8 * (size_t)NC * (nb + 2) + sizeof(int32_t) * (3 + kWarps) * (size_t)row_len;
+  const size_t base =
+      8 * (size_t)NC * (nb + 2) + sizeof(int32_t) * (3 + (PPIPE_P2_PREFILTER ? kWarps : 0)) * (size_t)row_len;
   return base + (size_t)kWarps * kEmitBuf * 32 + (size_t)kWarps * slot_bytes<NC>();
 }
 
@@ -1272,7 +1285,7 @@ __global__ void __launch_bounds__(32 * kWarps, PPIPE_12_CTAS_PER_SM)
 #endif
 constexpr int k3aCtasPerSm = PPIPE_3A_CTAS_PER_SM;
 #ifndef PPIPE_3B_CTAS_PER_SM
-#define PPIPE_3B_CTAS_PER_SM 7
+#define PPIPE_3B_CTAS_PER_SM 8
 #endif
 constexpr int k3bCtasPerSm = PPIPE_3B_CTAS_PER_SM;  // pass 2 holds more live state: fewer, fatter warps
 template <int NC, bool W>
