@@ -1281,15 +1281,17 @@ __global__ void __launch_bounds__(32 * kWarps, PPIPE_12_CTAS_PER_SM)
 // bucket-best tables of each (k_2, k_3, b) unit; units with a feasible candidate
 // are "hot": their finalized tables go to global memory for kernel 3. ----
 #ifndef PPIPE_3A_CTAS_PER_SM
-#define PPIPE_3A_CTAS_PER_SM 9  // 94 registers, no spills (measured: 8 -> 9 CTAs/SM, score3a 32.3 -> 32.0 ms)
+#define PPIPE_3A_CTAS_PER_SM 10  // <= 102 registers, no spills; 10 x 23.1 KB of shared memory fit (measured: 8 / 9 / 10 CTAs/SM, score3a 32.3 / 32.0 / 31.2 ms)
 #endif
-constexpr int k3aCtasPerSm = PPIPE_3A_CTAS_PER_SM;
+// (more than 5 classes: 8, where the larger slot arrays need 128 registers without spills)
+template <int NC>
+constexpr int k3aCtasPerSm() { return NC <= 5 ? PPIPE_3A_CTAS_PER_SM : 8; }
 #ifndef PPIPE_3B_CTAS_PER_SM
 #define PPIPE_3B_CTAS_PER_SM 8
 #endif
 constexpr int k3bCtasPerSm = PPIPE_3B_CTAS_PER_SM;  // pass 2 holds more live state: fewer, fatter warps
 template <int NC, bool W>
-__global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm)
+__global__ void __launch_bounds__(32 * kWarps, k3aCtasPerSm<NC>())
     score3a_kernel(Problem pb, ScoreOut out, int nb_log2, int row_len) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ int s_tile;
