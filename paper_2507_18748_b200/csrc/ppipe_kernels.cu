@@ -870,13 +870,16 @@ __device__ void k3_tile(const CtaCtx<NC>& cx, int k3, int c1_base, int c1_lo, in
     const int4 r4 = *reinterpret_cast<const int4*>(Rs + c2);
     // Some lane passed at some c2 of the group. Slot j of this lane is a real
     // pair iff 32 j + lane < c2 - c1_base.
+    // pass 2 runs this loop rolled: its per-c2 values come from shared memory and a hit
+    // mask instead of select chains over the group's registers
+    const unsigned hm = (h0 != 0 ? 1u : 0u) | (h1 != 0 ? 2u : 0u) | (h2 != 0 ? 4u : 0u) | (h3 != 0 ? 8u : 0u);
 #pragma unroll(pass == 1 ? kUUnrollP1 : kUUnrollP2)
     for (int u = 0; u < 4; ++u) {
-      const int hu = u == 0 ? h0 : (u == 1 ? h1 : (u == 2 ? h2 : h3));
+      const int hu = pass == 2 ? (int)((hm >> u) & 1u) : (u == 0 ? h0 : (u == 1 ? h1 : (u == 2 ? h2 : h3)));
       if (!__any_sync(FULL_MASK, hu)) continue;
-      const int Bv = u == 0 ? b4.x : (u == 1 ? b4.y : (u == 2 ? b4.z : b4.w));
-      const int Q = u == 0 ? q4.x : (u == 1 ? q4.y : (u == 2 ? q4.z : q4.w));
-      const int R = u == 0 ? r4.x : (u == 1 ? r4.y : (u == 2 ? r4.z : r4.w));
+      const int Bv = pass == 2 ? Bs[c2 + u] : (u == 0 ? b4.x : (u == 1 ? b4.y : (u == 2 ? b4.z : b4.w)));
+      const int Q = pass == 2 ? Qs[c2 + u] : (u == 0 ? q4.x : (u == 1 ? q4.y : (u == 2 ? q4.z : q4.w)));
+      const int R = pass == 2 ? Rs[c2 + u] : (u == 0 ? r4.x : (u == 1 ? r4.y : (u == 2 ? r4.z : r4.w)));
       const int relu = rel + u;
       if (pass == 1 && (u % PPIPE_P1_FOLD_EVERY) != 0) {
         // count only: the fold takes one c2 of every PPIPE_P1_FOLD_EVERY of a hit group.
